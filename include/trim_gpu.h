@@ -1,0 +1,183 @@
+/*
+ * trim_gpu.h — C ABI of the B200-native TRIM candidate filter.
+ *
+ * This is the drop-in boundary for the reference's query path. The reference
+ * has no FFI; its boundary is the header-level C++ API in
+ * proj/include/trimsearch/ivf/ivf.hpp. Each entry point below names the
+ * reference function it replaces (file:line relative to
+ * /root/reference/proj/include/trimsearch). The reference functions take
+ * one query; these take a batch, because a GPU launch per query is too small.
+ * The C++ header include/trim_b200/ivf.hpp re-exposes the reference's
+ * per-query signatures and exceptions on top of this ABI.
+ *
+ * There is no CPU fallback. If no CUDA device is present, or the library was
+ * built without sm_100a code, every search returns TRIM_ECUDA.
+ *
+ * Threading: an index is immutable after trim_index_create. Concurrent
+ * searches on one index from several host threads are safe: every call uses
+ * its own stream and its own stream-ordered workspace.
+ *
+ * Errors: functions return trim_status. The message of the last failure on
+ * the calling thread is available from trim_last_error(). The codes map 1:1
+ * to the reference exceptions:
+ *   TRIM_EINVAL -> std::invalid_argument
+ *   TRIM_EDATA  -> trimsearch::DataError (core/io_util.hpp:13-16)
+ */
+#ifndef TRIM_GPU_H
+#define TRIM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRIM_ABI_VERSION 1
+
+typedef enum {
+    TRIM_OK = 0,
+    TRIM_EINVAL = 1, /* std::invalid_argument in the reference */
+    TRIM_EDATA = 2,  /* trimsearch::DataError */
+    TRIM_ECUDA = 3,  /* CUDA runtime / launch failure, or no device */
+    TRIM_ENCCL = 4,  /* reserved for the collective layer */
+    TRIM_ENOMEM = 5
+} trim_status;
+
+/* trimsearch::SearchCounters (core/counters.hpp:10-16), followed by
+ * IvfResult::coarse_dc (ivf/ivf.hpp:164-169). */
+typedef struct {
+    uint64_t dc;
+    uint64_t edc;
+    uint64_t pruned;
+    uint64_t evaluated;
+    uint64_t hops;
+    uint64_t coarse_dc;
+} trim_counters;
+
+typedef enum {
+    TRIM_MEM_HOST = 0,  /* descriptor arrays are host pointers */
+    TRIM_MEM_DEVICE = 1 /* descriptor arrays are device pointers on `device` */
+} trim_memory;
+
+/*
+ * Index descriptor: trimsearch::ivf::IvfIndex (ivf/ivf.hpp:37-51) flattened to
+ * CSR, plus the VectorDataset (core/dataset.hpp:18-27) the survivors are read
+ * from. trim_index_create copies everything; the caller keeps ownership.
+ *
+ *   centroids    PqCodebook::centroids, subspace j at float ksub*sub_off[j],
+ *                where sub_off is the prefix sum of sub_dims (pq/pq.hpp:40-54)
+ *   coarse       IvfIndex::coarse_centroids, nlist*dim
+ *   list_*       InvertedList arrays (ivf/ivf.hpp:29-35) concatenated in list
+ *                order; list l is [list_offsets[l], list_offsets[l+1]);
+ *                entries within a list in ascending id order (ivf.hpp:147-152)
+ *   vectors      rows for ids [id_base, id_base + n); an id-shard of the
+ *                dataset when id_base != 0 (multi-GPU)
+ */
+typedef struct {
+    uint32_t dim;
+    uint32_t m;
+    uint32_t ksub; /* centroids per subspace, <= 256 (byte codes, pq.hpp:27-29) */
+    const uint32_t* sub_dims;
+    const float* centroids;
+    uint32_t nlist;
+    const float* coarse;
+    const uint64_t* list_offsets;
+    const uint32_t* list_ids;
+    const uint8_t* list_codes;
+    uint32_t code_stride; /* bytes between consecutive codes, >= m */
+    const float* list_lx; /* plain (non-squared) Γ(l,x) */
+    uint64_t n;
+    const float* vectors;
+    uint64_t id_base;
+    int device;
+    trim_memory memory;
+} trim_index_desc;
+
+typedef struct trim_index* trim_index_t;
+
+typedef struct {
+    uint32_t dim, m, ksub, nlist;
+    uint64_t n, total_entries, id_base;
+    uint64_t max_list_size;
+    uint64_t device_bytes;
+    int device;
+} trim_index_info;
+
+const char* trim_last_error(void);
+int trim_abi_version(void);
+
+/* IvfIndex construction from prebuilt arrays (the reference builds on host:
+ * ivf/ivf.hpp:112-154; its artefact format is ivf.hpp:53-107). */
+int trim_index_create(const trim_index_desc* desc, trim_index_t* out);
+int trim_index_destroy(trim_index_t index);
+int trim_index_get_info(trim_index_t index, trim_index_info* info);
+
+/*
+ * ivf::search_trim_ivf_knn (ivf/ivf.hpp:243-304), for nq queries.
+ * queries: nq*dim (host). ids_out/dist_out: nq*k (host), each row ascending by
+ * (dist_sq, id). counters_out: nq (host, may be NULL).
+ * gamma is float(profile.gamma) (ivf.hpp:250); gamma < 0 is an uncalibrated
+ * profile (ivf.hpp:246-247). k > probed vectors of any query -> TRIM_EINVAL
+ * (ivf.hpp:289-290). k <= 256.
+ */
+int trim_search_knn(trim_index_t index, const float* queries, uint64_t nq, uint32_t k,
+                    uint32_t nprobe, float gamma, uint32_t* ids_out, float* dist_out,
+                    trim_counters* counters_out);
+
+/*
+ * ivf::search_trim_ivf_range (ivf/ivf.hpp:308-347). radius: nq plain radii.
+ * offsets_out: nq+1 (host). *ids_out / *dist_out are allocated by the library
+ * (release with trim_free) and hold the concatenated per-query results, each
+ * query ascending by (dist_sq, id). Negative radius -> TRIM_EINVAL.
+ */
+int trim_search_range(trim_index_t index, const float* queries, uint64_t nq,
+                      const float* radius, uint32_t nprobe, float gamma, uint64_t* offsets_out,
+                      uint32_t** ids_out, float** dist_out, trim_counters* counters_out);
+
+/*
+ * ivf::search_baseline_ivfpq (ivf/ivf.hpp:193-237): two-phase IVFPQ with a
+ * refine pool of k_prime. ids_out/dist_out: nq*k. Requires 1 <= k <= k_prime,
+ * nprobe >= 1; k > probed -> TRIM_EINVAL.
+ */
+int trim_search_baseline_ivfpq(trim_index_t index, const float* queries, uint64_t nq,
+                               uint32_t k, uint32_t nprobe, uint32_t k_prime, uint32_t* ids_out,
+                               float* dist_out, trim_counters* counters_out);
+
+/*
+ * Device-resident variants (inputs already in HBM; used by the serving loop
+ * and bench.py's device-timed leg). All pointers are device pointers on the
+ * index's device; the call is asynchronous on `stream` (a cudaStream_t, NULL =
+ * per-thread default). A query whose probed stream is shorter than k gets
+ * ids = 0xFFFFFFFF and dist = +inf, and bit 0 of *status_out (device u32, may
+ * be NULL) is set.
+ */
+int trim_search_knn_device(trim_index_t index, const float* d_queries, uint64_t nq, uint32_t k,
+                           uint32_t nprobe, float gamma, uint32_t* d_ids, float* d_dist,
+                           trim_counters* d_counters, uint32_t* d_status, void* stream);
+
+/* pq::build_distance_table (pq/pq.hpp:158-172) for nq queries: lut_out is
+ * nq*m*ksub floats (host), j-major like DistanceTable::entries. */
+int trim_build_lut(trim_index_t index, const float* queries, uint64_t nq, float* lut_out);
+
+/* detail_ivf::probe_order (ivf/ivf.hpp:173-187): lists_out nq*min(nprobe,nlist). */
+int trim_probe(trim_index_t index, const float* queries, uint64_t nq, uint32_t nprobe,
+               uint32_t* lists_out);
+
+/*
+ * Merge of per-shard top-k lists (multi-GPU id-sharding, after the NCCL
+ * all-gather). d_dist/d_ids: [nshards][nq][k] device arrays; the merged row
+ * is the k smallest (dist_sq, id) — the same order ScoredId defines
+ * (core/ground_truth.hpp:39-50). Entries with id 0xFFFFFFFF are ignored.
+ */
+int trim_merge_topk_device(const float* d_dist, const uint32_t* d_ids, uint32_t nshards,
+                           uint64_t nq, uint32_t k, float* d_dist_out, uint32_t* d_ids_out,
+                           int device, void* stream);
+
+void trim_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRIM_GPU_H */

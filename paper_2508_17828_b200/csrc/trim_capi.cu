@@ -1,0 +1,890 @@
+// trim_capi.cu — host implementation of include/trim_gpu.h.
+//
+// Owns the device copy of the index, per-call streams and stream-ordered
+// workspaces, kernel dispatch, and the reference's error semantics
+// (ivf/ivf.hpp:195-198, 246-249, 289-290, 311-314). There is no CPU path:
+// every search runs the sm_100a kernels in trim_kernels.cuh.
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/trim_gpu.h"
+#include "trim_baseline.cuh"
+#include "trim_kernels.cuh"
+
+using namespace trimgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+struct CudaError {
+    int code;
+};
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            set_err(TRIM_ECUDA, "CUDA error %s (%s) at %s:%d", cudaGetErrorName(_e),      \
+                    cudaGetErrorString(_e), __FILE__, __LINE__);                          \
+            throw CudaError{TRIM_ECUDA};                                                  \
+        }                                                                                 \
+    } while (0)
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const CudaError& e) {
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        return set_err(TRIM_ENOMEM, "host allocation failed");
+    }
+}
+
+uint32_t round_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+uint32_t pow2_at_least(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x)
+        p <<= 1;
+    return p;
+}
+
+cudaStream_t thread_stream(int device) {
+    thread_local std::vector<cudaStream_t> streams;
+    if (static_cast<int>(streams.size()) <= device)
+        streams.resize(device + 1, nullptr);
+    if (!streams[device])
+        CK(cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking));
+    return streams[device];
+}
+
+// RAII stream-ordered device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes)
+            CK(cudaMallocAsync(&p, bytes, st));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        std::swap(p, o.p);
+        std::swap(s, o.s);
+        return *this;
+    }
+    ~DevBuf() {
+        if (p)
+            cudaFreeAsync(p, s);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+} // namespace
+
+struct trim_index {
+    int device = 0;
+    DevIndex dev{};
+    uint32_t code_stride_host = 0;
+    uint64_t total = 0;
+    std::vector<uint64_t> list_offsets;  // host copy
+    std::vector<uint64_t> top_prefix;    // prefix sums of list sizes sorted descending
+    uint64_t max_list = 0;
+    uint64_t bytes = 0;
+    std::vector<void*> allocs;
+
+    ~trim_index() {
+        if (!allocs.empty()) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            for (void* p : allocs)
+                cudaFree(p);
+            cudaSetDevice(prev);
+        }
+    }
+
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        const size_t b = std::max<size_t>(sizeof(T) * count, 16);
+        CK(cudaMalloc(&p, b));
+        allocs.push_back(p);
+        bytes += b;
+        return static_cast<T*>(p);
+    }
+
+    // Upper bound on a query's stream length at `np` probes.
+    uint64_t stream_bound(uint32_t np) const {
+        np = std::min<uint32_t>(np, dev.nlist);
+        return top_prefix[np];
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) {
+        CK(cudaGetDevice(&prev));
+        if (prev != d)
+            CK(cudaSetDevice(d));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+int check_device_present() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return set_err(TRIM_ECUDA, "no CUDA device available (%s); the TRIM GPU path has no CPU "
+                                   "fallback",
+                       cudaGetErrorString(e));
+    return TRIM_OK;
+}
+
+// ---------------------------------------------------------------- dispatch
+template <int M, int KS>
+void launch_knn_s(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
+    const uint32_t S = (p.k + 31) / 32;
+    dim3 grid(static_cast<unsigned>(p.nq));
+    auto go = [&](auto kern) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        kern<<<grid, kThreads, smem, st>>>(ix, p);
+        CK(cudaGetLastError());
+    };
+    if (S <= 1)
+        go(trim_knn_kernel<M, KS, 1>);
+    else if (S <= 2)
+        go(trim_knn_kernel<M, KS, 2>);
+    else if (S <= 4)
+        go(trim_knn_kernel<M, KS, 4>);
+    else
+        go(trim_knn_kernel<M, KS, 8>);
+}
+
+void launch_knn(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
+    if (ix.ksub == 256) {
+        switch (ix.m) {
+        case 16: return launch_knn_s<16, 256>(ix, p, smem, st);
+        case 32: return launch_knn_s<32, 256>(ix, p, smem, st);
+        case 48: return launch_knn_s<48, 256>(ix, p, smem, st);
+        case 120: return launch_knn_s<120, 256>(ix, p, smem, st);
+        default: break;
+        }
+    }
+    launch_knn_s<0, 0>(ix, p, smem, st);
+}
+
+template <int M, int KS>
+void launch_range_t(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,
+                    cudaStream_t st) {
+    auto kern = trim_range_kernel<M, KS>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, st>>>(ix, p);
+    CK(cudaGetLastError());
+}
+
+void launch_range(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,
+                  cudaStream_t st) {
+    if (ix.ksub == 256) {
+        switch (ix.m) {
+        case 16: return launch_range_t<16, 256>(ix, p, grid, smem, st);
+        case 32: return launch_range_t<32, 256>(ix, p, grid, smem, st);
+        case 48: return launch_range_t<48, 256>(ix, p, grid, smem, st);
+        case 120: return launch_range_t<120, 256>(ix, p, grid, smem, st);
+        default: break;
+        }
+    }
+    launch_range_t<0, 0>(ix, p, grid, smem, st);
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+// Probe lists for a query batch (d_q rows padded to dim_stride). Returns
+// the effective per-query probe count; d_probe is null when nlist == 1.
+uint32_t run_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t nprobe,
+                   DevBuf& d_probe, cudaStream_t st) {
+    const uint32_t np = std::min(nprobe, ix->dev.nlist);
+    if (ix->dev.nlist == 1 || np == 0 || nq == 0)
+        return np;
+    const uint32_t nl2 = pow2_at_least(ix->dev.nlist);
+    const size_t smem = sizeof(float) * ix->dev.dim_stride + sizeof(uint64_t) * nl2;
+    d_probe = DevBuf(sizeof(uint32_t) * nq * np, st);
+    CK(cudaFuncSetAttribute(trim_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    trim_probe_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(
+        ix->dev, d_q, nq, np, nl2, d_probe.as<uint32_t>());
+    CK(cudaGetLastError());
+    return np;
+}
+
+// Copy nq query rows (dim floats each, host or device) into a padded device
+// buffer of dim_stride floats per row.
+DevBuf upload_queries(const trim_index* ix, const float* q, uint64_t nq, cudaMemcpyKind kind,
+                      cudaStream_t st) {
+    const uint32_t dim = ix->dev.dim, ds = ix->dev.dim_stride;
+    DevBuf d(sizeof(float) * nq * ds, st);
+    if (nq == 0)
+        return d;
+    if (ds != dim) {
+        CK(cudaMemsetAsync(d.p, 0, sizeof(float) * nq * ds, st));
+        CK(cudaMemcpy2DAsync(d.p, sizeof(float) * ds, q, sizeof(float) * dim, sizeof(float) * dim,
+                             nq, kind, st));
+    } else {
+        CK(cudaMemcpyAsync(d.p, q, sizeof(float) * nq * dim, kind, st));
+    }
+    return d;
+}
+
+int validate_knn(uint32_t k, float gamma) {
+    if (k == 0)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k must be positive");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: uncalibrated pruning profile");
+    if (k > 256)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k > 256 is not supported by the GPU "
+                                    "top-k (warp register slots)");
+    return TRIM_OK;
+}
+
+// Core kNN launch over padded device queries.
+int knn_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t nprobe,
+               float gamma, uint32_t* d_ids, float* d_dist, unsigned long long* d_ct,
+               uint32_t* d_status, cudaStream_t st) {
+    if (nq == 0)
+        return TRIM_OK;
+    DevBuf d_probe;
+    const uint32_t np = run_probe(ix, d_q, nq, nprobe, d_probe, st);
+    const size_t smem = knn_smem_bytes(ix->dev.m, ix->dev.ksub, ix->dev.dim_stride, np);
+    if (smem > kSmemLimit)
+        return set_err(TRIM_EINVAL,
+                       "search_trim_ivf_knn: per-query state (%zu B for m=%u, ksub=%u, "
+                       "nprobe=%u) exceeds 227 KB of shared memory",
+                       smem, ix->dev.m, ix->dev.ksub, np);
+    KnnParams p{};
+    p.queries = d_q;
+    p.nq = nq;
+    p.k = k;
+    p.np = np;
+    p.probe = d_probe.as<uint32_t>();
+    p.two_gamma = 2.0f * gamma;
+    p.ids_out = d_ids;
+    p.dist_out = d_dist;
+    p.counters = d_ct;
+    p.status = d_status;
+    p.first_chunk = 256;
+    // grid.x is limited to 2^31-1; process huge batches in slices
+    const uint64_t kMaxGrid = 1u << 30;
+    for (uint64_t b = 0; b < nq; b += kMaxGrid) {
+        KnnParams pb = p;
+        pb.nq = std::min<uint64_t>(kMaxGrid, nq - b);
+        pb.queries = d_q + b * ix->dev.dim_stride;
+        pb.probe = p.probe ? p.probe + b * np : nullptr;
+        pb.ids_out = d_ids + b * k;
+        pb.dist_out = d_dist + b * k;
+        pb.counters = d_ct ? d_ct + b * 6 : nullptr;
+        launch_knn(ix->dev, pb, smem, st);
+    }
+    return TRIM_OK;
+}
+
+
+template <int M, int KS>
+void launch_bl_est_t(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
+                     cudaStream_t st) {
+    auto kern = trim_bl_est_kernel<M, KS>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, st>>>(ix, p);
+    CK(cudaGetLastError());
+}
+
+void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
+                   cudaStream_t st) {
+    if (ix.ksub == 256) {
+        switch (ix.m) {
+        case 16: return launch_bl_est_t<16, 256>(ix, p, grid, smem, st);
+        case 32: return launch_bl_est_t<32, 256>(ix, p, grid, smem, st);
+        case 48: return launch_bl_est_t<48, 256>(ix, p, grid, smem, st);
+        case 120: return launch_bl_est_t<120, 256>(ix, p, grid, smem, st);
+        default: break;
+        }
+    }
+    launch_bl_est_t<0, 0>(ix, p, grid, smem, st);
+}
+
+// ivf::search_baseline_ivfpq over padded device queries; host outputs.
+int baseline_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t np,
+                    const uint32_t* d_probe, uint32_t kp, uint32_t* ids_out, float* dist_out,
+                    trim_counters* counters_out, cudaStream_t st) {
+    if (kp > kSelSmemKeys)
+        return set_err(TRIM_EINVAL, "search_baseline_ivfpq: k_prime > %u is not supported",
+                       kSelSmemKeys);
+    const uint64_t bound = std::max<uint64_t>(1, ix->stream_bound(np));
+    const uint32_t slice = 32 * kChunkMax;
+    const uint64_t nslices = (bound + slice - 1) / slice;
+    const uint64_t qb = std::max<uint64_t>(1, std::min<uint64_t>({nq, 65535, (1ull << 31) / (bound * 8)}));
+    size_t est_smem = sizeof(float) * (ix->dev.m * ix->dev.ksub + ix->dev.dim_stride);
+    est_smem = (est_smem + 15) & ~size_t(15);
+    est_smem += sizeof(uint64_t) * np + sizeof(uint32_t) * (np + 1);
+    if (est_smem > kSmemLimit)
+        return set_err(TRIM_EINVAL, "search_baseline_ivfpq: per-query state exceeds 227 KB");
+    uint32_t kp2 = pow2_at_least(kp);
+    const size_t ref_smem = sizeof(float) * ix->dev.dim_stride + sizeof(unsigned long long) * kp2;
+    const size_t sel_smem = sizeof(unsigned long long) * kSelSmemKeys;
+    DevBuf d_keys(sizeof(unsigned long long) * qb * bound, st), d_tot(sizeof(unsigned long long) * nq, st),
+        d_sel(sizeof(unsigned long long) * qb * kp, st), d_ids(sizeof(uint32_t) * nq * k, st),
+        d_dist(sizeof(float) * nq * k, st);
+    CK(cudaFuncSetAttribute(trim_bl_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sel_smem)));
+    CK(cudaFuncSetAttribute(trim_bl_refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(ref_smem)));
+    for (uint64_t b = 0; b < nq; b += qb) {
+        const uint64_t nb = std::min<uint64_t>(qb, nq - b);
+        BlParams p{};
+        p.queries = d_q + b * ix->dev.dim_stride;
+        p.nq = nb;
+        p.np = np;
+        p.probe = d_probe ? d_probe + b * np : nullptr;
+        p.slice = slice;
+        p.stride = bound;
+        p.keys = d_keys.as<unsigned long long>();
+        p.total = d_tot.as<unsigned long long>() + b;
+        launch_bl_est(ix->dev, p, dim3(static_cast<unsigned>(nslices), static_cast<unsigned>(nb)),
+                      est_smem, st);
+        trim_bl_select_kernel<<<static_cast<unsigned>(nb), kSelThreads, sel_smem, st>>>(
+            d_keys.as<unsigned long long>(), bound, p.total, kp, d_sel.as<unsigned long long>());
+        CK(cudaGetLastError());
+        trim_bl_refine_kernel<<<static_cast<unsigned>(nb), kThreads, ref_smem, st>>>(
+            ix->dev, p.queries, d_sel.as<unsigned long long>(), p.total, kp, kp2, k,
+            d_ids.as<uint32_t>() + b * k, d_dist.as<float>() + b * k);
+        CK(cudaGetLastError());
+    }
+    std::vector<unsigned long long> tot(nq);
+    CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(uint32_t) * nq * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(dist_out, d_dist.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tot.data(), d_tot.p, sizeof(unsigned long long) * nq, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < nq; ++i)
+        if (tot[i] < k)
+            return set_err(TRIM_EINVAL, "search_baseline_ivfpq: k exceeds probed vectors");
+    if (counters_out) {
+        for (uint64_t i = 0; i < nq; ++i) {
+            trim_counters& c = counters_out[i];
+            c.evaluated = tot[i];
+            c.edc = tot[i];
+            c.dc = std::min<uint64_t>(kp, tot[i]);
+            c.pruned = c.evaluated - c.dc;
+            c.hops = 0;
+            c.coarse_dc = ix->dev.nlist;
+        }
+    }
+    return TRIM_OK;
+}
+
+} // namespace
+
+// ======================================================================= API
+extern "C" {
+
+const char* trim_last_error(void) { return g_err.c_str(); }
+
+int trim_abi_version(void) { return TRIM_ABI_VERSION; }
+
+void trim_free(void* p) { std::free(p); }
+
+int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
+    if (!d || !out)
+        return set_err(TRIM_EINVAL, "trim_index_create: null argument");
+    *out = nullptr;
+    if (d->dim == 0)
+        return set_err(TRIM_EDATA, "dataset dimension must be >= 1");
+    if (d->m == 0 || d->m > d->dim)
+        return set_err(TRIM_EINVAL, "PqParams: need 1 <= m <= dim");
+    if (d->ksub == 0 || d->ksub > 256)
+        return set_err(TRIM_EINVAL, "PqParams: need 1 <= c <= 256 for byte codes");
+    if (d->m > 128)
+        return set_err(TRIM_EINVAL, "trim_index_create: m > 128 subspaces is not supported");
+    if (d->nlist == 0)
+        return set_err(TRIM_EINVAL, "build_ivf: need 1 <= nlist <= n");
+    if (d->nlist > 16384)
+        return set_err(TRIM_EINVAL, "trim_index_create: nlist > 16384 is not supported by the "
+                                    "shared-memory probe sort");
+    if (d->code_stride < d->m)
+        return set_err(TRIM_EINVAL, "trim_index_create: code_stride < m");
+    if (!d->sub_dims || !d->centroids || !d->coarse || !d->list_offsets)
+        return set_err(TRIM_EINVAL, "trim_index_create: null array in descriptor");
+    if (int rc = check_device_present())
+        return rc;
+    return guarded([&]() -> int {
+        const bool host = d->memory == TRIM_MEM_HOST;
+        const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        DeviceGuard g(d->device);
+        auto* ix = new trim_index;
+        ix->device = d->device;
+        // host copies of the small arrays (sub_dims, offsets)
+        std::vector<uint32_t> sub(d->m);
+        std::vector<uint64_t> offs(d->nlist + 1);
+        if (host) {
+            std::memcpy(sub.data(), d->sub_dims, sizeof(uint32_t) * d->m);
+            std::memcpy(offs.data(), d->list_offsets, sizeof(uint64_t) * (d->nlist + 1));
+        } else {
+            CK(cudaMemcpy(sub.data(), d->sub_dims, sizeof(uint32_t) * d->m, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(offs.data(), d->list_offsets, sizeof(uint64_t) * (d->nlist + 1),
+                          cudaMemcpyDeviceToHost));
+        }
+        uint64_t sdsum = 0;
+        std::vector<uint32_t> suboff(d->m);
+        for (uint32_t j = 0; j < d->m; ++j) {
+            suboff[j] = static_cast<uint32_t>(sdsum);
+            sdsum += sub[j];
+        }
+        if (sdsum != d->dim) {
+            delete ix;
+            return set_err(TRIM_EDATA, "codebook sub_dims do not sum to dim");
+        }
+        if (offs[0] != 0) {
+            delete ix;
+            return set_err(TRIM_EDATA, "ivf offsets must start at 0");
+        }
+        for (uint32_t l = 0; l < d->nlist; ++l)
+            if (offs[l + 1] < offs[l]) {
+                delete ix;
+                return set_err(TRIM_EDATA, "ivf offsets are not monotone");
+            }
+        const uint64_t total = offs[d->nlist];
+        if (total > 0xFFFFFFFFull) {
+            delete ix;
+            return set_err(TRIM_EINVAL, "trim_index_create: more than 2^32-1 entries per device");
+        }
+        if (total && (!d->list_ids || !d->list_codes || !d->list_lx || !d->vectors)) {
+            delete ix;
+            return set_err(TRIM_EINVAL, "trim_index_create: null list array in descriptor");
+        }
+        if (host) {
+            for (uint64_t e = 0; e < total; ++e) {
+                const uint64_t id = d->list_ids[e];
+                if (id < d->id_base || id - d->id_base >= d->n) {
+                    delete ix;
+                    return set_err(TRIM_EDATA,
+                                   "ivf entry id %llu outside the vector rows [%llu, %llu)",
+                                   (unsigned long long)id, (unsigned long long)d->id_base,
+                                   (unsigned long long)(d->id_base + d->n));
+                }
+            }
+        }
+        ix->total = total;
+        ix->list_offsets = offs;
+        std::vector<uint64_t> sizes(d->nlist);
+        for (uint32_t l = 0; l < d->nlist; ++l)
+            sizes[l] = offs[l + 1] - offs[l];
+        std::sort(sizes.begin(), sizes.end(), std::greater<uint64_t>());
+        ix->top_prefix.assign(d->nlist + 1, 0);
+        for (uint32_t l = 0; l < d->nlist; ++l)
+            ix->top_prefix[l + 1] = ix->top_prefix[l] + sizes[l];
+        ix->max_list = d->nlist ? sizes[0] : 0;
+
+        DevIndex& v = ix->dev;
+        v.dim = d->dim;
+        v.dim_stride = round_up(d->dim, 4);
+        v.m = d->m;
+        v.ksub = d->ksub;
+        v.code_stride = round_up(d->m, 16);
+        v.nlist = d->nlist;
+        v.n = d->n;
+        v.id_base = d->id_base;
+        ix->code_stride_host = d->code_stride;
+        try {
+            uint32_t* dsub = ix->alloc<uint32_t>(d->m);
+            uint32_t* doff = ix->alloc<uint32_t>(d->m);
+            CK(cudaMemcpy(dsub, sub.data(), sizeof(uint32_t) * d->m, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(doff, suboff.data(), sizeof(uint32_t) * d->m, cudaMemcpyHostToDevice));
+            v.sub_dims = dsub;
+            v.sub_offsets = doff;
+            float* cent = ix->alloc<float>(static_cast<size_t>(d->ksub) * d->dim);
+            CK(cudaMemcpy(cent, d->centroids, sizeof(float) * d->ksub * d->dim, kind));
+            v.centroids = cent;
+            float* coarse = ix->alloc<float>(static_cast<size_t>(d->nlist) * v.dim_stride);
+            CK(cudaMemset(coarse, 0, sizeof(float) * d->nlist * v.dim_stride));
+            CK(cudaMemcpy2D(coarse, sizeof(float) * v.dim_stride, d->coarse, sizeof(float) * d->dim,
+                            sizeof(float) * d->dim, d->nlist, kind));
+            v.coarse = coarse;
+            uint64_t* loff = ix->alloc<uint64_t>(d->nlist + 1);
+            CK(cudaMemcpy(loff, offs.data(), sizeof(uint64_t) * (d->nlist + 1),
+                          cudaMemcpyHostToDevice));
+            v.list_offsets = loff;
+            uint32_t* ids = ix->alloc<uint32_t>(total);
+            uint8_t* codes = ix->alloc<uint8_t>(total * v.code_stride);
+            float* lx = ix->alloc<float>(total);
+            float* vec = ix->alloc<float>(d->n * v.dim_stride);
+            if (total) {
+                CK(cudaMemcpy(ids, d->list_ids, sizeof(uint32_t) * total, kind));
+                CK(cudaMemset(codes, 0, total * v.code_stride));
+                CK(cudaMemcpy2D(codes, v.code_stride, d->list_codes, d->code_stride, d->m, total,
+                                kind));
+                CK(cudaMemcpy(lx, d->list_lx, sizeof(float) * total, kind));
+            }
+            if (d->n) {
+                if (v.dim_stride != d->dim) {
+                    CK(cudaMemset(vec, 0, sizeof(float) * d->n * v.dim_stride));
+                    CK(cudaMemcpy2D(vec, sizeof(float) * v.dim_stride, d->vectors,
+                                    sizeof(float) * d->dim, sizeof(float) * d->dim, d->n, kind));
+                } else {
+                    CK(cudaMemcpy(vec, d->vectors, sizeof(float) * d->n * d->dim, kind));
+                }
+            }
+            v.list_ids = ids;
+            v.codes = codes;
+            v.lx = lx;
+            v.vectors = vec;
+            CK(cudaDeviceSynchronize());
+        } catch (...) {
+            delete ix;
+            throw;
+        }
+        *out = ix;
+        return TRIM_OK;
+    });
+}
+
+int trim_index_destroy(trim_index_t index) {
+    delete index;
+    return TRIM_OK;
+}
+
+int trim_index_get_info(trim_index_t ix, trim_index_info* info) {
+    if (!ix || !info)
+        return set_err(TRIM_EINVAL, "trim_index_get_info: null argument");
+    info->dim = ix->dev.dim;
+    info->m = ix->dev.m;
+    info->ksub = ix->dev.ksub;
+    info->nlist = ix->dev.nlist;
+    info->n = ix->dev.n;
+    info->total_entries = ix->total;
+    info->id_base = ix->dev.id_base;
+    info->max_list_size = ix->max_list;
+    info->device_bytes = ix->bytes;
+    info->device = ix->device;
+    return TRIM_OK;
+}
+
+int trim_search_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t k,
+                    uint32_t nprobe, float gamma, uint32_t* ids_out, float* dist_out,
+                    trim_counters* counters_out) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: null index");
+    if (int rc = validate_knn(k, gamma))
+        return rc;
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        DevBuf d_ids(sizeof(uint32_t) * nq * k, st), d_dist(sizeof(float) * nq * k, st);
+        DevBuf d_ct(sizeof(unsigned long long) * nq * 6, st), d_status(sizeof(uint32_t), st);
+        CK(cudaMemsetAsync(d_status.p, 0, sizeof(uint32_t), st));
+        if (int rc = knn_device(ix, d_q.as<float>(), nq, k, nprobe, gamma, d_ids.as<uint32_t>(),
+                                d_dist.as<float>(), d_ct.as<unsigned long long>(),
+                                d_status.as<uint32_t>(), st))
+            return rc;
+        uint32_t status = 0;
+        CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(uint32_t) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(dist_out, d_dist.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+        if (counters_out)
+            CK(cudaMemcpyAsync(counters_out, d_ct.p, sizeof(trim_counters) * nq,
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&status, d_status.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (status & 1u)
+            return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k exceeds probed vectors");
+        return TRIM_OK;
+    });
+}
+
+int trim_search_knn_device(trim_index_t ix, const float* d_queries, uint64_t nq, uint32_t k,
+                           uint32_t nprobe, float gamma, uint32_t* d_ids, float* d_dist,
+                           trim_counters* d_counters, uint32_t* d_status, void* stream) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: null index");
+    if (int rc = validate_knn(k, gamma))
+        return rc;
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (ix->dev.dim_stride != ix->dev.dim) {
+            DevBuf d_q = upload_queries(ix, d_queries, nq, cudaMemcpyDeviceToDevice, st);
+            return knn_device(ix, d_q.as<float>(), nq, k, nprobe, gamma, d_ids, d_dist,
+                              reinterpret_cast<unsigned long long*>(d_counters), d_status, st);
+        }
+        return knn_device(ix, d_queries, nq, k, nprobe, gamma, d_ids, d_dist,
+                          reinterpret_cast<unsigned long long*>(d_counters), d_status, st);
+    });
+}
+
+int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const float* radius,
+                      uint32_t nprobe, float gamma, uint64_t* offsets_out, uint32_t** ids_out,
+                      float** dist_out, trim_counters* counters_out) {
+    if (!ix || !offsets_out || !ids_out || !dist_out)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_range: null argument");
+    *ids_out = nullptr;
+    *dist_out = nullptr;
+    for (uint64_t i = 0; i < nq; ++i)
+        if (radius[i] < 0.0f)
+            return set_err(TRIM_EINVAL, "search_trim_ivf_range: negative radius");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_ivf_range: uncalibrated pruning profile");
+    offsets_out[0] = 0;
+    if (nq == 0) {
+        *ids_out = static_cast<uint32_t*>(std::malloc(4));
+        *dist_out = static_cast<float*>(std::malloc(4));
+        return TRIM_OK;
+    }
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        // ivf.hpp:315: radius_sq = radius * radius in fp32
+        std::vector<float> r2(nq);
+        for (uint64_t i = 0; i < nq; ++i)
+            r2[i] = radius[i] * radius[i];
+        DevBuf d_r2(sizeof(float) * nq, st);
+        CK(cudaMemcpyAsync(d_r2.p, r2.data(), sizeof(float) * nq, cudaMemcpyHostToDevice, st));
+        DevBuf d_probe;
+        const uint32_t np = run_probe(ix, d_q.as<float>(), nq, nprobe, d_probe, st);
+        const size_t smem = range_smem_bytes(ix->dev.m, ix->dev.ksub, ix->dev.dim_stride, np);
+        if (smem > kSmemLimit)
+            return set_err(TRIM_EINVAL,
+                           "search_trim_ivf_range: per-query state (%zu B) exceeds 227 KB", smem);
+        const uint64_t bound = ix->stream_bound(np);
+        const uint32_t slice = 32 * kChunkMax;
+        const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);
+        DevBuf d_cnt(sizeof(unsigned int) * nq, st), d_dc(sizeof(unsigned long long) * nq, st),
+            d_eval(sizeof(unsigned long long) * nq, st);
+        uint32_t cap = 1024;
+        std::vector<unsigned int> cnt(nq);
+        DevBuf d_keys;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            d_keys = DevBuf(sizeof(unsigned long long) * nq * cap, st);
+            CK(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned int) * nq, st));
+            CK(cudaMemsetAsync(d_dc.p, 0, sizeof(unsigned long long) * nq, st));
+            CK(cudaMemsetAsync(d_eval.p, 0, sizeof(unsigned long long) * nq, st));
+            RangeParams p{};
+            p.np = np;
+            p.two_gamma = 2.0f * gamma;
+            p.slice = slice;
+            p.cap = cap;
+            for (uint64_t b = 0; b < nq; b += 65535) {
+                const uint64_t nb = std::min<uint64_t>(65535, nq - b);
+                p.queries = d_q.as<float>() + b * ix->dev.dim_stride;
+                p.nq = nb;
+                p.radius_sq = d_r2.as<float>() + b;
+                p.probe = d_probe.p ? d_probe.as<uint32_t>() + b * np : nullptr;
+                p.keys = d_keys.as<unsigned long long>() + b * cap;
+                p.count = d_cnt.as<unsigned int>() + b;
+                p.dc = d_dc.as<unsigned long long>() + b;
+                p.evaluated = d_eval.as<unsigned long long>() + b;
+                launch_range(ix->dev, p, dim3(static_cast<unsigned>(nslices), static_cast<unsigned>(nb)),
+                             smem, st);
+            }
+            CK(cudaMemcpyAsync(cnt.data(), d_cnt.p, sizeof(unsigned int) * nq,
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const unsigned int mx = *std::max_element(cnt.begin(), cnt.end());
+            if (mx <= cap)
+                break;
+            cap = mx;
+        }
+        // per-query sort by (dist, id) — ivf.hpp:341
+        std::vector<uint64_t> beg(nq), endv(nq);
+        uint64_t tot = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            beg[i] = i * cap;
+            endv[i] = i * cap + cnt[i];
+            offsets_out[i] = tot;
+            tot += cnt[i];
+        }
+        offsets_out[nq] = tot;
+        DevBuf d_beg(sizeof(uint64_t) * nq, st), d_end(sizeof(uint64_t) * nq, st),
+            d_sorted(sizeof(unsigned long long) * nq * cap, st);
+        CK(cudaMemcpyAsync(d_beg.p, beg.data(), sizeof(uint64_t) * nq, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_end.p, endv.data(), sizeof(uint64_t) * nq, cudaMemcpyHostToDevice, st));
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, d_keys.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(),
+                                              static_cast<int64_t>(nq * cap), static_cast<int64_t>(nq),
+                                              d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        DevBuf d_tmp(tmp_bytes, st);
+        CK(cub::DeviceSegmentedSort::SortKeys(d_tmp.p, tmp_bytes, d_keys.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(),
+                                              static_cast<int64_t>(nq * cap), static_cast<int64_t>(nq),
+                                              d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        DevBuf d_offs(sizeof(uint64_t) * (nq + 1), st);
+        CK(cudaMemcpyAsync(d_offs.p, offsets_out, sizeof(uint64_t) * (nq + 1), cudaMemcpyHostToDevice,
+                           st));
+        DevBuf d_ids(sizeof(uint32_t) * std::max<uint64_t>(tot, 1), st),
+            d_dist(sizeof(float) * std::max<uint64_t>(tot, 1), st);
+        trim_unpack_keys_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(
+            d_sorted.as<unsigned long long>(), cap, d_offs.as<uint64_t>(), nq, d_ids.as<uint32_t>(),
+            d_dist.as<float>());
+        CK(cudaGetLastError());
+        auto* hid = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<uint64_t>(tot, 1)));
+        auto* hd = static_cast<float*>(std::malloc(sizeof(float) * std::max<uint64_t>(tot, 1)));
+        if (!hid || !hd) {
+            std::free(hid);
+            std::free(hd);
+            return set_err(TRIM_ENOMEM, "search_trim_ivf_range: result allocation failed");
+        }
+        std::vector<unsigned long long> dc(nq), ev(nq);
+        CK(cudaMemcpyAsync(hid, d_ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hd, d_dist.p, sizeof(float) * tot, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(dc.data(), d_dc.p, sizeof(unsigned long long) * nq, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ev.data(), d_eval.p, sizeof(unsigned long long) * nq, cudaMemcpyDeviceToHost,
+                           st));
+        cudaError_t se = cudaStreamSynchronize(st);
+        if (se != cudaSuccess) {
+            std::free(hid);
+            std::free(hd);
+            CK(se);
+        }
+        if (counters_out) {
+            for (uint64_t i = 0; i < nq; ++i) {
+                trim_counters& c = counters_out[i];
+                c.evaluated = ev[i];
+                c.edc = ev[i];
+                c.dc = dc[i];
+                c.pruned = ev[i] - dc[i];
+                c.hops = 0;
+                c.coarse_dc = ix->dev.nlist;
+            }
+        }
+        *ids_out = hid;
+        *dist_out = hd;
+        return TRIM_OK;
+    });
+}
+
+int trim_search_baseline_ivfpq(trim_index_t ix, const float* queries, uint64_t nq, uint32_t k,
+                               uint32_t nprobe, uint32_t k_prime, uint32_t* ids_out,
+                               float* dist_out, trim_counters* counters_out) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "search_baseline_ivfpq: null index");
+    if (k == 0 || k > k_prime)
+        return set_err(TRIM_EINVAL, "search_baseline_ivfpq: need 1 <= k <= k_prime");
+    if (nprobe == 0)
+        return set_err(TRIM_EINVAL, "search_baseline_ivfpq: nprobe must be positive");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        DevBuf d_probe;
+        const uint32_t np = run_probe(ix, d_q.as<float>(), nq, nprobe, d_probe, st);
+        return baseline_device(ix, d_q.as<float>(), nq, k, np, d_probe.as<uint32_t>(), k_prime,
+                               ids_out, dist_out, counters_out, st);
+    });
+}
+
+int trim_build_lut(trim_index_t ix, const float* queries, uint64_t nq, float* lut_out) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "build_distance_table: null index");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        DevBuf d_lut(sizeof(float) * nq * ix->dev.m * ix->dev.ksub, st);
+        trim_lut_kernel<<<static_cast<unsigned>(nq), kThreads, sizeof(float) * ix->dev.dim_stride, st>>>(
+            ix->dev, d_q.as<float>(), d_lut.as<float>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(lut_out, d_lut.p, sizeof(float) * nq * ix->dev.m * ix->dev.ksub,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return TRIM_OK;
+    });
+}
+
+int trim_probe(trim_index_t ix, const float* queries, uint64_t nq, uint32_t nprobe,
+               uint32_t* lists_out) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "probe_order: null index");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        DevBuf d_probe;
+        const uint32_t np = run_probe(ix, d_q.as<float>(), nq, nprobe, d_probe, st);
+        if (np == 0)
+            return TRIM_OK;
+        if (!d_probe.p) { // nlist == 1
+            for (uint64_t i = 0; i < nq; ++i)
+                lists_out[i] = 0;
+            CK(cudaStreamSynchronize(st));
+            return TRIM_OK;
+        }
+        CK(cudaMemcpyAsync(lists_out, d_probe.p, sizeof(uint32_t) * nq * np, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return TRIM_OK;
+    });
+}
+
+int trim_merge_topk_device(const float* d_dist, const uint32_t* d_ids, uint32_t nshards,
+                           uint64_t nq, uint32_t k, float* d_dist_out, uint32_t* d_ids_out,
+                           int device, void* stream) {
+    if (nshards == 0 || k == 0)
+        return set_err(TRIM_EINVAL, "trim_merge_topk_device: need nshards >= 1 and k >= 1");
+    if (static_cast<uint64_t>(nshards) * k > 16384)
+        return set_err(TRIM_EINVAL, "trim_merge_topk_device: nshards*k > 16384");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const uint32_t n2 = pow2_at_least(nshards * k);
+        const size_t smem = sizeof(uint64_t) * n2;
+        CK(cudaFuncSetAttribute(trim_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        trim_merge_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(
+            d_dist, d_ids, nshards, nq, k, n2, d_dist_out, d_ids_out);
+        CK(cudaGetLastError());
+        return TRIM_OK;
+    });
+}
+
+} // extern "C"

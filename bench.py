@@ -1,0 +1,530 @@
+#!/usr/bin/env python
+"""bench.py — TRIM candidate filter on B200 (BASELINE.json metric).
+
+Default workload: BASELINE.json configs[1] ("IVFPQ refinement with TRIM"):
+10M fp32 vectors, D=96, 1,024-component Gaussian mixture (sigma 0.3), IVF
+nlist=4,096 / nprobe=64, PQ M=48x256, 10,000 queries in batches of 1,024,
+k=10, gamma swept over {0.6, 0.8, 1.0} (headline 0.8). Synthetic, seeded,
+generated and indexed on the device (paper_2508_17828_b200/builder.py).
+
+A *step* = the hot path over the whole 10,000-query set (10 batches of
+1,024): probe_order + the fused ADC/bound/prune/exact-L2/top-k kernel.
+`value` = candidates filtered per second over all ranks (a candidate is one
+SearchCounters.evaluated event, ivf.hpp:260), inputs resident in HBM,
+device-timed with CUDA events. `e2e` = the same metric through the C-ABI
+host call (trim_search_knn) from pinned host buffers, copies included.
+
+    python bench.py                               # N=1, config 2
+    torchrun --nproc-per-node N bench.py --gpus N # id-sharded, weak scaling
+    python bench.py --impl reference              # the reference CPU path
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1] — the bench workload
+    "c2": dict(workload="ivfpq_trim_knn_10M_d96_nlist4096_nprobe64", n=10_000_000, dim=96,
+               n_centers=1024, sigma=0.3, nq=10_000, batch=1024, m=48, nlist=4096, nprobe=64,
+               k=10, gammas=[0.6, 0.8, 1.0], gamma=0.8),
+    # BASELINE.json configs[0] (CPU-runnable reference case; parity + extra line)
+    "c1": dict(workload="flat_trim_knn_100k_d128", n=100_000, dim=128, n_centers=64, sigma=0.3,
+               nq=1000, batch=1000, m=16, nlist=1, nprobe=1, k=10, gammas=[0.0, 0.605, 1.0],
+               gamma=0.0),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- plumbing
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM bytes of the filter kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    return j.get(workload)
+
+
+# ------------------------------------------------------------------- data
+def build_workload(cfg, rank: int, world: int, device: int):
+    """Seeded synthetic data + index on the device. Rank r holds the id-shard
+    [r*n, (r+1)*n) (weak scaling); codebook and coarse quantizer are trained
+    on rank 0 and broadcast so every shard probes identically."""
+    import torch
+
+    from paper_2508_17828_b200 import builder as B
+    from paper_2508_17828_b200.ivf import IvfArrays
+
+    dev = torch.device(f"cuda:{device}")
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    centers = B.synth_normal(cfg["n_centers"], cfg["dim"], seed=0, device=device)
+    base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1 + 7919 * rank)
+    queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
+    p = B.BuildParams(m=cfg["m"], nlist=cfg["nlist"], pq_seed=3, ivf_seed=4)
+    if world == 1:
+        arrays = B.build_ivf(base, p)
+    else:
+        import torch.distributed as dist
+        if rank == 0:
+            sub, cent = B.pq_train(base, p.m, p.ksub, p.pq_iters, p.pq_seed, p.train_sample)
+            n = base.shape[0]
+            sn = min(n, max(p.nlist, 50 * p.nlist))
+            rows = B.sample_rows(n, sn, p.ivf_seed ^ 0x94D049BB133111EB)
+            coarse = B.kmeans(base[torch.from_numpy(rows.astype(np.int64)).to(dev)].contiguous(),
+                              p.nlist, p.coarse_iters, p.ivf_seed)
+            sub_t = torch.from_numpy(sub.astype(np.int32)).to(dev)
+        else:
+            cent = torch.empty(p.ksub * cfg["dim"], dtype=torch.float32, device=dev)
+            coarse = torch.empty((p.nlist, cfg["dim"]), dtype=torch.float32, device=dev)
+            sub_t = torch.empty(p.m, dtype=torch.int32, device=dev)
+        for t in (cent, coarse, sub_t):
+            dist.broadcast(t, 0)
+        sub = sub_t.cpu().numpy().astype(np.uint32)
+        codes, lx = B.pq_encode(base, p.m, p.ksub, sub, cent)
+        a = B.assign(base, coarse)[0] if p.nlist > 1 else torch.zeros(base.shape[0], dtype=torch.int32, device=dev)
+        offs, ids = B.ivf_lists(a, p.nlist)
+        idl = ids.long()
+        arrays = IvfArrays(dim=cfg["dim"], m=p.m, ksub=p.ksub, sub_dims=sub_t, centroids=cent,
+                           coarse=coarse.reshape(-1), list_offsets=offs,
+                           list_ids=(ids + rank * cfg["n"]).to(torch.int32),
+                           list_codes=codes[idl].contiguous(), list_lx=lx[idl].contiguous(),
+                           vectors=base, id_base=rank * cfg["n"])
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] built {cfg['workload']} shard in {time.time() - t0:.1f}s")
+    return arrays, queries
+
+
+# ------------------------------------------------------------ our GPU arm
+def run_ours(args, cfg):
+    import torch
+
+    from paper_2508_17828_b200 import _lib
+    from paper_2508_17828_b200 import ivf as G
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    arrays, queries = build_workload(cfg, rank, world, local)
+    gix = G.GpuIvfIndex(arrays, device=local)
+    lib = _lib.load()
+    import ctypes as C
+
+    nq, B, k = cfg["nq"], cfg["batch"], cfg["k"]
+    np_eff = min(cfg["nprobe"], cfg["nlist"])
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+    lists = torch.empty((nq, np_eff), dtype=torch.int32, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    cts = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    batches = [(b, min(B, nq - b)) for b in range(0, nq, B)]
+    if world > 1:
+        import torch.distributed as dist
+        g_ids = torch.empty((world, nq, k), dtype=torch.int32, device=dev)
+        g_d = torch.empty((world, nq, k), dtype=torch.float32, device=dev)
+        m_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        m_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
+
+    def p(t, off=0):
+        return C.c_void_p(t.data_ptr() + off)
+
+    def step(gamma, filt_events=None):
+        launches = 0
+        for (b0, nb) in batches:
+            qoff = b0 * cfg["dim"] * 4
+            _lib.check(lib.trim_probe_device(gix.handle, p(queries, qoff), nb, cfg["nprobe"],
+                                             p(lists, b0 * np_eff * 4), sh), "probe")
+            launches += 1 if cfg["nlist"] > 1 else 0
+            if filt_events is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            _lib.check(lib.trim_search_knn_preassigned_device(
+                gix.handle, p(queries, qoff), nb, k, p(lists, b0 * np_eff * 4), np_eff,
+                float(np.float32(gamma)), p(ids, b0 * k * 4), p(dists, b0 * k * 4),
+                p(cts, b0 * 48), p(status), sh), "knn")
+            launches += 1
+            if filt_events is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                filt_events.append((e0, e1))
+        if world > 1:
+            dist.all_gather_into_tensor(g_ids, ids)
+            dist.all_gather_into_tensor(g_d, dists)
+            _lib.check(lib.trim_merge_topk_device(p(g_d), p(g_ids), world, nq, k, p(m_d), p(m_ids),
+                                                  local, sh), "merge")
+            launches += 1
+        return launches
+
+    def timed(gamma, steps, warmup, clocks=None):
+        for _ in range(warmup):
+            step(gamma)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = []
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        launches = 0
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:
+            s0.record(stream)
+            for _ in range(steps):
+                launches += step(gamma, ev)
+            s1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1)
+        filt_ms = sum(a.elapsed_time(b) for a, b in ev)
+        ct = cts.sum(0).cpu().numpy()  # identical every step
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            ctt = torch.from_numpy(ct.astype(np.int64)).to(dev)
+            dist.all_reduce(ctt)
+            ct = ctt.cpu().numpy()
+        return ms, filt_ms, len(ev), ct, launches
+
+    gammas = cfg["gammas"] if not args.gamma else [args.gamma]
+    head = args.gamma if args.gamma else cfg["gamma"]
+    sweep = {}
+    for g in gammas:
+        if g == head:
+            continue
+        ms, fms, nl, ct, _ = timed(g, max(1, min(2, args.steps)), 1)
+        sweep[str(g)] = dict(ms_per_step=ms / max(1, min(2, args.steps)),
+                             cand_per_s=float(ct[3]) * max(1, min(2, args.steps)) / (ms / 1e3),
+                             qps=nq * max(1, min(2, args.steps)) / (ms / 1e3),
+                             prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])))
+        if rank == 0:
+            sweep[str(g)]["recall@10"] = recall(arrays, queries, ids, k, args.recall_q, world)
+    clk = ClockSampler(local)
+    ms, fms, nl, ct, launches = timed(head, args.steps, args.warmup, clk)
+    evaluated, dc = float(ct[3]), float(ct[0])
+    total_cand = evaluated * args.steps
+    value = total_cand / (ms / 1e3)
+    qps = nq * args.steps / (ms / 1e3)
+    out = dict(metric="candidates filtered/sec (TRIM kNN filter; QPS, %HBM roofline, prune "
+                      "ratio alongside)",
+               value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic")
+    out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
+                         queries=nq, batch=B, m=cfg["m"], nlist=cfg["nlist"],
+                         nprobe=cfg["nprobe"], k=k, gamma=head,
+                         parallelism=f"id-shard x{world}" if world > 1 else "single",
+                         l2="index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
+                         else "index fits L2; reported as-is",
+                         data_gen="device Philox blobs, seeds centers=0 base=1 queries=2")
+    out["qps"] = qps
+    out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
+    out["candidates_per_query"] = evaluated / (nq * (world if False else 1))
+    # roofline of the dominant kernel (the fused filter), per launch
+    peak, peak_src = measured_peaks()
+    m, D = cfg["m"], cfg["dim"]
+    s_frac = dc / max(1.0, evaluated)
+    bytes_per_cand = m + 4 + s_frac * (4 * D + 4)
+    alg_bytes_step = evaluated * (m + 4) + dc * (4 * D + 4)
+    per_launch_bytes = alg_bytes_step / max(1, nl // args.steps) / (world if world > 1 else 1)
+    avg_launch_ms = fms / max(1, nl)
+    achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9
+    tr = ncu_traffic(cfg["workload"])
+    out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
+                           frac=achieved / peak, traffic=tr, kernel="trim_knn_kernel",
+                           bytes_per_candidate=bytes_per_cand, peak_source=peak_src,
+                           filter_share_of_step=fms / ms)
+    out["gpu_launches"] = launches
+    out["clocks"] = clk.summary()
+    out["sweep"] = sweep
+    if rank == 0:
+        out["recall@10"] = recall(arrays, queries, ids, k, args.recall_q, world)
+    # e2e through the C-ABI host call with pinned host buffers
+    out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def recall(arrays, queries, ids, k, nsample, world):
+    """recall@k (bench::recall_at_k, metrics.hpp:14-24) of the local shard's
+    results vs an fp32 brute force (torch) on `nsample` queries. Informational."""
+    if world > 1 or nsample <= 0:
+        return None
+    import torch
+    x = arrays.vectors
+    q = queries[:nsample]
+    best = []
+    for i in range(0, q.shape[0], 16):
+        d = torch.cdist(q[i:i + 16], x)
+        best.append(torch.topk(d, k, largest=False).indices)
+    gt = torch.cat(best).cpu().numpy()
+    got = ids[:nsample].cpu().numpy().view(np.uint32)
+    hits = sum(len(set(gt[i].tolist()) & set(got[i].tolist())) for i in range(len(gt)))
+    return hits / (k * len(gt))
+
+
+def e2e(gix, queries, cfg, gamma, args, world, rank):
+    import torch
+
+    from paper_2508_17828_b200 import ivf as G
+    nq, B, k = cfg["nq"], cfg["batch"], cfg["k"]
+    hq = queries.cpu().pin_memory()
+    hqn = hq.numpy()
+    prof = G.PruningProfile.manual(gamma)
+    steps = max(1, min(args.steps, 3))
+
+    def once():
+        cand = 0
+        for b in range(0, nq, B):
+            ids, dist, ct = G.search_trim_ivf_knn_batch(gix, prof, hqn[b:b + B], k, cfg["nprobe"])
+            cand += int(ct[:, 3].sum())
+        return cand
+
+    once()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cand = 0
+    for _ in range(steps):
+        cand += once()
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
+                h2d_bytes_per_step=nq * cfg["dim"] * 4,
+                d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
+                api="trim_search_knn (C ABI, host buffers; pinned source)",
+                shard_local=world > 1)
+
+
+def _host_index(arrays):
+    from oracle.oracle import HostIndex
+    from paper_2508_17828_b200.builder import to_host
+    h = to_host(arrays)
+    return HostIndex(dim=h.dim, m=h.m, ksub=h.ksub, sub_dims=h.sub_dims, centroids=h.centroids,
+                     coarse=h.coarse, list_offsets=h.list_offsets, list_ids=h.list_ids,
+                     list_codes=h.list_codes, list_lx=h.list_lx, vectors=h.vectors)
+
+
+def _ref_time(hix, qs, cfg, gamma, target_s, threads):
+    """Reference CPU path (oracle/_ref: the unmodified reference headers) over a
+    bounded query sample, timed like bench::detail_sweep::run_queries
+    (sweep.hpp:121-152). Falls back to the C restatement if _ref is absent."""
+    from oracle import oracle as O
+    if O.ref_available():
+        ref = O.RefOracle()
+        ref.set_threads(threads)
+        sess = ref.session(hix)
+        kind = "reference"
+
+        def run(qsub):
+            sec, ct = ref.session_run(sess, 0, qsub, cfg["k"], cfg["nprobe"], gamma)
+            return sec, int(ct[3]), int(ct[0]), int(ct[2])
+    else:
+        co = O.COracle()
+        kind = "port"
+
+        def run(qsub):
+            t0 = time.perf_counter()
+            _, _, ct, _ = co.search_knn(hix, qsub, cfg["k"], cfg["nprobe"], gamma, threads=threads)
+            return time.perf_counter() - t0, int(ct[:, 3].sum()), int(ct[:, 0].sum()), int(ct[:, 2].sum())
+    n0 = min(len(qs), max(threads, 16))
+    sec, ev, dc, pr = run(qs[:n0])
+    per_q = sec / n0
+    n1 = int(min(len(qs), max(n0, target_s / max(per_q, 1e-9))))
+    if n1 > n0:
+        sec, ev, dc, pr = run(qs[:n1])
+    else:
+        n1 = n0
+    if kind == "reference":
+        ref.session_destroy(sess)
+    return dict(value=ev / sec, unit="candidates/s", cores=threads, kind=kind,
+                sample=f"first {n1} of {len(qs)} queries of {cfg['workload']} at gamma={gamma} "
+                       f"({sec:.1f}s)", qps=n1 / sec, prune_ratio=pr / max(1, pr + dc))
+
+
+def cpu_baseline(arrays, queries, cfg, gamma, args):
+    t0 = time.time()
+    hix = _host_index(arrays)
+    qs = queries.cpu().numpy()
+    log(f"host copy for the CPU baseline: {time.time() - t0:.1f}s")
+    return _ref_time(hix, qs, cfg, gamma, args.cpu_seconds, os.cpu_count() or 1)
+
+
+# ------------------------------------------------------ reference CPU arm
+def run_reference(args, cfg):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    torch.cuda.set_device(local)
+    arrays, queries = build_workload(cfg, 0, 1, local)
+    hix = _host_index(arrays)
+    qs = queries.cpu().numpy()
+    del arrays
+    torch.cuda.empty_cache()
+    threads = os.cpu_count() or 1
+    head = args.gamma if args.gamma else cfg["gamma"]
+    per_step_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    from oracle import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    # calibrate the per-step sample once
+    cal = _ref_time(hix, qs[:max(threads, 16)], cfg, head, 0.0, threads)
+    nstep = int(max(threads, min(len(qs), per_step_s * cal["qps"])))
+    vals, secs, evs = [], 0.0, 0
+    for i in range(args.warmup + args.steps):
+        sub = qs[(i * nstep) % len(qs):][:nstep]
+        if len(sub) < nstep:
+            sub = qs[:nstep]
+        r = _ref_time(hix, sub, cfg, head, 0.0, threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            n = int(r["sample"].split()[1])
+            secs += n / r["qps"]
+            evs += r["value"] * (n / r["qps"])
+    value = evs / secs
+    out = dict(metric="candidates filtered/sec (TRIM kNN filter; QPS, %HBM roofline, prune "
+                      "ratio alongside)",
+               value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=secs * 1e3 / args.steps, higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic",
+               impl="reference",
+               config=dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
+                           queries=nq_str(cfg), m=cfg["m"], nlist=cfg["nlist"],
+                           nprobe=cfg["nprobe"], k=cfg["k"], gamma=head),
+               cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind=kind,
+                                 sample=f"{nstep} queries per step of {cfg['workload']}"),
+               e2e=dict(value=value, unit="candidates/s", h2d_bytes_per_step=0,
+                        d2h_bytes_per_step=0))
+    print(json.dumps(out), flush=True)
+
+
+def nq_str(cfg):
+    return cfg["nq"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--gamma", type=float, default=None)
+    ap.add_argument("--n", type=int, default=None, help="override vectors per GPU (dev runs)")
+    ap.add_argument("--nq", type=int, default=None, help="override query count (dev runs)")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--recall-q", type=int, default=200)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+    if args.nq:
+        cfg["nq"] = args.nq
+    if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
+        log("note: the contract asks for >= 3 warm-up steps")
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

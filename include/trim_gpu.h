@@ -156,6 +156,17 @@ int trim_search_knn_device(trim_index_t index, const float* d_queries, uint64_t 
                            uint32_t nprobe, float gamma, uint32_t* d_ids, float* d_dist,
                            trim_counters* d_counters, uint32_t* d_status, void* stream);
 
+/* The two stages of trim_search_knn_device, separately (device pointers, async):
+ * probe_order into d_lists (nq*min(nprobe,nlist)), then the fused filter over
+ * those lists (like FAISS's search_preassigned). dim must be a multiple of 4. */
+int trim_probe_device(trim_index_t index, const float* d_queries, uint64_t nq, uint32_t nprobe,
+                      uint32_t* d_lists, void* stream);
+int trim_search_knn_preassigned_device(trim_index_t index, const float* d_queries, uint64_t nq,
+                                       uint32_t k, const uint32_t* d_lists, uint32_t np,
+                                       float gamma, uint32_t* d_ids, float* d_dist,
+                                       trim_counters* d_counters, uint32_t* d_status,
+                                       void* stream);
+
 /* pq::build_distance_table (pq/pq.hpp:158-172) for nq queries: lut_out is
  * nq*m*ksub floats (host), j-major like DistanceTable::entries. */
 int trim_build_lut(trim_index_t index, const float* queries, uint64_t nq, float* lut_out);
@@ -175,6 +186,49 @@ int trim_merge_topk_device(const float* d_dist, const uint32_t* d_ids, uint32_t 
                            int device, void* stream);
 
 void trim_free(void* p);
+
+/* ------------------------------------------------------------------------
+ * Device-side index build. The reference builds on host
+ * threads; these are its B200 equivalents. All d_* pointers are device
+ * memory on `device`; `stream` is a cudaStream_t (NULL = default).
+ * ------------------------------------------------------------------------ */
+
+/* Seeded N(0,1) rows (the role of make_normal_dataset, core/synthetic.hpp:11-18;
+ * Philox4x32-10 + Box-Muller, not libstdc++'s generator). */
+int trim_synth_normal_device(uint64_t n, uint32_t dim, uint64_t seed, float* d_out, int device,
+                             void* stream);
+/* Gaussian blobs, row i around center i % nc (make_blob_dataset,
+ * core/synthetic.hpp:21-33). */
+int trim_synth_blobs_device(const float* d_centers, uint64_t nc, uint32_t dim, uint64_t n,
+                            float sigma, uint64_t seed, float* d_out, int device, void* stream);
+/* Uniform [0,1) rows, optionally L2-normalised (dataset.hpp:44-56). */
+int trim_synth_uniform_device(uint64_t n, uint32_t dim, uint64_t seed, int normalize,
+                              float* d_out, int device, void* stream);
+/* The reference's seeded row sampler (pq/pq.hpp:72-80, ivf/ivf.hpp:121-126);
+ * host only. The caller xors the reference's seed constant in. */
+int trim_sample_rows(uint64_t n, uint64_t sample_n, uint64_t seed, uint64_t* rows_out);
+/* detail::nearest_centroid for n rows (pq/kmeans.hpp:27-41): exact fp32
+ * arithmetic, ties to the lowest index. d_dist may be NULL. */
+int trim_assign_device(const float* d_x, uint64_t n, uint32_t dim, const float* d_cent,
+                       uint32_t k, uint32_t* d_assign, float* d_dist, int device, void* stream);
+/* k-means (pq/kmeans.hpp:89-158 structure: k-means++ seeding, Lloyd steps,
+ * empty-cluster repair). Synchronous. */
+int trim_kmeans_device(const float* d_x, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters,
+                       uint64_t seed, float* d_centroids, int device);
+/* pq::train (pq/pq.hpp:65-113). sub_dims_out: host, m entries.
+ * d_centroids_out: ksub*dim floats in the trim_index_desc layout. */
+int trim_pq_train_device(const float* d_x, uint64_t n, uint32_t dim, uint32_t m, uint32_t ksub,
+                         uint32_t iters, uint64_t seed, uint64_t train_sample,
+                         uint32_t* sub_dims_out, float* d_centroids_out, int device);
+/* pq::encode for every row + Γ(l,x) (trim/landmarks.hpp:57-72), bit-exact.
+ * sub_dims: host. d_lx may be NULL. Synchronous. */
+int trim_pq_encode_device(const float* d_x, uint64_t n, uint32_t dim, uint32_t m, uint32_t ksub,
+                          const uint32_t* sub_dims, const float* d_centroids, uint8_t* d_codes,
+                          uint32_t code_stride, float* d_lx, int device, void* stream);
+/* Inverted lists from list assignments (ivf/ivf.hpp:145-152): d_ids holds
+ * the row ids grouped by list, ascending within a list; d_offsets nlist+1. */
+int trim_ivf_lists_device(const uint32_t* d_assign, uint64_t n, uint32_t nlist,
+                          uint64_t* d_offsets, uint32_t* d_ids, int device, void* stream);
 
 #ifdef __cplusplus
 }

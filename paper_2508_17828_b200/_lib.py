@@ -65,12 +65,38 @@ SIGNATURES = {
     "trim_search_knn_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                          C.c_uint32, C.c_float, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
+    "trim_probe_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
+                                    C.c_void_p]),
+    "trim_search_knn_preassigned_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                                     C.c_void_p, C.c_uint32, C.c_float, C.c_void_p,
+                                                     C.c_void_p, C.c_void_p, C.c_void_p,
+                                                     C.c_void_p]),
     "trim_build_lut": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "trim_probe": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p]),
     "trim_merge_topk_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
                                          C.c_uint32, C.c_void_p, C.c_void_p, C.c_int,
                                          C.c_void_p]),
     "trim_free": (None, [C.c_void_p]),
+    # device-side index build
+    "trim_synth_normal_device": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int,
+                                           C.c_void_p]),
+    "trim_synth_blobs_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                          C.c_float, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]),
+    "trim_synth_uniform_device": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
+                                            C.c_void_p, C.c_int, C.c_void_p]),
+    "trim_sample_rows": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "trim_assign_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint32,
+                                     C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "trim_kmeans_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint64, C.c_void_p, C.c_int]),
+    "trim_pq_train_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                       C.c_int]),
+    "trim_pq_encode_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                        C.c_int, C.c_void_p]),
+    "trim_ivf_lists_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_int, C.c_void_p]),
 }
 
 

@@ -74,6 +74,7 @@ trim_bl_est_kernel(DevIndex ix, BlParams p) {
 constexpr int kSelThreads = 1024;
 constexpr uint32_t kSelSmemKeys = 16384; // finish in shared memory below this
 
+#ifndef TRIM_M // non-template kernels: compiled once, in trim_capi.cu
 // One CTA per query: the k'-th smallest key (keys are unique: ids are),
 // then every key <= it, into sel[q*kp ...]. n <= kp selects everything.
 __global__ void __launch_bounds__(kSelThreads)
@@ -215,5 +216,7 @@ trim_bl_refine_kernel(DevIndex ix, const float* queries, const unsigned long lon
             key == ~0ull ? __int_as_float(0x7f800000) : __uint_as_float(static_cast<uint32_t>(key >> 32));
     }
 }
+
+#endif // TRIM_M
 
 } // namespace trimgpu

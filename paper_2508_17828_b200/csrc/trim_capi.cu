@@ -20,6 +20,7 @@
 #include "../../include/trim_gpu.h"
 #include "trim_baseline.cuh"
 #include "trim_kernels.cuh"
+#include "trim_launch.h"
 
 using namespace trimgpu;
 
@@ -171,61 +172,36 @@ int check_device_present() {
 }
 
 // ---------------------------------------------------------------- dispatch
-template <int M, int KS>
-void launch_knn_s(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
-    const uint32_t S = (p.k + 31) / 32;
-    dim3 grid(static_cast<unsigned>(p.nq));
-    auto go = [&](auto kern) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-        kern<<<grid, kThreads, smem, st>>>(ix, p);
-        CK(cudaGetLastError());
-    };
-    if (S <= 1)
-        go(trim_knn_kernel<M, KS, 1>);
-    else if (S <= 2)
-        go(trim_knn_kernel<M, KS, 2>);
-    else if (S <= 4)
-        go(trim_knn_kernel<M, KS, 4>);
-    else
-        go(trim_knn_kernel<M, KS, 8>);
-}
+// Specialised instantiations for the configs' code lengths (m = 16, 32, 48,
+// 120 with 256 centroids); anything else runs the runtime-(m, ksub) kernel.
+#define TRIM_DISPATCH(NAME, ...)                                            \
+    do {                                                                   \
+        cudaError_t _r;                                                    \
+        if (ix.ksub == 256 && ix.m == 16)                                  \
+            _r = NAME##16(__VA_ARGS__);                                    \
+        else if (ix.ksub == 256 && ix.m == 32)                             \
+            _r = NAME##32(__VA_ARGS__);                                    \
+        else if (ix.ksub == 256 && ix.m == 48)                             \
+            _r = NAME##48(__VA_ARGS__);                                    \
+        else if (ix.ksub == 256 && ix.m == 120)                            \
+            _r = NAME##120(__VA_ARGS__);                                   \
+        else                                                               \
+            _r = NAME##0(__VA_ARGS__);                                     \
+        CK(_r);                                                            \
+    } while (0)
 
 void launch_knn(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
-    if (ix.ksub == 256) {
-        switch (ix.m) {
-        case 16: return launch_knn_s<16, 256>(ix, p, smem, st);
-        case 32: return launch_knn_s<32, 256>(ix, p, smem, st);
-        case 48: return launch_knn_s<48, 256>(ix, p, smem, st);
-        case 120: return launch_knn_s<120, 256>(ix, p, smem, st);
-        default: break;
-        }
-    }
-    launch_knn_s<0, 0>(ix, p, smem, st);
-}
-
-template <int M, int KS>
-void launch_range_t(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,
-                    cudaStream_t st) {
-    auto kern = trim_range_kernel<M, KS>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, st>>>(ix, p);
-    CK(cudaGetLastError());
+    TRIM_DISPATCH(launch_knn_, ix, p, smem, st);
 }
 
 void launch_range(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,
                   cudaStream_t st) {
-    if (ix.ksub == 256) {
-        switch (ix.m) {
-        case 16: return launch_range_t<16, 256>(ix, p, grid, smem, st);
-        case 32: return launch_range_t<32, 256>(ix, p, grid, smem, st);
-        case 48: return launch_range_t<48, 256>(ix, p, grid, smem, st);
-        case 120: return launch_range_t<120, 256>(ix, p, grid, smem, st);
-        default: break;
-        }
-    }
-    launch_range_t<0, 0>(ix, p, grid, smem, st);
+    TRIM_DISPATCH(launch_range_, ix, p, grid, smem, st);
+}
+
+void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
+                   cudaStream_t st) {
+    TRIM_DISPATCH(launch_bl_est_, ix, p, grid, smem, st);
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -277,14 +253,13 @@ int validate_knn(uint32_t k, float gamma) {
     return TRIM_OK;
 }
 
-// Core kNN launch over padded device queries.
-int knn_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t nprobe,
-               float gamma, uint32_t* d_ids, float* d_dist, unsigned long long* d_ct,
-               uint32_t* d_status, cudaStream_t st) {
+// kNN filter launch over padded device queries and precomputed probe lists
+// (d_probe null => nlist == 1, the single list 0).
+int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t np,
+               const uint32_t* d_probe, float gamma, uint32_t* d_ids, float* d_dist,
+               unsigned long long* d_ct, uint32_t* d_status, cudaStream_t st) {
     if (nq == 0)
         return TRIM_OK;
-    DevBuf d_probe;
-    const uint32_t np = run_probe(ix, d_q, nq, nprobe, d_probe, st);
     const size_t smem = knn_smem_bytes(ix->dev.m, ix->dev.ksub, ix->dev.dim_stride, np);
     if (smem > kSmemLimit)
         return set_err(TRIM_EINVAL,
@@ -296,7 +271,7 @@ int knn_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.nq = nq;
     p.k = k;
     p.np = np;
-    p.probe = d_probe.as<uint32_t>();
+    p.probe = d_probe;
     p.two_gamma = 2.0f * gamma;
     p.ids_out = d_ids;
     p.dist_out = d_dist;
@@ -318,29 +293,16 @@ int knn_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     return TRIM_OK;
 }
 
-
-template <int M, int KS>
-void launch_bl_est_t(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
-                     cudaStream_t st) {
-    auto kern = trim_bl_est_kernel<M, KS>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, st>>>(ix, p);
-    CK(cudaGetLastError());
-}
-
-void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
-                   cudaStream_t st) {
-    if (ix.ksub == 256) {
-        switch (ix.m) {
-        case 16: return launch_bl_est_t<16, 256>(ix, p, grid, smem, st);
-        case 32: return launch_bl_est_t<32, 256>(ix, p, grid, smem, st);
-        case 48: return launch_bl_est_t<48, 256>(ix, p, grid, smem, st);
-        case 120: return launch_bl_est_t<120, 256>(ix, p, grid, smem, st);
-        default: break;
-        }
-    }
-    launch_bl_est_t<0, 0>(ix, p, grid, smem, st);
+// Probe + filter over padded device queries.
+int knn_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t nprobe,
+               float gamma, uint32_t* d_ids, float* d_dist, unsigned long long* d_ct,
+               uint32_t* d_status, cudaStream_t st) {
+    if (nq == 0)
+        return TRIM_OK;
+    DevBuf d_probe;
+    const uint32_t np = run_probe(ix, d_q, nq, nprobe, d_probe, st);
+    return knn_launch(ix, d_q, nq, k, np, d_probe.as<uint32_t>(), gamma, d_ids, d_dist, d_ct, d_status,
+                      st);
 }
 
 // ivf::search_baseline_ivfpq over padded device queries; host outputs.
@@ -418,6 +380,8 @@ int baseline_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_
 extern "C" {
 
 const char* trim_last_error(void) { return g_err.c_str(); }
+
+void trim__set_last_error(const char* msg) { g_err = msg; }
 
 int trim_abi_version(void) { return TRIM_ABI_VERSION; }
 
@@ -651,6 +615,54 @@ int trim_search_knn_device(trim_index_t ix, const float* d_queries, uint64_t nq,
         }
         return knn_device(ix, d_queries, nq, k, nprobe, gamma, d_ids, d_dist,
                           reinterpret_cast<unsigned long long*>(d_counters), d_status, st);
+    });
+}
+
+int trim_probe_device(trim_index_t ix, const float* d_queries, uint64_t nq, uint32_t nprobe,
+                      uint32_t* d_lists, void* stream) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "probe_order: null index");
+    if (nq == 0 || nprobe == 0)
+        return TRIM_OK;
+    if (ix->dev.dim_stride != ix->dev.dim)
+        return set_err(TRIM_EINVAL, "trim_probe_device: dim must be a multiple of 4 (use trim_probe)");
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const uint32_t np = std::min(nprobe, ix->dev.nlist);
+        if (ix->dev.nlist == 1) {
+            CK(cudaMemsetAsync(d_lists, 0, sizeof(uint32_t) * nq * np, st));
+            return TRIM_OK;
+        }
+        const uint32_t nl2 = pow2_at_least(ix->dev.nlist);
+        const size_t smem = sizeof(float) * ix->dev.dim_stride + sizeof(uint64_t) * nl2;
+        CK(cudaFuncSetAttribute(trim_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        trim_probe_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(ix->dev, d_queries, nq, np,
+                                                                             nl2, d_lists);
+        CK(cudaGetLastError());
+        return TRIM_OK;
+    });
+}
+
+int trim_search_knn_preassigned_device(trim_index_t ix, const float* d_queries, uint64_t nq,
+                                       uint32_t k, const uint32_t* d_lists, uint32_t np, float gamma,
+                                       uint32_t* d_ids, float* d_dist, trim_counters* d_counters,
+                                       uint32_t* d_status, void* stream) {
+    if (!ix)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: null index");
+    if (int rc = validate_knn(k, gamma))
+        return rc;
+    if (np > ix->dev.nlist)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: np > nlist");
+    if (ix->dev.dim_stride != ix->dev.dim)
+        return set_err(TRIM_EINVAL,
+                       "trim_search_knn_preassigned_device: dim must be a multiple of 4");
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        return knn_launch(ix, d_queries, nq, k, np, np ? d_lists : nullptr, gamma, d_ids, d_dist,
+                          reinterpret_cast<unsigned long long*>(d_counters), d_status,
+                          static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -1,0 +1,55 @@
+// trim_inst.cu — instantiates the filter kernels for one code length.
+// Built once per TRIM_M in {16, 32, 48, 120, 0 (= runtime m and ksub)}.
+#include "trim_baseline.cuh"
+#include "trim_kernels.cuh"
+#include "trim_launch.h"
+
+#ifndef TRIM_M
+#error "TRIM_M must be defined"
+#endif
+#if TRIM_M == 0
+#define TRIM_KS 0
+#else
+#define TRIM_KS 256
+#endif
+#define TRIM_CAT2(a, b) a##b
+#define TRIM_CAT(a, b) TRIM_CAT2(a, b)
+
+namespace trimgpu {
+
+namespace {
+template <typename K, typename... A>
+cudaError_t launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess)
+        return e;
+    kern<<<grid, kThreads, smem, st>>>(args...);
+    return cudaGetLastError();
+}
+} // namespace
+
+cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p, size_t smem,
+                                          cudaStream_t st) {
+    const uint32_t S = (p.k + 31) / 32;
+    const dim3 grid(static_cast<unsigned>(p.nq));
+    if (S <= 1)
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1>, grid, smem, st, ix, p);
+    if (S <= 2)
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2>, grid, smem, st, ix, p);
+    if (S <= 4)
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4>, grid, smem, st, ix, p);
+    return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8>, grid, smem, st, ix, p);
+}
+
+cudaError_t TRIM_CAT(launch_range_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,
+                                            size_t smem, cudaStream_t st) {
+    return launch(trim_range_kernel<TRIM_M, TRIM_KS>, grid, smem, st, ix, p);
+}
+
+cudaError_t TRIM_CAT(launch_bl_est_, TRIM_M)(const DevIndex& ix, const BlParams& p, dim3 grid,
+                                             size_t smem, cudaStream_t st) {
+    return launch(trim_bl_est_kernel<TRIM_M, TRIM_KS>, grid, smem, st, ix, p);
+}
+
+} // namespace trimgpu

@@ -556,6 +556,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
         atomicAdd(p.dc + q, static_cast<unsigned long long>(dc_local));
 }
 
+#ifndef TRIM_M // non-template kernels: compiled once, in trim_capi.cu
 // --------------------------------------------------------------------------
 // trim_probe_kernel — probe_order (ivf.hpp:173-187): coarse distances in the
 // reference's arithmetic, sorted by (dist, list id) in shared memory, first
@@ -667,5 +668,7 @@ trim_merge_kernel(const float* dist, const uint32_t* ids, uint32_t nshards, uint
             key == ~0ull ? __int_as_float(0x7f800000) : __uint_as_float(static_cast<uint32_t>(key >> 32));
     }
 }
+
+#endif // TRIM_M
 
 } // namespace trimgpu

@@ -1,0 +1,383 @@
+// trim_adc.cuh — conflict-free ADC over a shared-memory PQ lookup table.
+//
+// The reference ADC (pq/pq.hpp:186-192) is a sequential fp32 sum over
+// j = 0..m-1 of LUT[j][code_j]. With the natural [j][c] layout, 32 lanes
+// reading the same subspace hit banks code % 32 at random (~3.5-way
+// conflicts, measured).
+//
+// Layout here ("blocked"). Subspaces are grouped in blocks of 32 columns; a
+// FULL block is 256 rows (= codes) x 32 floats, so an entry's bank is its
+// column. The last block may be a HALF block (<= 16 live columns): 256 rows
+// x 16 floats — two lanes then share each column (2-way conflicts on those
+// lookups) — or, when it is the only block (m <= 16), 16 columns stored
+// twice (32 floats per row, conflict-free). Partial blocks are padded with
+// zero columns (adding +0.0f to a non-negative sum is exact). m = 48 takes
+// 32 KB + 16 KB.
+//
+// Two schedules:
+//   FastCode (fast) — lane l reads column l ^ s at step s, so the 32 lanes
+//               read 32 distinct banks; any-order fp32 sum with four partial
+//               accumulators, used with a rigorous error interval
+//               (est_lower_bound) to decide which candidates can possibly
+//               pass the threshold;
+//   adc_exact — lane l reads column (l + s) mod 32 and adds the values in
+//               exactly the reference order j = 0, 1, ... (two predicated
+//               passes), bit-identical to pq::adc_lookup. Used for the
+//               candidates the interval cannot decide and for the survivors.
+// A lookup is PRMT (code byte) + LOP3 (lane column, with the shared base
+// folded in) + IMAD (row) + LDS + FADD.
+#pragma once
+
+#include "trim_common.cuh"
+
+// The dynamic shared-memory window of every TRIM kernel; the LUT sits at
+// offset 0.
+extern __shared__ __align__(16) unsigned char trim_dyn_smem[];
+
+namespace trimgpu {
+
+constexpr uint32_t kFullBytes = 256u * 32u * 4u; // 32 KB
+
+// Block structure of m subspaces.
+struct LutShape {
+    uint32_t nfull; // 32-column blocks (incl. a zero-padded 17..31 tail)
+    uint32_t half;  // 1 if the last block has <= 16 live columns
+    uint32_t hdup;  // the HALF block is duplicated (only when it is the only block)
+    __host__ __device__ static LutShape of(uint32_t m) {
+        LutShape s;
+        const uint32_t rem = m & 31u;
+        s.nfull = m >> 5;
+        s.half = 0;
+        if (rem > 16)
+            ++s.nfull;
+        else if (rem)
+            s.half = 1;
+        s.hdup = s.half && s.nfull == 0;
+        return s;
+    }
+    __host__ __device__ uint32_t blocks() const { return nfull + half; }
+    __host__ __device__ uint32_t half_row_bytes() const { return hdup ? 128u : 64u; }
+    __host__ __device__ size_t bytes() const {
+        return static_cast<size_t>(nfull) * kFullBytes + (half ? 256u * half_row_bytes() : 0u);
+    }
+};
+
+__host__ __device__ inline size_t lut_bytes(int /*M_template*/, uint32_t m) { return LutShape::of(m).bytes(); }
+
+// pq::build_distance_table (pq.hpp:158-172) into the blocked layout. Entry
+// values are the reference's euclidean_sq, bit for bit.
+__device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const float* q_smem, float* lut) {
+    const LutShape sh = LutShape::of(ix.m);
+    const uint32_t hrow = sh.half_row_bytes() / 4;          // floats per HALF row
+    float* hblk = lut + sh.nfull * (kFullBytes / 4);
+    for (uint32_t j = 0; j < ix.m; ++j) {
+        const uint32_t sd = ix.sub_dims[j];
+        const uint32_t off = ix.sub_offsets[j];
+        const float* cb = ix.centroids + static_cast<size_t>(ix.ksub) * off;
+        const uint32_t b = j >> 5, t = j & 31u;
+        for (uint32_t c = threadIdx.x; c < ix.ksub; c += blockDim.x) {
+            const float v = euclid_sq_generic(q_smem + off, cb + c * sd, sd);
+            if (b < sh.nfull) {
+                lut[b * (kFullBytes / 4) + c * 32 + t] = v;
+            } else {
+                hblk[c * hrow + t] = v;
+                if (sh.hdup)
+                    hblk[c * hrow + t + 16] = v;
+            }
+        }
+    }
+    // zero every non-live column of the last block: both schedules read all
+    // columns, and +0.0f leaves the sum unchanged
+    const uint32_t rem = ix.m & 31u;
+    if (rem) {
+        const uint32_t width = sh.half ? 16u : 32u;
+        const uint32_t pad = width - rem;
+        for (uint32_t i = threadIdx.x; i < 256 * pad; i += blockDim.x) {
+            const uint32_t c = i / pad, t = rem + i % pad;
+            if (sh.half) {
+                hblk[c * hrow + t] = 0.0f;
+                if (sh.hdup)
+                    hblk[c * hrow + t + 16] = 0.0f;
+            } else {
+                lut[(ix.m >> 5) * (kFullBytes / 4) + c * 32 + t] = 0.0f;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t sel32(bool p, uint32_t a, uint32_t b) { return p ? a : b; }
+
+// Shared-memory load at a 32-bit .shared window address.
+__device__ __forceinline__ float lds_f32(uint32_t saddr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+    return v;
+}
+
+// .shared window address of the LUT (a multiple of 128: the per-lane column
+// bits can be XORed into it).
+__device__ __forceinline__ uint32_t lut_saddr() {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(trim_dyn_smem));
+}
+
+// Per-lane constants of the fast schedule.
+struct LaneAdc {
+    uint32_t l;      // lane
+    uint32_t lf;     // LUT base + 4*l       (FULL blocks: column l ^ s)
+    uint32_t lh;     // HALF base + 4*lane'  (lane' = l, or l & 15 without duplication)
+    uint32_t sel[4]; // PRMT selectors: output byte 0 = code byte (q ^ (l & 3))
+    __device__ __forceinline__ void init(uint32_t lane, const LutShape& sh) {
+        l = lane;
+        const uint32_t base = lut_saddr();
+        lf = base + 4u * lane;
+        lh = base + sh.nfull * kFullBytes + 4u * (sh.hdup ? lane : (lane & 15u));
+        const uint32_t x = lane & 3u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            sel[q] = 0x4440u | (static_cast<uint32_t>(q) ^ x);
+    }
+};
+
+// Code words of one block for the fast schedule. load_block_fast only issues
+// the loads (so a prefetch has no dependent instructions); the top bit of the
+// word permutation (wl = (l >> 2) & (NW-1)) is applied by the load addresses
+// (16-byte halves of a FULL block, 8-byte halves of a HALF block), and
+// permute_block applies the rest with selects, leaving word i = original
+// word i ^ wl.
+template <bool HALF>
+__device__ __forceinline__ void load_block_fast(const uint8_t* __restrict__ code, uint32_t b, uint32_t l,
+                                                uint32_t w[8]) {
+    if (!HALF) {
+        const uint32_t top = (l >> 4) & 1u; // bit 2 of wl
+        const uint4* p = reinterpret_cast<const uint4*>(code + 32 * b);
+        const uint4 a = __ldg(p + top);
+        const uint4 c = __ldg(p + (top ^ 1u));
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = c.x; w[5] = c.y; w[6] = c.z; w[7] = c.w;
+    } else {
+        const uint32_t top = (l >> 3) & 1u; // bit 1 of wl
+        const uint2* p = reinterpret_cast<const uint2*>(code + 32 * b);
+        const uint2 a = __ldg(p + top);
+        const uint2 c = __ldg(p + (top ^ 1u));
+        w[0] = a.x; w[1] = a.y; w[2] = c.x; w[3] = c.y;
+    }
+}
+
+template <bool HALF>
+__device__ __forceinline__ void permute_block(uint32_t w[8], uint32_t l) {
+    const bool b0 = (l >> 2) & 1u;
+    if (!HALF) {
+        const bool b1 = (l >> 3) & 1u;
+        uint32_t t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            t[i] = sel32(b0, w[i ^ 1], w[i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            w[i] = sel32(b1, t[i ^ 2], t[i]);
+    } else {
+        const uint32_t a = sel32(b0, w[1], w[0]), b = sel32(b0, w[0], w[1]);
+        const uint32_t c = sel32(b0, w[3], w[2]), d = sel32(b0, w[2], w[3]);
+        w[0] = a; w[1] = b; w[2] = c; w[3] = d;
+    }
+}
+
+// Any-order sum of one block; lane reads column l ^ s at step s. ROWB = row
+// bytes; IMM = block byte offset (folds into the LDS immediate). Four partial
+// sums keep four independent FADD chains in flight.
+template <int STEPS, uint32_t ROWB, uint32_t IMM>
+__device__ __forceinline__ float block_fast(uint32_t lbase, const uint32_t w[8], const LaneAdc& la,
+                                            float acc) {
+    float part[4] = {acc, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int s = 0; s < STEPS; ++s) {
+        const uint32_t c = __byte_perm(w[s >> 2], 0, la.sel[s & 3]);
+        const uint32_t col = lbase ^ (static_cast<uint32_t>(s) << 2);
+        part[s & 3] = __fadd_rn(part[s & 3], lds_f32(c * ROWB + col + IMM));
+    }
+    return __fadd_rn(__fadd_rn(part[0], part[1]), __fadd_rn(part[2], part[3]));
+}
+
+// Fast ADC split into load (global -> registers) and sum, so a thread can
+// have the next candidate's loads in flight while it sums the current one.
+template <int M>
+struct FastCode {
+    static constexpr uint32_t kMaxB = M > 0 ? (static_cast<uint32_t>(M) + 31) / 32 : 4;
+    uint32_t w[kMaxB][8];
+
+    __device__ __forceinline__ void load(const uint8_t* __restrict__ code, uint32_t m, uint32_t l) {
+        const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
+#pragma unroll
+        for (uint32_t b = 0; b < kMaxB; ++b) {
+            if (b < sh.nfull)
+                load_block_fast<false>(code, b, l, w[b]);
+            else if (b == sh.nfull && sh.half)
+                load_block_fast<true>(code, b, l, w[b]);
+        }
+    }
+
+    template <uint32_t B>
+    __device__ __forceinline__ float sum_block(const LutShape& sh, const LaneAdc& la, float acc) {
+        if (B < sh.nfull) {
+            permute_block<false>(w[B], la.l);
+            return block_fast<32, 128u, B * kFullBytes>(la.lf, w[B], la, acc);
+        }
+        if (B == sh.nfull && sh.half) {
+            permute_block<true>(w[B], la.l);
+            if (M > 0 && !LutShape::of(static_cast<uint32_t>(M)).hdup)
+                return block_fast<16, 64u, 0u>(la.lh, w[B], la, acc);
+            return sh.hdup ? block_fast<16, 128u, 0u>(la.lh, w[B], la, acc)
+                           : block_fast<16, 64u, 0u>(la.lh, w[B], la, acc);
+        }
+        return acc;
+    }
+
+    // Consumes the loaded words (permutes them in place).
+    __device__ __forceinline__ float sum(uint32_t m, const LaneAdc& la) {
+        const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
+        float acc = 0.0f;
+        acc = sum_block<0>(sh, la, acc);
+        if (kMaxB > 1)
+            acc = sum_block<(kMaxB > 1 ? 1 : 0)>(sh, la, acc);
+        if (kMaxB > 2)
+            acc = sum_block<(kMaxB > 2 ? 2 : 0)>(sh, la, acc);
+        if (kMaxB > 3)
+            acc = sum_block<(kMaxB > 3 ? 3 : 0)>(sh, la, acc);
+        return acc;
+    }
+};
+
+// ------------------------------------------------------- exact (reference order)
+__device__ __forceinline__ void load_block_plain(const uint8_t* __restrict__ code, uint32_t b, bool half,
+                                                 uint32_t w[8]) {
+    const uint4* p = reinterpret_cast<const uint4*>(code + 32 * b);
+    const uint4 a = __ldg(p);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    if (!half) {
+        const uint4 c = __ldg(p + 1);
+        w[4] = c.x; w[5] = c.y; w[6] = c.z; w[7] = c.w;
+    } else {
+        w[4] = w[5] = w[6] = w[7] = 0;
+    }
+}
+
+// Rotate the NW words (4*NW bytes) left by r bytes: byte s <- byte (s + r) mod (4*NW).
+template <int NW>
+__device__ __forceinline__ void rot_bytes(uint32_t w[8], uint32_t r) {
+    const uint32_t wr = (r >> 2) & (NW - 1);
+#pragma unroll
+    for (int k = 1; k < NW; k <<= 1) {
+        const bool p = wr & k;
+        uint32_t t[8];
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+            t[i] = sel32(p, w[(i + k) & (NW - 1)], w[i]);
+#pragma unroll
+        for (int i = 0; i < NW; ++i)
+            w[i] = t[i];
+    }
+    const uint32_t sh = 8 * (r & 3u);
+    uint32_t t[8];
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+        t[i] = __funnelshift_r(w[i], w[(i + 1) & (NW - 1)], sh);
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+        w[i] = t[i];
+}
+
+// Exact sequential block sum: the lane reads column (r + s) mod S at step s
+// (r = its rotation), so values arrive in column order r, r+1, ..., S-1,
+// 0, ..., r-1; the reference order 0..S-1 is restored by adding the wrapped
+// part (s >= S-r) first, then the rest. b0 = address of column r in row 0.
+template <int S>
+__device__ __forceinline__ float block_exact(uint32_t b0, uint32_t rowb, uint32_t w[8], uint32_t r,
+                                             float acc) {
+    constexpr int NW = S / 4;
+    rot_bytes<NW>(w, r);
+    const uint32_t b1 = b0 - 4 * S; // wrapped (s >= S - r)
+    float v[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const uint32_t c = (w[s >> 2] >> (8 * (s & 3))) & 0xFFu;
+        const bool wrap = static_cast<uint32_t>(s) + r >= S;
+        v[s] = lds_f32(c * rowb + (wrap ? b1 : b0) + 4 * s);
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (static_cast<uint32_t>(s) + r >= S)
+            acc = __fadd_rn(acc, v[s]);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (static_cast<uint32_t>(s) + r < S)
+            acc = __fadd_rn(acc, v[s]);
+    return acc;
+}
+
+template <int M>
+__device__ __forceinline__ float adc_exact(const uint8_t* __restrict__ code, uint32_t m, uint32_t l) {
+    const uint32_t mm = M > 0 ? static_cast<uint32_t>(M) : m;
+    const LutShape sh = LutShape::of(mm);
+    const uint32_t base = lut_saddr();
+    float acc = 0.0f;
+    uint32_t w[8];
+    constexpr uint32_t kMaxB = M > 0 ? (static_cast<uint32_t>(M) + 31) / 32 : 4;
+#pragma unroll
+    for (uint32_t b = 0; b < kMaxB; ++b) {
+        if (b >= sh.nfull)
+            break;
+        load_block_plain(code, b, false, w);
+        acc = block_exact<32>(base + b * kFullBytes + 4 * l, 128u, w, l, acc);
+    }
+    if (sh.half) {
+        load_block_plain(code, sh.nfull, true, w);
+        const uint32_t r = l & 15u;
+        const uint32_t hb = base + sh.nfull * kFullBytes + (sh.hdup ? 64u * (l >> 4) : 0u) + 4 * r;
+        acc = block_exact<16>(hb, sh.half_row_bytes(), w, r, acc);
+    }
+    return acc;
+}
+
+// --------------------------------------------------------- rigorous interval
+// Any two fp32 summations of the same m non-negative terms, each in any
+// order or tree (height <= k), differ by at most 2*gamma_k/(1-gamma_k) times
+// either result (gamma_k = k*u/(1-k*u), u = 2^-24; Higham, "Accuracy and
+// Stability of Numerical Algorithms", eq. 4.4). The fast sum adds +0.0f
+// zero-padding terms and at most 6 extra partial-sum combines per block;
+// adc_rel_eps(m) uses k = m + 8*blocks and doubles the bound.
+__host__ __device__ inline float adc_rel_eps(uint32_t m) {
+    const double u = 1.0 / 16777216.0;
+    const double k = static_cast<double>(m + 8 * LutShape::of(m).blocks());
+    const double g = k * u / (1.0 - k * u);
+    return static_cast<float>(2.0 * (2.0 * g / (1.0 - g)));
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Lower bound on the reference's est = relaxed_lb(sqrt(adc_ref), glx, gamma)
+// (lower_bound.hpp:18-22) given any-order sum a of the same terms:
+// adc_ref in [a(1-eps), a(1+eps)], then every reference operation
+// (sqrt, sub, square, products, add; each correctly rounded, monotone) is
+// bounded with directed rounding. sqrt.approx (rel. error < 2^-21) is
+// widened by 2^-16.
+__device__ __forceinline__ float est_lower_bound(float a, float glx, float two_gamma, float eps) {
+    const float a_lo = __fmul_rd(a, 1.0f - eps);
+    const float a_hi = __fmul_ru(a, 1.0f + eps);
+    const float g_lo = __fmul_rd(sqrt_approx(a_lo), 1.0f - 1.0f / 65536.0f);
+    const float g_hi = __fmul_ru(sqrt_approx(a_hi), 1.0f + 1.0f / 65536.0f);
+    const float d_lo = __fsub_rd(g_lo, glx);
+    const float d_hi = __fsub_ru(g_hi, glx);
+    float e_lo = 0.0f;
+    if (d_lo > 0.0f)
+        e_lo = __fmul_rd(d_lo, d_lo);
+    else if (d_hi < 0.0f)
+        e_lo = __fmul_rd(d_hi, d_hi);
+    const float t_lo = __fmul_rd(__fmul_rd(two_gamma, g_lo), glx);
+    return __fadd_rd(e_lo, t_lo);
+}
+
+} // namespace trimgpu

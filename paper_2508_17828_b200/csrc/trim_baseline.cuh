@@ -28,12 +28,12 @@ struct BlParams {
 template <int M, int KS>
 __global__ void __launch_bounds__(kThreads)
 trim_bl_est_kernel(DevIndex ix, BlParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     const uint32_t q = blockIdx.y, tid = threadIdx.x;
-    float* qv = reinterpret_cast<float*>(smem);
-    float* lut = qv + ix.dim_stride;
-    size_t off = sizeof(float) * (ix.m * ix.ksub + ix.dim_stride);
-    off = (off + 15) & ~size_t(15);
+    const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m;
+    float* lut = reinterpret_cast<float*>(smem);
+    float* qv = lut + lut_bytes(M, m) / sizeof(float);
+    size_t off = lut_bytes(M, m) + sizeof(float) * ix.dim_stride;
     StreamSmem st;
     st.base = reinterpret_cast<uint64_t*>(smem + off);
     off += sizeof(uint64_t) * p.np;
@@ -49,7 +49,7 @@ trim_bl_est_kernel(DevIndex ix, BlParams p) {
     if (begin >= total)
         return;
     const uint32_t end = min(total, begin + p.slice);
-    build_lut_smem(ix, qv, lut);
+    build_lut_blocked(ix, qv, lut);
     __syncthreads();
     uint32_t lo = 0, hi = p.np;
     while (lo + 1 < hi) {
@@ -65,8 +65,9 @@ trim_bl_est_kernel(DevIndex ix, BlParams p) {
         while (st.cum[li + 1] <= pp)
             ++li;
         const uint32_t e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
-        const float est = adc_sum<M, KS>(lut, ix.codes + static_cast<size_t>(e) * ix.code_stride,
-                                         ix.m, ix.ksub);
+        // exact reference-order ADC, conflict-free (lane-rotated schedule)
+        const float est = adc_exact<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m,
+                                       tid & 31u);
         out[pp] = scored_key(est, __ldg(ix.list_ids + e));
     }
 }
@@ -80,7 +81,7 @@ constexpr uint32_t kSelSmemKeys = 16384; // finish in shared memory below this
 __global__ void __launch_bounds__(kSelThreads)
 trim_bl_select_kernel(const unsigned long long* keys, uint64_t stride,
                       const unsigned long long* totals, uint32_t kp, unsigned long long* sel) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem);
     __shared__ uint32_t hist[256];
     __shared__ uint32_t s_bucket, s_rank, s_count, s_n;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kThreads)
 trim_bl_refine_kernel(DevIndex ix, const float* queries, const unsigned long long* sel,
                       const unsigned long long* totals, uint32_t kp, uint32_t kp_pow2, uint32_t k,
                       uint32_t* ids_out, float* dist_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     float* qv = reinterpret_cast<float*>(smem);
     unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem + sizeof(float) * ix.dim_stride);
     const uint32_t q = blockIdx.x, tid = threadIdx.x;

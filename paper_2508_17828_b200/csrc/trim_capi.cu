@@ -206,6 +206,13 @@ void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+// The kernel specialisation (m template value) launch_* will pick.
+int dispatch_m(const DevIndex& ix) {
+    if (ix.ksub == 256 && (ix.m == 16 || ix.m == 32 || ix.m == 48 || ix.m == 120))
+        return static_cast<int>(ix.m);
+    return 0;
+}
+
 // Probe lists for a query batch (d_q rows padded to dim_stride). Returns
 // the effective per-query probe count; d_probe is null when nlist == 1.
 uint32_t run_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t nprobe,
@@ -260,7 +267,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
                unsigned long long* d_ct, uint32_t* d_status, cudaStream_t st) {
     if (nq == 0)
         return TRIM_OK;
-    const size_t smem = knn_smem_bytes(ix->dev.m, ix->dev.ksub, ix->dev.dim_stride, np);
+    const size_t smem = knn_smem_bytes(dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
     if (smem > kSmemLimit)
         return set_err(TRIM_EINVAL,
                        "search_trim_ivf_knn: per-query state (%zu B for m=%u, ksub=%u, "
@@ -273,6 +280,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.np = np;
     p.probe = d_probe;
     p.two_gamma = 2.0f * gamma;
+    p.adc_eps = adc_rel_eps(ix->dev.m);
     p.ids_out = d_ids;
     p.dist_out = d_dist;
     p.counters = d_ct;
@@ -316,8 +324,7 @@ int baseline_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_
     const uint32_t slice = 32 * kChunkMax;
     const uint64_t nslices = (bound + slice - 1) / slice;
     const uint64_t qb = std::max<uint64_t>(1, std::min<uint64_t>({nq, 65535, (1ull << 31) / (bound * 8)}));
-    size_t est_smem = sizeof(float) * (ix->dev.m * ix->dev.ksub + ix->dev.dim_stride);
-    est_smem = (est_smem + 15) & ~size_t(15);
+    size_t est_smem = lut_bytes(dispatch_m(ix->dev), ix->dev.m) + sizeof(float) * ix->dev.dim_stride;
     est_smem += sizeof(uint64_t) * np + sizeof(uint32_t) * (np + 1);
     if (est_smem > kSmemLimit)
         return set_err(TRIM_EINVAL, "search_baseline_ivfpq: per-query state exceeds 227 KB");
@@ -696,12 +703,12 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
         CK(cudaMemcpyAsync(d_r2.p, r2.data(), sizeof(float) * nq, cudaMemcpyHostToDevice, st));
         DevBuf d_probe;
         const uint32_t np = run_probe(ix, d_q.as<float>(), nq, nprobe, d_probe, st);
-        const size_t smem = range_smem_bytes(ix->dev.m, ix->dev.ksub, ix->dev.dim_stride, np);
+        const size_t smem = range_smem_bytes(dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
         if (smem > kSmemLimit)
             return set_err(TRIM_EINVAL,
                            "search_trim_ivf_range: per-query state (%zu B) exceeds 227 KB", smem);
         const uint64_t bound = ix->stream_bound(np);
-        const uint32_t slice = 32 * kChunkMax;
+        const uint32_t slice = 32 * kRangeChunk;
         const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);
         DevBuf d_cnt(sizeof(unsigned int) * nq, st), d_dc(sizeof(unsigned long long) * nq, st),
             d_eval(sizeof(unsigned long long) * nq, st);
@@ -716,6 +723,7 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
             RangeParams p{};
             p.np = np;
             p.two_gamma = 2.0f * gamma;
+            p.adc_eps = adc_rel_eps(ix->dev.m);
             p.slice = slice;
             p.cap = cap;
             for (uint64_t b = 0; b < nq; b += 65535) {

@@ -11,16 +11,18 @@
 // Paths are relative to /root/reference/proj/include/trimsearch.
 #pragma once
 
+#include "trim_adc.cuh"
 #include "trim_common.cuh"
 
 namespace trimgpu {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / kWarp;
-constexpr int kChunkU = 4;                      // candidates per thread per chunk
-constexpr int kChunkMax = kThreads * kChunkU;   // 1024 stream positions per chunk
-constexpr int kBins = kChunkU * kWarps;         // 32 survivor bins of 32 slots
-constexpr int kMaxSeg = 32;                     // lists touched by one chunk
+constexpr int kChunkU = 2;                      // kNN: candidates per thread per chunk
+constexpr int kChunkMax = kThreads * kChunkU;   // 512 stream positions per kNN chunk
+constexpr int kBins = kChunkU * kWarps;         // 16 survivor bins of 32 slots
+constexpr int kRangeU = 4;                      // range: candidates per thread per chunk
+constexpr int kRangeChunk = kThreads * kRangeU; // 1024
 
 // --------------------------------------------------------------------------
 // Shared helpers: the per-query candidate stream.
@@ -64,35 +66,6 @@ __device__ __forceinline__ uint32_t load_stream(const DevIndex& ix, const uint32
     }
     __syncthreads();
     return s.cum[np];
-}
-
-// ADC (pq/pq.hpp:186-192): sequential fp32 sum from 0 over j = 0..m-1 of
-// lut[j][code_j]; code bytes come in 16-byte vectors.
-template <int M, int KS>
-__device__ __forceinline__ float adc_sum(const float* __restrict__ lut,
-                                         const uint8_t* __restrict__ code, uint32_t m,
-                                         uint32_t ksub) {
-    constexpr int kBlocks = M > 0 ? (M + 15) / 16 : 8;
-    const uint32_t mm = M > 0 ? static_cast<uint32_t>(M) : m;
-    const uint32_t ks = KS > 0 ? static_cast<uint32_t>(KS) : ksub;
-    const uint4* cw = reinterpret_cast<const uint4*>(code);
-    float acc = 0.0f;
-#pragma unroll
-    for (int b = 0; b < kBlocks; ++b) {
-        if (M == 0 && static_cast<uint32_t>(b * 16) >= mm)
-            break;
-        const uint4 w = __ldg(cw + b);
-        const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const uint32_t j = static_cast<uint32_t>(b * 16 + t);
-            if (j < mm) {
-                const uint32_t c = (words[t >> 2] >> (8 * (t & 3))) & 0xFFu;
-                acc = __fadd_rn(acc, lut[j * ks + c]);
-            }
-        }
-    }
-    return acc;
 }
 
 // --------------------------------------------------------------------------
@@ -215,196 +188,166 @@ struct KnnParams {
     uint32_t np;             // probed lists per query
     const uint32_t* probe;   // nq*np list ids, or null when nlist == 1
     float two_gamma;
+    float adc_eps;           // adc_rel_eps(m)
     uint32_t* ids_out;       // nq*k
     float* dist_out;         // nq*k
     unsigned long long* counters; // nq*6
     uint32_t* status;        // bit0: some query had < k probed entries
-    uint32_t first_chunk;    // ramp: first chunk after the seeds
+    uint32_t first_chunk;    // unused (kept for ABI stability of the launcher)
 };
 
-__host__ __device__ inline size_t knn_smem_bytes(uint32_t m, uint32_t ksub, uint32_t dim_stride,
+// Warp-specialised pipeline: warp 0 replays, warps 1..kWorkers filter.
+constexpr uint32_t kWorkers = kWarps - 1;          // 7
+constexpr uint32_t kLaneU = 1;                     // candidates per worker lane per chunk
+constexpr uint32_t kPerWorker = kWarp * kLaneU;    // 64 stream positions per worker per chunk
+constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 448 stream positions per chunk
+constexpr uint32_t kRing = 8;                      // chunk buffers in flight
+
+__host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
                                                  uint32_t np) {
-    size_t b = 0;
-    b += sizeof(float) * m * ksub;               // lut
+    size_t b = lut_bytes(mt, m);                 // blocked lut at offset 0
     b += sizeof(float) * dim_stride;             // query
-    b = (b + 15) & ~size_t(15);
     b += sizeof(uint64_t) * np;                  // base
     b += sizeof(uint32_t) * (np + 1);            // cum
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint32_t) * kChunkMax * 3;       // survivors: entry/id, est, d
-    b += sizeof(int64_t) * kMaxSeg + sizeof(uint32_t) * kMaxSeg; // segments
-    b += sizeof(uint32_t) * (kBins + 8);         // bin counts + scalars
+    b += sizeof(uint32_t) * kRing * kChunkW * 3; // superset bins: entry/id, est, d
+    b += sizeof(uint32_t) * kRing * kWorkers;    // bin counts
+    b = (b + 15) & ~size_t(15);
+    b += sizeof(uint64_t) * 2 * kRing;           // full/empty mbarriers
+    b += 16;                                     // published threshold
     return b;
 }
 
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(saddr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(saddr(bar)), "r"(parity)
+                     : "memory");
+        if (done)
+            break;
+    }
+}
+__device__ __forceinline__ float ld_volatile(const float* p) {
+    return *reinterpret_cast<const volatile float*>(p);
+}
+
+// --------------------------------------------------------------------------
+// trim_knn_kernel — one CTA owns one query's candidate stream.
+//
+// The reference threshold max_dis is sequential state (ivf.hpp:256-287,
+// SPEC.md:500). Worker warps (1..7) stream the query's candidates in chunks
+// of 224 positions (warp w, lane l: position c*224 + (w-1)*32 + l), each with
+// the latest threshold T the replay warp has published — any published T is
+// >= the reference's running threshold at every later position, because the
+// threshold only decreases. A worker keeps the superset {est_lower_bound < T}
+// (the any-order ADC's rigorous interval, trim_adc.cuh), recomputes the
+// reference-order ADC and est for those, and computes exact L2 for every
+// member with est < T. Warp 0 replays the chunk's members in stream order
+// with the live threshold: evaluate iff est < T_live (prune on tie,
+// ivf.hpp:275), replace iff (d, id) < top (ivf.hpp:277-282). The evaluate /
+// prune decisions, counters and result set are therefore the reference's,
+// for any gamma. Chunks flow through a ring of kRing buffers guarded by
+// mbarriers (full: 224 worker-lane arrivals; empty: 32 replay-lane arrivals),
+// so workers never wait for the replay except when the ring is full; the
+// next chunk's codes are prefetched into registers while the current one is
+// filtered.
+// --------------------------------------------------------------------------
 template <int M, int KS, int S>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (M == 0 || M > 64) ? 2 : 3)
 trim_knn_kernel(DevIndex ix, KnnParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     const uint32_t q = blockIdx.x;
     if (q >= p.nq)
         return;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m;
 
-    float* qv = reinterpret_cast<float*>(smem); // dim_stride % 4 == 0: lut stays 16B-aligned
-    float* lut = qv + ix.dim_stride;
-    size_t off = sizeof(float) * (ix.m * ix.ksub + ix.dim_stride);
-    off = (off + 15) & ~size_t(15);
+    float* lut = reinterpret_cast<float*>(smem); // offset 0
+    float* qv = lut + lut_bytes(M, m) / sizeof(float);
+    size_t off = lut_bytes(M, m) + sizeof(float) * ix.dim_stride;
     StreamSmem st;
     st.base = reinterpret_cast<uint64_t*>(smem + off);
     off += sizeof(uint64_t) * p.np;
     st.cum = reinterpret_cast<uint32_t*>(smem + off);
     off += sizeof(uint32_t) * (p.np + 1);
     off = (off + 15) & ~size_t(15);
-    uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off); // entry index, then id
-    float* s_est = reinterpret_cast<float*>(s_e + kChunkMax);
-    float* s_d = s_est + kChunkMax;
-    int64_t* seg_delta = reinterpret_cast<int64_t*>(s_d + kChunkMax);
-    uint32_t* seg_rel = reinterpret_cast<uint32_t*>(seg_delta + kMaxSeg);
-    uint32_t* bin_cnt = seg_rel + kMaxSeg;
-    uint32_t* scal = bin_cnt + kBins; // [0]=T bits [1]=cn [2]=nseg [3]=li cursor
+    uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);  // [kRing][kChunkW]: entry, then id
+    float* s_est = reinterpret_cast<float*>(s_e + kRing * kChunkW);
+    float* s_d = s_est + kRing * kChunkW;
+    uint32_t* bin_cnt = reinterpret_cast<uint32_t*>(s_d + kRing * kChunkW); // [kRing][kWorkers]
+    // (bins: worker w of ring slot s owns s_*[s*kChunkW + w*kPerWorker ...], in stream order)
+    off = reinterpret_cast<unsigned char*>(bin_cnt + kRing * kWorkers) - smem;
+    off = (off + 15) & ~size_t(15);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
+    uint64_t* empty = full + kRing;
+    float* s_T = reinterpret_cast<float*>(empty + kRing);
 
-    // query vector (rows padded to dim_stride with zeros)
+    const float kInf = __int_as_float(0x7f800000);
+    const float kNegInf = __int_as_float(0xff800000);
+
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = tid; i < ix.dim_stride; i += kThreads)
         qv[i] = qg[i];
-    __syncthreads();
-    build_lut_smem(ix, qv, lut);
-    const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
-                                       p.np, st); // includes a barrier
-
-    WarpTopK<S> topk;
-    uint64_t dc = 0;
-    if (warp == 0)
-        topk.init(p.k);
     if (tid == 0) {
-        scal[0] = __float_as_uint(__int_as_float(0x7f800000));
-        scal[3] = 0;
+        for (uint32_t s = 0; s < kRing; ++s) {
+            mbar_init(full + s, kWorkers * kWarp);
+            mbar_init(empty + s, kWarp);
+        }
+        *s_T = kInf;
     }
     __syncthreads();
+    build_lut_blocked(ix, qv, lut);
+    const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
+                                       p.np, st); // ends with a barrier
+    const uint32_t nchunks = (total + kChunkW - 1) / kChunkW;
 
-    uint32_t pos = 0;
-    uint32_t chunk_want = p.first_chunk;
-    while (pos < total) {
-        // ---- segment table for [pos, pos+cn): warp 0 ----
-        if (warp == 0) {
-            const uint32_t first = pos < p.k ? max(p.k - pos, chunk_want) : chunk_want;
-            const uint32_t want_end = min(total, pos + min(first, static_cast<uint32_t>(kChunkMax)));
-            const uint32_t li0 = scal[3];
-            const uint32_t li = li0 + lane;
-            const bool in = li < p.np;
-            const uint32_t c0 = in ? st.cum[li] : total;
-            const uint32_t c1 = in ? st.cum[li + 1] : total;
-            const uint32_t sb = max(c0, pos);
-            const bool nonempty = in && c0 < want_end && c1 > sb;
-            const uint32_t mask = __ballot_sync(0xffffffffu, nonempty);
-            const uint32_t cover = (li0 + kWarp < p.np) ? st.cum[li0 + kWarp] : total;
-            const uint32_t end = min(want_end, cover);
-            if (nonempty) {
-                const uint32_t slot = __popc(mask & ((1u << lane) - 1u));
-                seg_rel[slot] = sb - pos;
-                seg_delta[slot] = static_cast<int64_t>(st.base[li]) - static_cast<int64_t>(c0);
-            }
-            const uint32_t consumed = __popc(__ballot_sync(0xffffffffu, in && c1 <= end));
-            if (lane == 0) {
-                scal[1] = end - pos;
-                scal[2] = __popc(mask);
-                scal[3] = li0 + consumed;
-            }
-        }
-        __syncthreads(); // (A) segments, cn, T
-
-        const uint32_t cn = scal[1];
-        const uint32_t nseg = scal[2];
-        const float T = __uint_as_float(scal[0]);
-
-        // ---- ADC + relaxed bound for the chunk, threshold frozen ----
-        uint32_t e_u[kChunkU];
-        float est_u[kChunkU];
-        uint32_t bal_u[kChunkU];
-#pragma unroll
-        for (int u = 0; u < kChunkU; ++u) {
-            const uint32_t r = static_cast<uint32_t>(u) * kThreads + tid;
-            bool surv = false;
-            e_u[u] = 0;
-            est_u[u] = 0.0f;
-            if (r < cn) {
-                uint32_t s = 0;
-                while (s + 1 < nseg && seg_rel[s + 1] <= r)
-                    ++s;
-                const uint32_t pp = pos + r;
-                const uint32_t e = static_cast<uint32_t>(static_cast<int64_t>(pp) + seg_delta[s]);
-                e_u[u] = e;
-                if (pp < p.k) {
-                    // seed (ivf.hpp:264-271): evaluated unconditionally, no ADC
-                    est_u[u] = __int_as_float(0xff800000);
-                    surv = true;
-                } else {
-                    const float a = adc_sum<M, KS>(lut, ix.codes + static_cast<size_t>(e) * ix.code_stride,
-                                                   ix.m, ix.ksub);
-                    const float est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
-                    est_u[u] = est;
-                    surv = est < T;
-                }
-            }
-            bal_u[u] = __ballot_sync(0xffffffffu, surv);
-            if (surv) {
-                const uint32_t slot = (static_cast<uint32_t>(u) * kWarps + warp) * kWarp +
-                                      __popc(bal_u[u] & ((1u << lane) - 1u));
-                s_e[slot] = e_u[u];
-                s_est[slot] = est_u[u];
-            }
-            if (lane == 0)
-                bin_cnt[u * kWarps + warp] = __popc(bal_u[u]);
-        }
-        __syncthreads(); // (B) survivors + bin counts
-
-        // ---- exact distances of the superset (lane per survivor) ----
-#pragma unroll
-        for (int u = 0; u < kChunkU; ++u) {
-            const uint32_t g = static_cast<uint32_t>(u) * kThreads + tid;
-            const uint32_t b = g >> 5;
-            if ((g & 31u) < bin_cnt[b]) {
-                const uint32_t id = __ldg(ix.list_ids + s_e[g]);
-                const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
-                s_d[g] = euclid_sq_vec4(qv, row, ix.dim);
-                s_e[g] = id;
-            }
-        }
-        __syncthreads(); // (C) distances
-
-        // ---- in-order replay with the live threshold: warp 0 ----
-        if (warp == 0) {
-            const uint32_t nz = __ballot_sync(0xffffffffu, bin_cnt[lane] != 0);
-            uint32_t bins = nz;
+    if (warp == 0) {
+        // ------------------------------------------------ replay warp
+        WarpTopK<S> topk;
+        topk.init(p.k);
+        uint64_t dc = 0;
+        for (uint32_t c = 0; c < nchunks; ++c) {
+            const uint32_t s = c % kRing;
+            mbar_wait(full + s, (c / kRing) & 1u);
+            const uint32_t* cnts = bin_cnt + s * kWorkers;
+            uint32_t bins = __ballot_sync(0xffffffffu, lane < kWorkers && cnts[lane] != 0);
             while (bins) {
-                const uint32_t b = __ffs(bins) - 1;
+                const uint32_t w = __ffs(bins) - 1;
                 bins &= bins - 1;
-                const uint32_t cnt = bin_cnt[b];
+                const uint32_t cnt = cnts[w];
+                const uint32_t g0 = s * kChunkW + w * kPerWorker;
                 for (uint32_t i = 0; i < cnt; ++i) {
-                    const uint32_t g = b * kWarp + i;
-                    const float est = s_est[g];
+                    const float est = s_est[g0 + i];
                     if (est < topk.wd) { // ivf.hpp:275 — prune on tie
                         ++dc;
-                        topk.offer(s_d[g], s_e[g]);
+                        topk.offer(s_d[g0 + i], s_e[g0 + i]);
                     }
                 }
             }
             if (lane == 0)
-                scal[0] = __float_as_uint(topk.wd);
+                *reinterpret_cast<volatile float*>(s_T) = topk.wd;
+            __syncwarp();
+            mbar_arrive(empty + s);
         }
-        pos += cn;
-        chunk_want = min(chunk_want * 2u, static_cast<uint32_t>(kChunkMax));
-        __syncthreads(); // (D) T published, buffers free
-    }
-
-    if (warp == 0) {
         uint32_t* io = p.ids_out + static_cast<size_t>(q) * p.k;
         float* dout = p.dist_out + static_cast<size_t>(q) * p.k;
         if (total < p.k) {
             for (uint32_t i = lane; i < p.k; i += kWarp) {
                 io[i] = kInvalidId;
-                dout[i] = __int_as_float(0x7f800000);
+                dout[i] = kInf;
             }
             if (lane == 0 && p.status)
                 atomicOr(p.status, 1u);
@@ -412,16 +355,110 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             topk.store_sorted(p.k, io, dout);
         }
         if (lane == 0 && p.counters) {
-            unsigned long long* c = p.counters + static_cast<size_t>(q) * 6;
+            unsigned long long* cc = p.counters + static_cast<size_t>(q) * 6;
             const uint64_t evaluated = total;
             const uint64_t seeds = min(static_cast<uint64_t>(p.k), evaluated);
-            c[0] = dc;                       // dc
-            c[1] = evaluated - seeds;        // edc
-            c[2] = evaluated - dc;           // pruned
-            c[3] = evaluated;                // evaluated
-            c[4] = 0;                        // hops
-            c[5] = ix.nlist;                 // coarse_dc (probe_order always runs)
+            cc[0] = dc;                // dc
+            cc[1] = evaluated - seeds; // edc
+            cc[2] = evaluated - dc;    // pruned
+            cc[3] = evaluated;         // evaluated
+            cc[4] = 0;                 // hops
+            cc[5] = ix.nlist;          // coarse_dc (probe_order always runs)
         }
+        return;
+    }
+
+    // ---------------------------------------------------- worker warps
+    const uint32_t w = warp - 1;
+    LaneAdc la;
+    la.init(lane, LutShape::of(m));
+    uint32_t li = 0; // list cursor (positions of a lane only increase)
+    struct Cand {
+        FastCode<M> fc;
+        float lx;
+        uint32_t e;
+        uint32_t kind; // 0: past the end, 1: seed, 2: candidate
+    };
+    struct Slot {
+        Cand c[kLaneU];
+    };
+    Slot sa, sb; // double buffer in registers (static names: no local-memory indexing)
+    auto fetch = [&](uint32_t c, Slot& d) {
+#pragma unroll
+        for (uint32_t u = 0; u < kLaneU; ++u) {
+            const uint32_t pp = c * kChunkW + w * kPerWorker + u * kWarp + lane;
+            Cand& x = d.c[u];
+            x.kind = 0;
+            x.e = 0;
+            x.lx = 0.0f;
+            if (c < nchunks && pp < total) {
+                while (st.cum[li + 1] <= pp)
+                    ++li;
+                x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
+                x.kind = pp < p.k ? 1u : 2u; // seeds (ivf.hpp:264-271): always evaluated
+                if (x.kind == 2u) {
+                    x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
+                    x.lx = __ldg(ix.lx + x.e);
+                }
+            }
+        }
+    };
+    auto process = [&](uint32_t c, Slot& cur) {
+        const uint32_t s = c % kRing;
+        if (c >= kRing)
+            mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
+        float T = ld_volatile(s_T);
+        if (T == kInf && c >= 1) { // the seeds are not replayed yet: wait for chunk c-1
+            mbar_wait(empty + (c - 1) % kRing, ((c - 1) / kRing) & 1u);
+            T = ld_volatile(s_T);
+        }
+        const uint32_t g0 = s * kChunkW + w * kPerWorker;
+        uint32_t n = 0;
+#pragma unroll
+        for (uint32_t u = 0; u < kLaneU; ++u) {
+            Cand& x = cur.c[u];
+            bool keep = x.kind == 1u;
+            if (x.kind == 2u)
+                keep = est_lower_bound(x.fc.sum(m, la), x.lx, p.two_gamma, p.adc_eps) < T;
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const uint32_t r = n + __popc(bal & ((1u << lane) - 1u));
+                s_e[g0 + r] = x.e;
+                s_est[g0 + r] = x.kind == 1u ? kNegInf : 0.0f;
+            }
+            n += __popc(bal);
+        }
+        __syncwarp();
+        for (uint32_t i = lane; i < n; i += kWarp) {
+            // reference-order ADC + est (conflict-free rotation over active lanes), exact L2
+            const uint32_t e = s_e[g0 + i];
+            float est = s_est[g0 + i];
+            if (est != kNegInf) {
+                const float a = adc_exact<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
+                est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
+            }
+            if (est < T) {
+                const uint32_t id = __ldg(ix.list_ids + e);
+                const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
+                s_d[g0 + i] = euclid_sq_vec4(qv, row, ix.dim);
+                s_e[g0 + i] = id;
+                s_est[g0 + i] = est;
+            } else {
+                s_est[g0 + i] = kInf; // pruned even at the published threshold
+            }
+        }
+        if (lane == 0)
+            bin_cnt[s * kWorkers + w] = n;
+        mbar_arrive(full + s);
+    };
+    fetch(0, sa);
+    for (uint32_t c = 0; c < nchunks; c += 2) {
+        fetch(c + 1, sb); // prefetch: loads in flight while chunk c is filtered
+        process(c, sa);
+        if (c + 1 >= nchunks)
+            break;
+        fetch(c + 2, sa);
+        process(c + 1, sb);
     }
 }
 
@@ -438,6 +475,7 @@ struct RangeParams {
     uint32_t np;
     const uint32_t* probe;
     float two_gamma;
+    float adc_eps;
     uint32_t slice;          // stream positions per CTA
     uint32_t cap;            // pool entries per query
     unsigned long long* keys;  // nq*cap
@@ -446,16 +484,14 @@ struct RangeParams {
     unsigned long long* evaluated; // nq (stream length), written by slice 0
 };
 
-__host__ __device__ inline size_t range_smem_bytes(uint32_t m, uint32_t ksub, uint32_t dim_stride,
+__host__ __device__ inline size_t range_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
                                                    uint32_t np) {
-    size_t b = 0;
-    b += sizeof(float) * m * ksub;
+    size_t b = lut_bytes(mt, m);
     b += sizeof(float) * dim_stride;
-    b = (b + 15) & ~size_t(15);
     b += sizeof(uint64_t) * np;
     b += sizeof(uint32_t) * (np + 1);
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint32_t) * kChunkMax; // survivor entries
+    b += sizeof(uint32_t) * kRangeChunk; // superset entries
     b += sizeof(uint32_t) * 8;
     return b;
 }
@@ -463,13 +499,13 @@ __host__ __device__ inline size_t range_smem_bytes(uint32_t m, uint32_t ksub, ui
 template <int M, int KS>
 __global__ void __launch_bounds__(kThreads)
 trim_range_kernel(DevIndex ix, RangeParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     const uint32_t q = blockIdx.y;
-    const uint32_t tid = threadIdx.x;
-    float* qv = reinterpret_cast<float*>(smem); // dim_stride % 4 == 0: lut stays 16B-aligned
-    float* lut = qv + ix.dim_stride;
-    size_t off = sizeof(float) * (ix.m * ix.ksub + ix.dim_stride);
-    off = (off + 15) & ~size_t(15);
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m;
+    float* lut = reinterpret_cast<float*>(smem);
+    float* qv = lut + lut_bytes(M, m) / sizeof(float);
+    size_t off = lut_bytes(M, m) + sizeof(float) * ix.dim_stride;
     StreamSmem st;
     st.base = reinterpret_cast<uint64_t*>(smem + off);
     off += sizeof(uint64_t) * p.np;
@@ -477,7 +513,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     off += sizeof(uint32_t) * (p.np + 1);
     off = (off + 15) & ~size_t(15);
     uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);
-    uint32_t* scal = s_e + kChunkMax; // [0] survivor count
+    uint32_t* scal = s_e + kRangeChunk; // [0] superset count
 
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = tid; i < ix.dim_stride; i += kThreads)
@@ -490,42 +526,43 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     if (begin >= total)
         return;
     const uint32_t end = min(total, begin + p.slice);
-    build_lut_smem(ix, qv, lut);
+    build_lut_blocked(ix, qv, lut);
     const float r2 = p.radius_sq[q];
+    LaneAdc la;
+    la.init(lane, LutShape::of(m));
 
-    // list cursor: first list whose range contains `begin`
-    uint32_t li = 0;
-    {
-        uint32_t lo = 0, hi = p.np; // find last li with cum[li] <= begin
-        while (lo + 1 < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (st.cum[mid] <= begin)
-                lo = mid;
-            else
-                hi = mid;
-        }
-        li = lo;
+    // first list whose range contains `begin`
+    uint32_t lo = 0, hi = p.np;
+    while (lo + 1 < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (st.cum[mid] <= begin)
+            lo = mid;
+        else
+            hi = mid;
     }
+    uint32_t li[kRangeU];
+#pragma unroll
+    for (int u = 0; u < kRangeU; ++u)
+        li[u] = lo;
     uint32_t dc_local = 0;
     if (tid == 0)
         scal[0] = 0;
     __syncthreads();
 
-    for (uint32_t pos = begin; pos < end; pos += kChunkMax) {
-        const uint32_t cn = min(static_cast<uint32_t>(kChunkMax), end - pos);
+    for (uint32_t pos = begin; pos < end; pos += kRangeChunk) {
+        const uint32_t cn = min(static_cast<uint32_t>(kRangeChunk), end - pos);
 #pragma unroll
-        for (int u = 0; u < kChunkU; ++u) {
+        for (int u = 0; u < kRangeU; ++u) {
             const uint32_t r = static_cast<uint32_t>(u) * kThreads + tid;
             if (r < cn) {
                 const uint32_t pp = pos + r;
-                uint32_t l = li;
-                while (st.cum[l + 1] <= pp)
-                    ++l;
-                const uint32_t e = static_cast<uint32_t>(st.base[l] + (pp - st.cum[l]));
-                const float a = adc_sum<M, KS>(lut, ix.codes + static_cast<size_t>(e) * ix.code_stride,
-                                               ix.m, ix.ksub);
-                const float est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
-                if (est <= r2) {
+                while (st.cum[li[u] + 1] <= pp)
+                    ++li[u];
+                const uint32_t e = static_cast<uint32_t>(st.base[li[u]] + (pp - st.cum[li[u]]));
+                FastCode<M> fc;
+                fc.load(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
+                const float a = fc.sum(m, la);
+                if (est_lower_bound(a, __ldg(ix.lx + e), p.two_gamma, p.adc_eps) <= r2) {
                     const uint32_t slot = atomicAdd(&scal[0], 1u);
                     s_e[slot] = e;
                 }
@@ -533,26 +570,31 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
         }
         __syncthreads();
         const uint32_t ns = scal[0];
-        dc_local += ns;
         for (uint32_t i = tid; i < ns; i += kThreads) {
-            const uint32_t id = __ldg(ix.list_ids + s_e[i]);
-            const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
-            const float d = euclid_sq_vec4(qv, row, ix.dim);
-            if (d <= r2) {
-                const uint32_t slot = atomicAdd(p.count + q, 1u);
-                if (slot < p.cap)
-                    p.keys[static_cast<size_t>(q) * p.cap + slot] = scored_key(d, id);
+            const uint32_t e = s_e[i];
+            const float a = adc_exact<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
+            const float est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
+            if (est <= r2) { // ivf.hpp:331
+                ++dc_local;
+                const uint32_t id = __ldg(ix.list_ids + e);
+                const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
+                const float d = euclid_sq_vec4(qv, row, ix.dim);
+                if (d <= r2) { // ivf.hpp:334
+                    const uint32_t slot = atomicAdd(p.count + q, 1u);
+                    if (slot < p.cap)
+                        p.keys[static_cast<size_t>(q) * p.cap + slot] = scored_key(d, id);
+                }
             }
         }
-        // advance the list cursor past lists fully before the next chunk
-        while (li + 1 < p.np && st.cum[li + 1] <= pos + cn)
-            ++li;
         __syncthreads();
         if (tid == 0)
             scal[0] = 0;
         __syncthreads();
     }
-    if (tid == 0 && dc_local)
+    // block-wide sum of exact evaluations
+    for (int o = 16; o > 0; o >>= 1)
+        dc_local += __shfl_xor_sync(0xffffffffu, dc_local, o);
+    if (lane == 0 && dc_local)
         atomicAdd(p.dc + q, static_cast<unsigned long long>(dc_local));
 }
 
@@ -565,7 +607,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
 __global__ void __launch_bounds__(kThreads)
 trim_probe_kernel(DevIndex ix, const float* queries, uint64_t nq, uint32_t np, uint32_t nl_pow2,
                   uint32_t* probe_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     const uint32_t q = blockIdx.x;
     float* qv = reinterpret_cast<float*>(smem);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + sizeof(float) * ((ix.dim_stride + 3) & ~3u));
@@ -605,7 +647,7 @@ trim_probe_kernel(DevIndex ix, const float* queries, uint64_t nq, uint32_t np, u
 // pq::build_distance_table to global memory (one CTA per query).
 __global__ void __launch_bounds__(kThreads)
 trim_lut_kernel(DevIndex ix, const float* queries, float* lut_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     float* qv = reinterpret_cast<float*>(smem);
     const uint32_t q = blockIdx.x;
     for (uint32_t i = threadIdx.x; i < ix.dim_stride; i += blockDim.x)
@@ -631,7 +673,7 @@ __global__ void trim_unpack_keys_kernel(const unsigned long long* keys, uint32_t
 __global__ void __launch_bounds__(kThreads)
 trim_merge_kernel(const float* dist, const uint32_t* ids, uint32_t nshards, uint64_t nq,
                   uint32_t k, uint32_t n_pow2, float* dist_out, uint32_t* ids_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char* smem = trim_dyn_smem;
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     const uint32_t q = blockIdx.x;
     const uint32_t n = nshards * k;

@@ -182,24 +182,53 @@ __device__ __forceinline__ void permute_block(uint32_t w[8], uint32_t l) {
     }
 }
 
-// Any-order sum of one block; lane reads column l ^ s at step s. ROWB = row
-// bytes; IMM = block byte offset (folds into the LDS immediate). Four partial
-// sums keep four independent FADD chains in flight.
-template <int STEPS, uint32_t ROWB, uint32_t IMM>
-__device__ __forceinline__ float block_fast(uint32_t lbase, const uint32_t w[8], const LaneAdc& la,
-                                            float acc) {
-    float part[4] = {acc, 0.0f, 0.0f, 0.0f};
+// Any-order sum of steps [S0, S1) of one block; lane reads column l ^ s at
+// step s. ROWB = row bytes; IMM = block byte offset (folds into the LDS
+// immediate). Four partial sums keep four independent FADD chains in flight.
+template <int S0, int S1, uint32_t ROWB, uint32_t IMM>
+__device__ __forceinline__ void block_fast(uint32_t lbase, const uint32_t w[8], const LaneAdc& la,
+                                           float part[4]) {
 #pragma unroll
-    for (int s = 0; s < STEPS; ++s) {
+    for (int s = S0; s < S1; ++s) {
         const uint32_t c = __byte_perm(w[s >> 2], 0, la.sel[s & 3]);
         const uint32_t col = lbase ^ (static_cast<uint32_t>(s) << 2);
         part[s & 3] = __fadd_rn(part[s & 3], lds_f32(c * ROWB + col + IMM));
     }
-    return __fadd_rn(__fadd_rn(part[0], part[1]), __fadd_rn(part[2], part[3]));
 }
 
-// Fast ADC split into load (global -> registers) and sum, so a thread can
-// have the next candidate's loads in flight while it sums the current one.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Early-exit test on a PARTIAL any-order ADC sum a_p (a subset of the m
+// non-negative LUT terms, so adc_ref >= a_p(1-eps)). est(g) = (g-x)^2 +
+// 2*gamma*g*x is increasing for g >= (1-gamma)*x; if g_lo = sqrt(a_p(1-eps))
+// is already there, est_ref >= est(g_lo) and the candidate is provably
+// pruned when that (rounded down, then shrunk by 4u for the reference's own
+// rounding) is >= T. omg_hi = 1 - gamma rounded up.
+struct StageCheck {
+    float glx, two_gamma, omg_hi, eps, T;
+    __device__ __forceinline__ bool pruned(float a_p) const {
+        const float g_lo = __fmul_rd(sqrt_approx(__fmul_rd(a_p, 1.0f - eps)), 1.0f - 1.0f / 65536.0f);
+        if (!(g_lo >= __fmul_ru(omg_hi, glx)))
+            return false;
+        const float d_lo = __fsub_rd(g_lo, glx), d_hi = __fsub_ru(g_lo, glx);
+        const float e = d_lo >= 0.0f ? __fmul_rd(d_lo, d_lo) : (d_hi <= 0.0f ? __fmul_rd(d_hi, d_hi) : 0.0f);
+        const float t = __fmul_rd(__fmul_rd(two_gamma, g_lo), glx);
+        return __fmul_rd(__fadd_rd(e, t), 1.0f - 4.0f / 16777216.0f) >= T;
+    }
+};
+
+__device__ __forceinline__ float sum4(const float p[4]) {
+    return __fadd_rn(__fadd_rn(p[0], p[1]), __fadd_rn(p[2], p[3]));
+}
+
+// Fast ADC split into load (global -> registers) and a staged sum, so a
+// thread can have the next candidate's loads in flight while it sums the
+// current one, and a warp whose candidates are all provably pruned stops
+// after the first 16 (or 32, 64, ...) subspaces.
 template <int M>
 struct FastCode {
     static constexpr uint32_t kMaxB = M > 0 ? (static_cast<uint32_t>(M) + 31) / 32 : 4;
@@ -216,34 +245,72 @@ struct FastCode {
         }
     }
 
-    template <uint32_t B>
-    __device__ __forceinline__ float sum_block(const LutShape& sh, const LaneAdc& la, float acc) {
-        if (B < sh.nfull) {
-            permute_block<false>(w[B], la.l);
-            return block_fast<32, 128u, B * kFullBytes>(la.lf, w[B], la, acc);
-        }
-        if (B == sh.nfull && sh.half) {
-            permute_block<true>(w[B], la.l);
-            if (M > 0 && !LutShape::of(static_cast<uint32_t>(M)).hdup)
-                return block_fast<16, 64u, 0u>(la.lh, w[B], la, acc);
-            return sh.hdup ? block_fast<16, 128u, 0u>(la.lh, w[B], la, acc)
-                           : block_fast<16, 64u, 0u>(la.lh, w[B], la, acc);
-        }
-        return acc;
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (uint32_t b = 0; b < kMaxB; ++b)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                w[b][i] = 0;
     }
 
-    // Consumes the loaded words (permutes them in place).
-    __device__ __forceinline__ float sum(uint32_t m, const LaneAdc& la) {
+    // One FULL block B (compile-time), two 16-step stages. Returns true when
+    // the whole warp is provably pruned.
+    template <uint32_t B>
+    __device__ __forceinline__ bool full_block(const LutShape& sh, const LaneAdc& la, const StageCheck& ck,
+                                               float part[4], bool& live) {
+        if (B >= sh.nfull)
+            return false;
+        permute_block<false>(w[B], la.l);
+        block_fast<0, 16, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+        if (live && ck.pruned(sum4(part)))
+            live = false;
+        if (!__any_sync(0xffffffffu, live))
+            return true;
+        block_fast<16, 32, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+        if (B + 1 == sh.nfull && !sh.half)
+            return false; // last block: the caller's full check decides
+        if (live && ck.pruned(sum4(part)))
+            live = false;
+        return !__any_sync(0xffffffffu, live);
+    }
+
+    // Full any-order sum, or a negative value if a stage proved est >= T for
+    // this lane. `alive` = this lane has a candidate; dead lanes still step
+    // along (their lookups keep the schedule conflict-free) but never vote.
+    // Warp-collective.
+    __device__ __forceinline__ float sum_staged(uint32_t m, const LaneAdc& la, const StageCheck& ck,
+                                                bool alive) {
         const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
-        float acc = 0.0f;
-        acc = sum_block<0>(sh, la, acc);
-        if (kMaxB > 1)
-            acc = sum_block<(kMaxB > 1 ? 1 : 0)>(sh, la, acc);
-        if (kMaxB > 2)
-            acc = sum_block<(kMaxB > 2 ? 2 : 0)>(sh, la, acc);
-        if (kMaxB > 3)
-            acc = sum_block<(kMaxB > 3 ? 3 : 0)>(sh, la, acc);
-        return acc;
+        float part[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        bool live = alive;
+        if (full_block<0>(sh, la, ck, part, live))
+            return -1.0f;
+        if (kMaxB > 1 && full_block<(kMaxB > 1 ? 1u : 0u)>(sh, la, ck, part, live))
+            return -1.0f;
+        if (kMaxB > 2 && full_block<(kMaxB > 2 ? 2u : 0u)>(sh, la, ck, part, live))
+            return -1.0f;
+        if (kMaxB > 3 && full_block<(kMaxB > 3 ? 3u : 0u)>(sh, la, ck, part, live))
+            return -1.0f;
+        if (sh.half) {
+            const uint32_t hb = sh.nfull;
+            uint32_t* wh = w[0];
+#pragma unroll
+            for (uint32_t b = 1; b < kMaxB; ++b)
+                if (b == hb)
+                    wh = w[b];
+            permute_block<true>(wh, la.l);
+            if (sh.hdup) { // the only block (m <= 16): one early check after 8 steps
+                block_fast<0, 8, 128u, 0u>(la.lh, wh, la, part);
+                if (live && ck.pruned(sum4(part)))
+                    live = false;
+                if (!__any_sync(0xffffffffu, live))
+                    return -1.0f;
+                block_fast<8, 16, 128u, 0u>(la.lh, wh, la, part);
+            } else {
+                block_fast<0, 16, 64u, 0u>(la.lh, wh, la, part);
+            }
+        }
+        return live ? sum4(part) : -1.0f;
     }
 };
 
@@ -344,18 +411,14 @@ __device__ __forceinline__ float adc_exact(const uint8_t* __restrict__ code, uin
 // either result (gamma_k = k*u/(1-k*u), u = 2^-24; Higham, "Accuracy and
 // Stability of Numerical Algorithms", eq. 4.4). The fast sum adds +0.0f
 // zero-padding terms and at most 6 extra partial-sum combines per block;
-// adc_rel_eps(m) uses k = m + 8*blocks and doubles the bound.
+// adc_rel_eps(m) uses k = m + 8*blocks and doubles the bound. The same eps
+// bounds a partial sum from above by the reference's full sum (the omitted
+// terms are non-negative).
 __host__ __device__ inline float adc_rel_eps(uint32_t m) {
     const double u = 1.0 / 16777216.0;
     const double k = static_cast<double>(m + 8 * LutShape::of(m).blocks());
     const double g = k * u / (1.0 - k * u);
     return static_cast<float>(2.0 * (2.0 * g / (1.0 - g)));
-}
-
-__device__ __forceinline__ float sqrt_approx(float x) {
-    float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
 }
 
 // Lower bound on the reference's est = relaxed_lb(sqrt(adc_ref), glx, gamma)

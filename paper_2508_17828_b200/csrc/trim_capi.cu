@@ -206,6 +206,16 @@ void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+// 1 - gamma rounded up to a float (the stage check needs an upper bound on
+// (1 - gamma) * glx).
+float omg_round_up(float gamma) {
+    const double exact = 1.0 - static_cast<double>(gamma);
+    float f = static_cast<float>(exact);
+    if (static_cast<double>(f) < exact)
+        f = std::nextafter(f, 2.0f);
+    return f;
+}
+
 // The kernel specialisation (m template value) launch_* will pick.
 int dispatch_m(const DevIndex& ix) {
     if (ix.ksub == 256 && (ix.m == 16 || ix.m == 32 || ix.m == 48 || ix.m == 120))
@@ -281,6 +291,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.probe = d_probe;
     p.two_gamma = 2.0f * gamma;
     p.adc_eps = adc_rel_eps(ix->dev.m);
+    p.omg_hi = omg_round_up(gamma);
     p.ids_out = d_ids;
     p.dist_out = d_dist;
     p.counters = d_ct;
@@ -724,6 +735,7 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
             p.np = np;
             p.two_gamma = 2.0f * gamma;
             p.adc_eps = adc_rel_eps(ix->dev.m);
+            p.omg_hi = omg_round_up(gamma);
             p.slice = slice;
             p.cap = cap;
             for (uint64_t b = 0; b < nq; b += 65535) {

@@ -189,6 +189,7 @@ struct KnnParams {
     const uint32_t* probe;   // nq*np list ids, or null when nlist == 1
     float two_gamma;
     float adc_eps;           // adc_rel_eps(m)
+    float omg_hi;            // 1 - gamma, rounded up
     uint32_t* ids_out;       // nq*k
     float* dist_out;         // nq*k
     unsigned long long* counters; // nq*6
@@ -401,6 +402,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     x.lx = __ldg(ix.lx + x.e);
                 }
             }
+            if (x.kind != 2u) // dead lanes still step through the schedule: valid rows
+                x.fc.zero();
         }
     };
     auto process = [&](uint32_t c, Slot& cur) {
@@ -417,9 +420,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
 #pragma unroll
         for (uint32_t u = 0; u < kLaneU; ++u) {
             Cand& x = cur.c[u];
+            const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
+            const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
             bool keep = x.kind == 1u;
-            if (x.kind == 2u)
-                keep = est_lower_bound(x.fc.sum(m, la), x.lx, p.two_gamma, p.adc_eps) < T;
+            if (x.kind == 2u && a >= 0.0f)
+                keep = est_lower_bound(a, x.lx, p.two_gamma, p.adc_eps) < T;
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const uint32_t r = n + __popc(bal & ((1u << lane) - 1u));
@@ -476,6 +481,7 @@ struct RangeParams {
     const uint32_t* probe;
     float two_gamma;
     float adc_eps;
+    float omg_hi;            // 1 - gamma, rounded up
     uint32_t slice;          // stream positions per CTA
     uint32_t cap;            // pool entries per query
     unsigned long long* keys;  // nq*cap
@@ -530,6 +536,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     const float r2 = p.radius_sq[q];
     LaneAdc la;
     la.init(lane, LutShape::of(m));
+    const float r2_excl = __int_as_float(__float_as_int(r2) + 1); // smallest float > r2 (r2 >= 0)
 
     // first list whose range contains `begin`
     uint32_t lo = 0, hi = p.np;
@@ -554,18 +561,24 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
 #pragma unroll
         for (int u = 0; u < kRangeU; ++u) {
             const uint32_t r = static_cast<uint32_t>(u) * kThreads + tid;
-            if (r < cn) {
+            const bool valid = r < cn;
+            uint32_t e = 0;
+            float glx = 0.0f;
+            FastCode<M> fc;
+            fc.zero();
+            if (valid) {
                 const uint32_t pp = pos + r;
                 while (st.cum[li[u] + 1] <= pp)
                     ++li[u];
-                const uint32_t e = static_cast<uint32_t>(st.base[li[u]] + (pp - st.cum[li[u]]));
-                FastCode<M> fc;
+                e = static_cast<uint32_t>(st.base[li[u]] + (pp - st.cum[li[u]]));
                 fc.load(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
-                const float a = fc.sum(m, la);
-                if (est_lower_bound(a, __ldg(ix.lx + e), p.two_gamma, p.adc_eps) <= r2) {
-                    const uint32_t slot = atomicAdd(&scal[0], 1u);
-                    s_e[slot] = e;
-                }
+                glx = __ldg(ix.lx + e);
+            }
+            const StageCheck ck{glx, p.two_gamma, p.omg_hi, p.adc_eps, r2_excl};
+            const float a = fc.sum_staged(m, la, ck, valid); // warp-collective: every lane calls
+            if (valid && a >= 0.0f && est_lower_bound(a, glx, p.two_gamma, p.adc_eps) <= r2) {
+                const uint32_t slot = atomicAdd(&scal[0], 1u);
+                s_e[slot] = e;
             }
         }
         __syncthreads();

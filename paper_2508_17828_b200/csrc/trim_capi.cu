@@ -225,19 +225,39 @@ int dispatch_m(const DevIndex& ix) {
 
 // Probe lists for a query batch (d_q rows padded to dim_stride). Returns
 // the effective per-query probe count; d_probe is null when nlist == 1.
+// probe_order for a batch into d_out (nq*np): the tiled kernel when np and the
+// distance table fit its shared-memory plan, else the one-query bitonic kernel.
+void launch_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t np, uint32_t* d_out,
+                  cudaStream_t st) {
+    const DevIndex& v = ix->dev;
+    if (np <= kProbeMaxNp) {
+        for (uint32_t tile = 128; tile >= 32; tile >>= 1) {
+            const size_t smem = probe_tiled_smem(v.nlist, v.dim_stride, tile);
+            if (smem <= kSmemLimit) {
+                CK(cudaFuncSetAttribute(trim_probe_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+                const unsigned grid = static_cast<unsigned>((nq + kProbeQ - 1) / kProbeQ);
+                trim_probe_tiled_kernel<<<grid, kThreads, smem, st>>>(v, d_q, nq, np, tile, d_out);
+                CK(cudaGetLastError());
+                return;
+            }
+        }
+    }
+    const uint32_t nl2 = pow2_at_least(v.nlist);
+    const size_t smem = sizeof(float) * v.dim_stride + sizeof(uint64_t) * nl2;
+    CK(cudaFuncSetAttribute(trim_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    trim_probe_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(v, d_q, nq, np, nl2, d_out);
+    CK(cudaGetLastError());
+}
+
 uint32_t run_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t nprobe,
                    DevBuf& d_probe, cudaStream_t st) {
     const uint32_t np = std::min(nprobe, ix->dev.nlist);
     if (ix->dev.nlist == 1 || np == 0 || nq == 0)
         return np;
-    const uint32_t nl2 = pow2_at_least(ix->dev.nlist);
-    const size_t smem = sizeof(float) * ix->dev.dim_stride + sizeof(uint64_t) * nl2;
     d_probe = DevBuf(sizeof(uint32_t) * nq * np, st);
-    CK(cudaFuncSetAttribute(trim_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    trim_probe_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(
-        ix->dev, d_q, nq, np, nl2, d_probe.as<uint32_t>());
-    CK(cudaGetLastError());
+    launch_probe(ix, d_q, nq, np, d_probe.as<uint32_t>(), st);
     return np;
 }
 
@@ -652,13 +672,7 @@ int trim_probe_device(trim_index_t ix, const float* d_queries, uint64_t nq, uint
             CK(cudaMemsetAsync(d_lists, 0, sizeof(uint32_t) * nq * np, st));
             return TRIM_OK;
         }
-        const uint32_t nl2 = pow2_at_least(ix->dev.nlist);
-        const size_t smem = sizeof(float) * ix->dev.dim_stride + sizeof(uint64_t) * nl2;
-        CK(cudaFuncSetAttribute(trim_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-        trim_probe_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(ix->dev, d_queries, nq, np,
-                                                                             nl2, d_lists);
-        CK(cudaGetLastError());
+        launch_probe(ix, d_queries, nq, np, d_lists, st);
         return TRIM_OK;
     });
 }

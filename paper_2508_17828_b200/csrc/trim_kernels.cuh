@@ -657,6 +657,190 @@ trim_probe_kernel(DevIndex ix, const float* queries, uint64_t nq, uint32_t np, u
         probe_out[static_cast<size_t>(q) * np + i] = static_cast<uint32_t>(keys[i] & 0xffffffffu);
 }
 
+// --------------------------------------------------------------------------
+// trim_probe_tiled_kernel — probe_order (ivf.hpp:173-187) for kProbeQ queries
+// per CTA: centroid tiles are staged transposed in shared memory
+// ([dim/4][tile][float4], conflict-free float4 reads), every (query,
+// centroid) distance uses the reference's 4-accumulator order, and warp w
+// then selects query w's np smallest (dist, list id) by an 8-bit radix
+// select over the distance bits (ties resolved by ascending list id, as
+// std::sort on ScoredId does) and sorts them with a warp bitonic sort.
+// Requires np <= kProbeMaxNp.
+// --------------------------------------------------------------------------
+constexpr uint32_t kProbeQ = 8;        // queries per CTA (one selecting warp each)
+constexpr uint32_t kProbeMaxNp = 256;
+
+__host__ __device__ inline size_t probe_tiled_smem(uint32_t nlist, uint32_t dim_stride, uint32_t tile) {
+    return sizeof(float) * kProbeQ * dim_stride          // queries
+         + sizeof(float) * dim_stride * tile              // centroid tile (transposed)
+         + sizeof(uint32_t) * kProbeQ * nlist             // distance bits
+         + kProbeQ * (sizeof(uint32_t) * 256 + sizeof(uint64_t) * kProbeMaxNp); // hist + sort
+}
+
+__global__ void __launch_bounds__(kThreads)
+trim_probe_tiled_kernel(DevIndex ix, const float* queries, uint64_t nq, uint32_t np, uint32_t tile,
+                        uint32_t* probe_out) {
+    unsigned char* smem = trim_dyn_smem;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q0 = static_cast<uint64_t>(blockIdx.x) * kProbeQ;
+    const uint32_t ds = ix.dim_stride, nv = ds >> 2, nlist = ix.nlist;
+    const uint32_t full4 = ix.dim >> 2, tail = ix.dim & 3u;
+    float* qs = reinterpret_cast<float*>(smem);
+    float4* ct = reinterpret_cast<float4*>(qs + kProbeQ * ds); // [nv][tile]
+    uint32_t* keys = reinterpret_cast<uint32_t*>(ct + static_cast<size_t>(nv) * tile); // [kProbeQ][nlist]
+    uint32_t* hist = keys + static_cast<size_t>(kProbeQ) * nlist;                        // [kProbeQ][256]
+    uint64_t* sel = reinterpret_cast<uint64_t*>(hist + kProbeQ * 256);                   // [kProbeQ][kProbeMaxNp]
+
+    for (uint32_t i = tid; i < kProbeQ * ds; i += kThreads) {
+        const uint64_t qq = q0 + i / ds;
+        qs[i] = qq < nq ? queries[qq * ds + i % ds] : 0.0f;
+    }
+    // ---- distances: warp w -> query w, lane -> centroids lane + 32j of the tile
+    const float4* qv4 = reinterpret_cast<const float4*>(qs + warp * ds);
+    const uint32_t per = tile / 32;
+    for (uint32_t c0 = 0; c0 < nlist; c0 += tile) {
+        __syncthreads();
+        for (uint32_t i = tid; i < nv * tile; i += kThreads) {
+            const uint32_t c = i % tile, v = i / tile;
+            ct[v * tile + c] = (c0 + c < nlist)
+                ? *reinterpret_cast<const float4*>(ix.coarse + static_cast<size_t>(c0 + c) * ds + 4 * v)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        for (uint32_t j = 0; j < per; ++j) {
+            const uint32_t c = lane + 32 * j;
+            float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+            for (uint32_t v = 0; v < full4; ++v) {
+                const float4 a = qv4[v];
+                const float4 b = ct[v * tile + c];
+                const float d0 = __fsub_rn(a.x, b.x), d1 = __fsub_rn(a.y, b.y);
+                const float d2 = __fsub_rn(a.z, b.z), d3 = __fsub_rn(a.w, b.w);
+                a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+                a1 = __fadd_rn(a1, __fmul_rn(d1, d1));
+                a2 = __fadd_rn(a2, __fmul_rn(d2, d2));
+                a3 = __fadd_rn(a3, __fmul_rn(d3, d3));
+            }
+            if (tail) { // distance.hpp:23-26: the remainder goes into acc0, in order
+                const float4 a = qv4[full4];
+                const float4 b = ct[full4 * tile + c];
+                const float d0 = __fsub_rn(a.x, b.x);
+                a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+                if (tail > 1) {
+                    const float d1 = __fsub_rn(a.y, b.y);
+                    a0 = __fadd_rn(a0, __fmul_rn(d1, d1));
+                }
+                if (tail > 2) {
+                    const float d2 = __fsub_rn(a.z, b.z);
+                    a0 = __fadd_rn(a0, __fmul_rn(d2, d2));
+                }
+            }
+            if (c0 + c < nlist)
+                keys[warp * nlist + c0 + c] = __float_as_uint(__fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3)));
+        }
+    }
+    __syncthreads();
+    const uint64_t q = q0 + warp;
+    if (q >= nq)
+        return;
+    // ---- radix select of the np-th smallest distance bits (non-negative floats
+    // order like their bit patterns)
+    const uint32_t* kq = keys + warp * nlist;
+    uint32_t* h = hist + warp * 256;
+    uint32_t prefix = 0, pmask = 0, rank = np; // rank: 1-based among keys matching prefix
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t i = lane; i < 256; i += 32)
+            h[i] = 0;
+        __syncwarp();
+        for (uint32_t c = lane; c < nlist; c += 32) {
+            const uint32_t kk = kq[c];
+            if ((kk & pmask) == prefix)
+                atomicAdd(&h[(kk >> shift) & 0xFFu], 1u);
+        }
+        __syncwarp();
+        // bucket b with cum(b) < rank <= cum(b) + h[b]: lane owns bins 8*lane..8*lane+7
+        uint32_t loc[8], s = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            loc[i] = h[8 * lane + i];
+            s += loc[i];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<uint32_t>(o))
+                incl += t;
+        }
+        const uint32_t excl = incl - s;
+        const bool mine = excl < rank && rank <= incl;
+        uint32_t bucket = 0, before = 0;
+        if (mine) {
+            uint32_t cum = excl;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (cum + loc[i] >= rank) {
+                    bucket = 8 * lane + i;
+                    before = cum;
+                    break;
+                }
+                cum += loc[i];
+            }
+        }
+        const uint32_t src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        bucket = __shfl_sync(0xffffffffu, bucket, src);
+        before = __shfl_sync(0xffffffffu, before, src);
+        prefix |= bucket << shift;
+        pmask |= 0xFFu << shift;
+        rank -= before;
+        __syncwarp();
+    }
+    // prefix = the np-th smallest distance bits; take every key below it and
+    // the first `rank` keys equal to it in ascending list-id order
+    uint64_t* sq = sel + warp * kProbeMaxNp;
+    uint32_t n_lt = 0, n_eq = 0;
+    for (uint32_t c0 = 0; c0 < nlist; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const uint32_t kk = c < nlist ? kq[c] : 0xFFFFFFFFu;
+        const bool lt = c < nlist && kk < prefix;
+        const bool eq = c < nlist && kk == prefix;
+        const uint32_t blt = __ballot_sync(0xffffffffu, lt);
+        const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+        const uint32_t below = (1u << lane) - 1u;
+        if (lt)
+            sq[n_lt + __popc(blt & below)] = (static_cast<uint64_t>(kk) << 32) | c;
+        if (eq) {
+            const uint32_t r = n_eq + __popc(beq & below);
+            if (r < rank)
+                sq[np - rank + r] = (static_cast<uint64_t>(kk) << 32) | c;
+        }
+        n_lt += __popc(blt);
+        n_eq += __popc(beq);
+    }
+    // pad to a power of two and bitonic-sort (warp, shared memory)
+    uint32_t n2 = 1;
+    while (n2 < np)
+        n2 <<= 1;
+    for (uint32_t i = np + lane; i < n2; i += 32)
+        sq[i] = ~0ull;
+    __syncwarp();
+    for (uint32_t size = 2; size <= n2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < n2 / 2; i += 32) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = sq[lo], b = sq[hi];
+                if ((a > b) == up) {
+                    sq[lo] = b;
+                    sq[hi] = a;
+                }
+            }
+            __syncwarp();
+        }
+    for (uint32_t i = lane; i < np; i += 32)
+        probe_out[q * np + i] = static_cast<uint32_t>(sq[i] & 0xffffffffu);
+}
+
 // pq::build_distance_table to global memory (one CTA per query).
 __global__ void __launch_bounds__(kThreads)
 trim_lut_kernel(DevIndex ix, const float* queries, float* lut_out) {

@@ -245,12 +245,18 @@ struct FastCode {
         }
     }
 
-    __device__ __forceinline__ void zero() {
+    // Zero exactly the words load() would write (dead lanes still step through
+    // the schedule; unused words must stay dead for the register allocator).
+    __device__ __forceinline__ void zero(uint32_t m) {
+        const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
 #pragma unroll
-        for (uint32_t b = 0; b < kMaxB; ++b)
+        for (uint32_t b = 0; b < kMaxB; ++b) {
+            const uint32_t nw = b < sh.nfull ? 8u : (b == sh.nfull && sh.half ? 4u : 0u);
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                w[b][i] = 0;
+            for (uint32_t i = 0; i < 8; ++i)
+                if (i < nw)
+                    w[b][i] = 0;
+        }
     }
 
     // One FULL block B (compile-time), two 16-step stages. Returns true when

@@ -403,7 +403,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 }
             }
             if (x.kind != 2u) // dead lanes still step through the schedule: valid rows
-                x.fc.zero();
+                x.fc.zero(m);
         }
     };
     auto process = [&](uint32_t c, Slot& cur) {
@@ -565,7 +565,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
             uint32_t e = 0;
             float glx = 0.0f;
             FastCode<M> fc;
-            fc.zero();
+            fc.zero(m);
             if (valid) {
                 const uint32_t pp = pos + r;
                 while (st.cum[li[u] + 1] <= pp)

@@ -125,7 +125,7 @@ def ncu_traffic(workload: str):
 
 
 # ------------------------------------------------------------------- data
-def build_workload(cfg, rank: int, world: int, device: int):
+def build_workload(cfg, rank: int, world: int, device: int, sharded: bool = False):
     """Seeded synthetic data + index on the device. Rank r holds the id-shard
     [r*n, (r+1)*n) (weak scaling); codebook and coarse quantizer are trained
     on rank 0 and broadcast so every shard probes identically."""
@@ -141,7 +141,7 @@ def build_workload(cfg, rank: int, world: int, device: int):
     base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1 + 7919 * rank)
     queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
     p = B.BuildParams(m=cfg["m"], nlist=cfg["nlist"], pq_seed=3, ivf_seed=4)
-    if world == 1:
+    if not sharded:
         arrays = B.build_ivf(base, p)
     else:
         import torch.distributed as dist
@@ -182,12 +182,16 @@ def run_ours(args, cfg):
     from paper_2508_17828_b200 import ivf as G
 
     world, rank, local = dist_env()
-    if world > 1:
+    sharded = world > 1 or args.force_shard
+    if sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    arrays, queries = build_workload(cfg, rank, world, local)
+    arrays, queries = build_workload(cfg, rank, world, local, sharded)
     gix = G.GpuIvfIndex(arrays, device=local)
     lib = _lib.load()
     import ctypes as C
@@ -202,10 +206,10 @@ def run_ours(args, cfg):
     cts = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     batches = [(b, min(B, nq - b)) for b in range(0, nq, B)]
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
-        g_ids = torch.empty((world, nq, k), dtype=torch.int32, device=dev)
-        g_d = torch.empty((world, nq, k), dtype=torch.float32, device=dev)
+        g_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
+        g_d = torch.empty((world * nq, k), dtype=torch.float32, device=dev)
         m_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
         m_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
 
@@ -231,7 +235,7 @@ def run_ours(args, cfg):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 filt_events.append((e0, e1))
-        if world > 1:
+        if sharded:
             dist.all_gather_into_tensor(g_ids, ids)
             dist.all_gather_into_tensor(g_d, dists)
             _lib.check(lib.trim_merge_topk_device(p(g_d), p(g_ids), world, nq, k, p(m_d), p(m_ids),
@@ -243,7 +247,7 @@ def run_ours(args, cfg):
         for _ in range(warmup):
             step(gamma)
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         ev = []
@@ -257,13 +261,13 @@ def run_ours(args, cfg):
                 launches += step(gamma, ev)
             s1.record(stream)
             torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         ms = s0.elapsed_time(s1)
         filt_ms = sum(a.elapsed_time(b) for a, b in ev)
         ct = cts.sum(0).cpu().numpy()  # identical every step
-        if world > 1:
+        if sharded:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -331,7 +335,7 @@ def run_ours(args, cfg):
         out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
@@ -512,6 +516,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--recall-q", type=int, default=200)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the id-sharded path (all-gather + device merge) even at N=1")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.n:

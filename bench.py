@@ -59,29 +59,61 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region (NVML every
+    10 ms; nvidia-smi as a fallback)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown",
+    }
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.samples = []
+        self.sm = []
+        self.max_sm = None
+        self.reasons = set()
         self._stop = threading.Event()
         self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv = self._nv
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        for b, name in self.REASONS.items():
+            if bits & b:
+                self.reasons.add(name)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        self.sm.append(float(out[0]))
+        self.max_sm = float(out[1])
+        for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"],
+                           out[2:]):
+            if v.strip().lower() == "active":
+                self.reasons.add(name)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                (self._sample_nvml if self._nv else self._sample_smi)()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nv else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -93,16 +125,11 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 5 + i and s[5 + i].strip().lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_sm,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nv else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -406,41 +433,44 @@ def _host_index(arrays):
                      list_codes=h.list_codes, list_lx=h.list_lx, vectors=h.vectors)
 
 
-def _ref_time(hix, qs, cfg, gamma, target_s, threads):
-    """Reference CPU path (oracle/_ref: the unmodified reference headers) over a
-    bounded query sample, timed like bench::detail_sweep::run_queries
-    (sweep.hpp:121-152). Falls back to the C restatement if _ref is absent."""
-    from oracle import oracle as O
-    if O.ref_available():
-        ref = O.RefOracle()
-        ref.set_threads(threads)
-        sess = ref.session(hix)
-        kind = "reference"
+class RefTimer:
+    """The reference CPU path (oracle/_ref: the unmodified reference headers
+    compiled in place) over query samples, timed like
+    bench::detail_sweep::run_queries (sweep.hpp:121-152: steady_clock around a
+    parallel_for over queries). Falls back to the C restatement ("port") when
+    oracle/_ref is absent. Only bench.py's CPU legs use it."""
 
-        def run(qsub):
-            sec, ct = ref.session_run(sess, 0, qsub, cfg["k"], cfg["nprobe"], gamma)
+    def __init__(self, hix, cfg, gamma, threads):
+        from oracle import oracle as O
+        self.cfg, self.gamma, self.threads = cfg, gamma, threads
+        if O.ref_available():
+            self.kind = "reference"
+            self.ref = O.RefOracle()
+            self.ref.set_threads(threads)
+            self.sess = self.ref.session(hix)
+        else:
+            self.kind = "port"
+            self.co = O.COracle()
+            self.hix = hix
+
+    def run(self, qsub):
+        """-> (seconds, evaluated, dc, pruned) for one parallel batch."""
+        if self.kind == "reference":
+            sec, ct = self.ref.session_run(self.sess, 0, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma)
             return sec, int(ct[3]), int(ct[0]), int(ct[2])
-    else:
-        co = O.COracle()
-        kind = "port"
+        t0 = time.perf_counter()
+        _, _, ct, _ = self.co.search_knn(self.hix, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma,
+                                         threads=self.threads)
+        return time.perf_counter() - t0, int(ct[:, 3].sum()), int(ct[:, 0].sum()), int(ct[:, 2].sum())
 
-        def run(qsub):
-            t0 = time.perf_counter()
-            _, _, ct, _ = co.search_knn(hix, qsub, cfg["k"], cfg["nprobe"], gamma, threads=threads)
-            return time.perf_counter() - t0, int(ct[:, 3].sum()), int(ct[:, 0].sum()), int(ct[:, 2].sum())
-    n0 = min(len(qs), max(threads, 16))
-    sec, ev, dc, pr = run(qs[:n0])
-    per_q = sec / n0
-    n1 = int(min(len(qs), max(n0, target_s / max(per_q, 1e-9))))
-    if n1 > n0:
-        sec, ev, dc, pr = run(qs[:n1])
-    else:
-        n1 = n0
-    if kind == "reference":
-        ref.session_destroy(sess)
-    return dict(value=ev / sec, unit="candidates/s", cores=threads, kind=kind,
-                sample=f"first {n1} of {len(qs)} queries of {cfg['workload']} at gamma={gamma} "
-                       f"({sec:.1f}s)", qps=n1 / sec, prune_ratio=pr / max(1, pr + dc))
+    def close(self):
+        if self.kind == "reference":
+            self.ref.session_destroy(self.sess)
+
+    def calibrate(self, qs):
+        n0 = min(len(qs), max(4 * self.threads, 64))
+        sec, *_ = self.run(qs[:n0])
+        return n0 / max(sec, 1e-9)  # queries/s
 
 
 def cpu_baseline(arrays, queries, cfg, gamma, args):
@@ -448,7 +478,16 @@ def cpu_baseline(arrays, queries, cfg, gamma, args):
     hix = _host_index(arrays)
     qs = queries.cpu().numpy()
     log(f"host copy for the CPU baseline: {time.time() - t0:.1f}s")
-    return _ref_time(hix, qs, cfg, gamma, args.cpu_seconds, os.cpu_count() or 1)
+    threads = os.cpu_count() or 1
+    rt = RefTimer(hix, cfg, gamma, threads)
+    qps = rt.calibrate(qs)
+    n = int(min(len(qs), max(4 * threads, args.cpu_seconds * qps)))
+    sec, ev, dc, pr = rt.run(qs[:n])
+    rt.close()
+    return dict(value=ev / sec, unit="candidates/s", cores=threads, kind=rt.kind,
+                sample=f"first {n} of {len(qs)} queries of {cfg['workload']} at gamma={gamma}, "
+                       f"{threads} threads, {sec:.1f}s",
+                qps=n / sec, prune_ratio=pr / max(1, pr + dc))
 
 
 # ------------------------------------------------------ reference CPU arm
@@ -465,23 +504,21 @@ def run_reference(args, cfg):
     torch.cuda.empty_cache()
     threads = os.cpu_count() or 1
     head = args.gamma if args.gamma else cfg["gamma"]
+    rt = RefTimer(hix, cfg, head, threads)
+    qps = rt.calibrate(qs)
     per_step_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
-    from oracle import oracle as O
-    kind = "reference" if O.ref_available() else "port"
-    # calibrate the per-step sample once
-    cal = _ref_time(hix, qs[:max(threads, 16)], cfg, head, 0.0, threads)
-    nstep = int(max(threads, min(len(qs), per_step_s * cal["qps"])))
-    vals, secs, evs = [], 0.0, 0
+    nstep = int(min(len(qs), max(4 * threads, per_step_s * qps)))
+    secs, evs = 0.0, 0
     for i in range(args.warmup + args.steps):
-        sub = qs[(i * nstep) % len(qs):][:nstep]
+        start = (i * nstep) % len(qs)
+        sub = qs[start:start + nstep]
         if len(sub) < nstep:
-            sub = qs[:nstep]
-        r = _ref_time(hix, sub, cfg, head, 0.0, threads)
+            sub = np.concatenate([sub, qs[:nstep - len(sub)]])
+        sec, ev, _, _ = rt.run(sub)
         if i >= args.warmup:
-            vals.append(r["value"])
-            n = int(r["sample"].split()[1])
-            secs += n / r["qps"]
-            evs += r["value"] * (n / r["qps"])
+            secs += sec
+            evs += ev
+    rt.close()
     value = evs / secs
     out = dict(metric="candidates filtered/sec (TRIM kNN filter; QPS, %HBM roofline, prune "
                       "ratio alongside)",
@@ -490,17 +527,15 @@ def run_reference(args, cfg):
                scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic",
                impl="reference",
                config=dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
-                           queries=nq_str(cfg), m=cfg["m"], nlist=cfg["nlist"],
+                           queries=cfg["nq"], m=cfg["m"], nlist=cfg["nlist"],
                            nprobe=cfg["nprobe"], k=cfg["k"], gamma=head),
-               cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind=kind,
-                                 sample=f"{nstep} queries per step of {cfg['workload']}"),
+               qps=nstep * args.steps / secs,
+               cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind=rt.kind,
+                                 sample=f"{nstep} queries per step (of {len(qs)}) of {cfg['workload']}, "
+                                        f"{threads} threads"),
                e2e=dict(value=value, unit="candidates/s", h2d_bytes_per_step=0,
                         d2h_bytes_per_step=0))
     print(json.dumps(out), flush=True)
-
-
-def nq_str(cfg):
-    return cfg["nq"]
 
 
 def main():

@@ -317,7 +317,11 @@ def run_ours(args, cfg):
         if rank == 0:
             sweep[str(g)]["recall@10"] = recall(arrays, queries, ids, k, args.recall_q, world)
     clk = ClockSampler(local)
-    ms, fms, nl, ct, launches = timed(head, args.steps, args.warmup, clk)
+    for _ in range(args.warmup):
+        step(head)
+    gix.skipped_positions(reset=True)  # (synchronises; outside the timed region)
+    ms, fms, nl, ct, launches = timed(head, args.steps, 0, clk)
+    skipped = gix.skipped_positions() / args.steps  # list-level bound, per step (this rank)
     evaluated, dc = float(ct[3]), float(ct[0])
     total_cand = evaluated * args.steps
     value = total_cand / (ms / 1e3)
@@ -342,7 +346,11 @@ def run_ours(args, cfg):
     m, D = cfg["m"], cfg["dim"]
     s_frac = dc / max(1.0, evaluated)
     bytes_per_cand = m + 4 + s_frac * (4 * D + 4)
-    alg_bytes_step = evaluated * (m + 4) + dc * (4 * D + 4)
+    # positions pruned as whole lists by the list-level bound never read their
+    # code/lx: the kernel's algorithmic bytes count only the positions it scans
+    skipped_all = skipped * (world if world > 1 else 1)
+    scanned = evaluated - skipped_all
+    alg_bytes_step = scanned * (m + 4) + dc * (4 * D + 4)
     per_launch_bytes = alg_bytes_step / max(1, nl // args.steps) / (world if world > 1 else 1)
     avg_launch_ms = fms / max(1, nl)
     achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9
@@ -350,7 +358,11 @@ def run_ours(args, cfg):
     out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
                            frac=achieved / peak, traffic=tr, kernel="trim_knn_kernel",
                            bytes_per_candidate=bytes_per_cand, peak_source=peak_src,
-                           filter_share_of_step=fms / ms)
+                           filter_share_of_step=fms / ms,
+                           list_skip_fraction=skipped_all / max(1.0, evaluated),
+                           stream_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4))
+                           / max(1, nl // args.steps) / (world if world > 1 else 1)
+                           / (avg_launch_ms / 1e3) / 1e9)
     out["gpu_launches"] = launches
     out["clocks"] = clk.summary()
     out["sweep"] = sweep

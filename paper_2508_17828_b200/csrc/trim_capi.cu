@@ -118,6 +118,8 @@ struct trim_index {
     std::vector<uint64_t> list_offsets;  // host copy
     std::vector<uint64_t> top_prefix;    // prefix sums of list sizes sorted descending
     uint64_t max_list = 0;
+    uint32_t max_sub_dim = 0;
+    unsigned long long* d_skipped = nullptr; // trim_index_skip_stats
     uint64_t bytes = 0;
     std::vector<void*> allocs;
 
@@ -215,6 +217,22 @@ float omg_round_up(float gamma) {
         f = std::nextafter(f, 2.0f);
     return f;
 }
+
+// 1 - gamma rounded down.
+float omg_round_down(float gamma) {
+    const double exact = 1.0 - static_cast<double>(gamma);
+    float f = static_cast<float>(exact);
+    if (static_cast<double>(f) > exact)
+        f = std::nextafter(f, -2.0f);
+    return f;
+}
+
+// TRIM_LIST_SKIP=0 disables the list-level bound (A/B measurement only; results
+// and counters are identical either way).
+const bool g_list_skip = [] {
+    const char* e = std::getenv("TRIM_LIST_SKIP");
+    return !(e && e[0] == '0');
+}();
 
 // The kernel specialisation (m template value) launch_* will pick.
 int dispatch_m(const DevIndex& ix) {
@@ -316,7 +334,21 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.dist_out = d_dist;
     p.counters = d_ct;
     p.status = d_status;
-    p.first_chunk = 256;
+    // list-level bound slack (list_lower_bound): relative error bounds of the
+    // fp32 coarse distance (dim terms), of sqrt of the reference ADC (LUT entries of
+    // <= max_sd terms summed over m), and of relaxed_lb's evaluation; u = 2^-24
+    {
+        const double u = std::ldexp(1.0, -24);
+        const double kq1 = 1.0 - 2.0 * (ix->dev.dim + 16) * u;
+        const double kq2 = 1.0 - 2.0 * (ix->max_sub_dim + ix->dev.m + 10) * u;
+        const double kest = 1.0 - 16.0 * u;
+        p.kq1 = std::nextafter(static_cast<float>(kq1), 0.0f);
+        p.kq2 = std::nextafter(static_cast<float>(kq2), 0.0f);
+        p.kest = std::nextafter(static_cast<float>(kest), 0.0f);
+        p.omg_lo = omg_round_down(gamma);
+        p.skip_lists = g_list_skip ? 1u : 0u;
+        p.skipped = ix->d_skipped;
+    }
     // grid.x is limited to 2^31-1; process huge batches in slices
     const uint64_t kMaxGrid = 1u << 30;
     for (uint64_t b = 0; b < nq; b += kMaxGrid) {
@@ -471,6 +503,8 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
             suboff[j] = static_cast<uint32_t>(sdsum);
             sdsum += sub[j];
         }
+        for (uint32_t j = 0; j < d->m; ++j)
+            ix->max_sub_dim = std::max(ix->max_sub_dim, sub[j]);
         if (sdsum != d->dim) {
             delete ix;
             return set_err(TRIM_EDATA, "codebook sub_dims do not sum to dim");
@@ -569,6 +603,16 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
             v.codes = codes;
             v.lx = lx;
             v.vectors = vec;
+            float* lr = ix->alloc<float>(d->nlist);
+            float* lxmin = ix->alloc<float>(d->nlist);
+            float* lxmax = ix->alloc<float>(d->nlist);
+            v.list_R = lr;
+            v.list_xmin = lxmin;
+            v.list_xmax = lxmax;
+            ix->d_skipped = ix->alloc<unsigned long long>(1);
+            CK(cudaMemset(ix->d_skipped, 0, sizeof(unsigned long long)));
+            trim_list_meta_kernel<<<d->nlist, kThreads>>>(v, lr, lxmin, lxmax);
+            CK(cudaGetLastError());
             CK(cudaDeviceSynchronize());
         } catch (...) {
             delete ix;
@@ -598,6 +642,21 @@ int trim_index_get_info(trim_index_t ix, trim_index_info* info) {
     info->device_bytes = ix->bytes;
     info->device = ix->device;
     return TRIM_OK;
+}
+
+int trim_index_skip_stats(trim_index_t ix, uint64_t* skipped, int reset) {
+    if (!ix || !skipped)
+        return set_err(TRIM_EINVAL, "trim_index_skip_stats: null argument");
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        CK(cudaDeviceSynchronize());
+        unsigned long long v = 0;
+        CK(cudaMemcpy(&v, ix->d_skipped, sizeof v, cudaMemcpyDeviceToHost));
+        if (reset)
+            CK(cudaMemset(ix->d_skipped, 0, sizeof v));
+        *skipped = v;
+        return TRIM_OK;
+    });
 }
 
 int trim_search_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t k,

@@ -33,6 +33,10 @@ struct DevIndex {
     const uint8_t* codes; // total*code_stride
     const float* lx;      // total
     const float* vectors; // n*dim_stride
+    // per-list metadata for the list-level bound (trim_list_meta_kernel)
+    const float* list_R;    // nlist: >= max over the list of |c_l - landmark(x)|
+    const float* list_xmin; // nlist: min stored lx of the list
+    const float* list_xmax; // nlist: max stored lx of the list
 };
 
 // core/distance.hpp:11-29: four interleaved accumulators, remainder into

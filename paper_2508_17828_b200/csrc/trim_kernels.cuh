@@ -194,14 +194,19 @@ struct KnnParams {
     float* dist_out;         // nq*k
     unsigned long long* counters; // nq*6
     uint32_t* status;        // bit0: some query had < k probed entries
-    uint32_t first_chunk;    // unused (kept for ABI stability of the launcher)
+    uint32_t skip_lists;     // 1: apply the list-level bound (list_lower_bound)
+    float omg_lo;            // 1 - gamma, rounded down
+    float kq1;               // 1 - relative error bound of the fp32 coarse distance
+    float kq2;               // 1 - relative error bound of sqrt(reference ADC)
+    float kest;              // 1 - relative error bound of relaxed_lb's evaluation
+    unsigned long long* skipped; // positions skipped by the list bound (diagnostic)
 };
 
 // Warp-specialised pipeline: warp 0 replays, warps 1..kWorkers filter.
 constexpr uint32_t kWorkers = kWarps - 1;          // 7
 constexpr uint32_t kLaneU = 1;                     // candidates per worker lane per chunk
-constexpr uint32_t kPerWorker = kWarp * kLaneU;    // 64 stream positions per worker per chunk
-constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 448 stream positions per chunk
+constexpr uint32_t kPerWorker = kWarp * kLaneU;    // 32 stream positions per worker per chunk
+constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per chunk
 constexpr uint32_t kRing = 8;                      // chunk buffers in flight
 
 __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
@@ -210,12 +215,13 @@ __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t di
     b += sizeof(float) * dim_stride;             // query
     b += sizeof(uint64_t) * np;                  // base
     b += sizeof(uint32_t) * (np + 1);            // cum
+    b += sizeof(float) * np;                     // per-list lower bounds
     b = (b + 15) & ~size_t(15);
     b += sizeof(uint32_t) * kRing * kChunkW * 3; // superset bins: entry/id, est, d
     b += sizeof(uint32_t) * kRing * kWorkers;    // bin counts
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint64_t) * 2 * kRing;           // full/empty mbarriers
-    b += 16;                                     // published threshold
+    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan barrier
+    b += 16;                                     // published threshold, plan length
     return b;
 }
 
@@ -246,6 +252,40 @@ __device__ __forceinline__ float ld_volatile(const float* p) {
 }
 
 // --------------------------------------------------------------------------
+// List-level bound. For every entry x of inverted list l the reference computes
+// est = relaxed_lb(g, lx) with g = fl(sqrt(adc)) (ivf.hpp:273-275). With
+// D <= |q - c_l| (coarse distance, rounded down), R_l >= |c_l - landmark(x)|
+// (trim_list_meta_kernel) and the ADC's relative error folded into kq2,
+// g >= G := (D - R_l) * kq2 by the triangle inequality. relaxed_lb(g, x) =
+// (x - (1-γ)g)^2 + γ(2-γ)g^2 is increasing in g once g >= (1-γ)x, so if
+// G >= (1-γ) xmax_l every entry of the list has
+//     est >= min_{x in [xmin, xmax]} relaxed_lb(G, x)
+//         =  γ(2-γ)G^2 + dist((1-γ)G, [xmin, xmax])^2
+// up to the evaluation error folded into kest. Every product and sum below is
+// rounded toward the safe side, so the returned L is a rigorous lower bound on
+// est for all of the list's entries (0 when no bound holds).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin, float xmax,
+                                                  const KnnParams& p) {
+    const float omg_hi = p.omg_hi, omg_lo = p.omg_lo;
+    const float D = __fsqrt_rd(__fmul_rd(dq, p.kq1));
+    const float G0 = __fsub_rd(D, R);
+    if (!(G0 > 0.0f))
+        return 0.0f;
+    const float g = __fmul_rd(G0, p.kq2);
+    if (!(g >= __fmul_ru(omg_hi, xmax))) // outside the monotone region
+        return 0.0f;
+    const float omg2 = fmaxf(__fmul_ru(omg_lo, omg_lo), __fmul_ru(omg_hi, omg_hi));
+    if (!(omg2 <= 1.0f)) // γ(2-γ) may be negative (γ >= 2): no bound
+        return 0.0f;
+    const float c1 = __fsub_rd(1.0f, omg2); // γ(2-γ), rounded down
+    const float t1 = __fmul_rd(__fmul_rd(g, g), c1);
+    const float plo = __fmul_rd(omg_lo, g), phi = __fmul_ru(omg_hi, g); // (1-γ)g
+    const float gap = fmaxf(0.0f, fmaxf(__fsub_rd(xmin, phi), __fsub_rd(plo, xmax)));
+    return __fmul_rd(__fadd_rd(t1, __fmul_rd(gap, gap)), p.kest);
+}
+
+// --------------------------------------------------------------------------
 // trim_knn_kernel — one CTA owns one query's candidate stream.
 //
 // The reference threshold max_dis is sequential state (ivf.hpp:256-287,
@@ -265,6 +305,14 @@ __device__ __forceinline__ float ld_volatile(const float* p) {
 // so workers never wait for the replay except when the ring is full; the
 // next chunk's codes are prefetched into registers while the current one is
 // filtered.
+//
+// After chunk 0 (positions [0, 224), which hold every seed when k <= 224) the
+// replay warp plans the rest of the stream: a probed list that starts at
+// position >= 224 and whose list_lower_bound is >= the published T is pruned
+// as a whole (every entry has est >= L >= T >= T_live: the reference prunes
+// each of them, ivf.hpp:275), and the remaining positions are compacted in
+// place into cum/base. Chunks c >= 1 walk the compacted stream. Counters are
+// unchanged: skipped entries are evaluated-and-pruned positions.
 // --------------------------------------------------------------------------
 template <int M, int KS, int S>
 __global__ void __launch_bounds__(kThreads, (M == 0 || M > 64) ? 2 : 3)
@@ -284,6 +332,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     off += sizeof(uint64_t) * p.np;
     st.cum = reinterpret_cast<uint32_t*>(smem + off);
     off += sizeof(uint32_t) * (p.np + 1);
+    float* s_lb = reinterpret_cast<float*>(smem + off); // [np] list lower bounds
+    off += sizeof(float) * p.np;
     off = (off + 15) & ~size_t(15);
     uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);  // [kRing][kChunkW]: entry, then id
     float* s_est = reinterpret_cast<float*>(s_e + kRing * kChunkW);
@@ -294,7 +344,9 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     off = (off + 15) & ~size_t(15);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
     uint64_t* empty = full + kRing;
-    float* s_T = reinterpret_cast<float*>(empty + kRing);
+    uint64_t* plan = empty + kRing;
+    float* s_T = reinterpret_cast<float*>(plan + 2);
+    uint32_t* s_total2 = reinterpret_cast<uint32_t*>(s_T + 1);
 
     const float kInf = __int_as_float(0x7f800000);
     const float kNegInf = __int_as_float(0xff800000);
@@ -307,19 +359,36 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             mbar_init(full + s, kWorkers * kWarp);
             mbar_init(empty + s, kWarp);
         }
+        mbar_init(plan, kWarp);
         *s_T = kInf;
     }
     __syncthreads();
     build_lut_blocked(ix, qv, lut);
     const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
                                        p.np, st); // ends with a barrier
-    const uint32_t nchunks = (total + kChunkW - 1) / kChunkW;
+    const uint32_t nchunks0 = (total + kChunkW - 1) / kChunkW;
 
     if (warp == 0) {
         // ------------------------------------------------ replay warp
+        const bool skip = p.skip_lists && p.probe && p.k <= kChunkW && nchunks0 > 1;
+        if (skip) { // T-independent part of the plan, overlapped with chunk 0
+            const uint32_t* pl = p.probe + static_cast<size_t>(q) * p.np;
+            for (uint32_t i = lane; i < p.np; i += kWarp) {
+                float lb = 0.0f;
+                if (st.cum[i] >= kChunkW) {
+                    const uint32_t l = __ldg(pl + i);
+                    const float dq = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(l) * ix.dim_stride,
+                                                    ix.dim);
+                    lb = list_lower_bound(dq, __ldg(ix.list_R + l), __ldg(ix.list_xmin + l),
+                                          __ldg(ix.list_xmax + l), p);
+                }
+                s_lb[i] = lb;
+            }
+        }
         WarpTopK<S> topk;
         topk.init(p.k);
         uint64_t dc = 0;
+        uint32_t nchunks = nchunks0;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t s = c % kRing;
             mbar_wait(full + s, (c / kRing) & 1u);
@@ -338,8 +407,53 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     }
                 }
             }
+            const float T = topk.wd;
             if (lane == 0)
-                *reinterpret_cast<volatile float*>(s_T) = topk.wd;
+                *reinterpret_cast<volatile float*>(s_T) = T;
+            if (c == 0 && nchunks0 > 1) {
+                // plan: compact the positions >= kChunkW of the lists that are kept
+                // (workers read cum/base again only after the plan barrier)
+                uint32_t carry = 0, nk = 0;
+                for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) {
+                    const uint32_t i = b0 + lane;
+                    uint32_t len = 0;
+                    uint64_t bs = 0;
+                    if (i < p.np) {
+                        const uint32_t c0 = st.cum[i], c1 = st.cum[i + 1];
+                        if (c1 > kChunkW && !(skip && c0 >= kChunkW && s_lb[i] >= T)) {
+                            const uint32_t s0 = max(c0, kChunkW);
+                            len = c1 - s0;
+                            bs = st.base[i] + (s0 - c0);
+                        }
+                    }
+                    const uint32_t keep = __ballot_sync(0xffffffffu, len != 0);
+                    uint32_t v = len;
+#pragma unroll
+                    for (int o = 1; o < kWarp; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                        if (lane >= static_cast<uint32_t>(o))
+                            v += t;
+                    }
+                    __syncwarp(); // this batch's reads precede its (lower-index) writes
+                    if (len != 0) {
+                        const uint32_t j = nk + __popc(keep & ((1u << lane) - 1u));
+                        st.base[j] = bs;
+                        st.cum[j] = carry + v - len;
+                    }
+                    carry += __shfl_sync(0xffffffffu, v, kWarp - 1);
+                    nk += __popc(keep);
+                    __syncwarp();
+                }
+                if (lane == 0) {
+                    st.cum[nk] = carry;
+                    *s_total2 = carry;
+                    if (p.skipped && total - kChunkW != carry)
+                        atomicAdd(p.skipped, static_cast<unsigned long long>(total - kChunkW - carry));
+                }
+                nchunks = 1 + (carry + kChunkW - 1) / kChunkW;
+                __syncwarp();
+                mbar_arrive(plan);
+            }
             __syncwarp();
             mbar_arrive(empty + s);
         }
@@ -361,7 +475,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             const uint64_t seeds = min(static_cast<uint64_t>(p.k), evaluated);
             cc[0] = dc;                // dc
             cc[1] = evaluated - seeds; // edc
-            cc[2] = evaluated - dc;    // pruned
+            cc[2] = evaluated - dc;    // pruned (including skipped lists)
             cc[3] = evaluated;         // evaluated
             cc[4] = 0;                 // hops
             cc[5] = ix.nlist;          // coarse_dc (probe_order always runs)
@@ -374,6 +488,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     LaneAdc la;
     la.init(lane, LutShape::of(m));
     uint32_t li = 0; // list cursor (positions of a lane only increase)
+    uint32_t nchunks = nchunks0, bound = total;
     struct Cand {
         FastCode<M> fc;
         float lx;
@@ -384,19 +499,24 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         Cand c[kLaneU];
     };
     Slot sa, sb; // double buffer in registers (static names: no local-memory indexing)
+    // chunk 0: original positions [0, 224); chunk c >= 1: compacted positions
+    // (c-1)*224 + ... (original position >= 224 + that, equal when nothing is skipped)
     auto fetch = [&](uint32_t c, Slot& d) {
 #pragma unroll
         for (uint32_t u = 0; u < kLaneU; ++u) {
-            const uint32_t pp = c * kChunkW + w * kPerWorker + u * kWarp + lane;
+            const uint32_t pp = (c == 0 ? 0u : (c - 1) * kChunkW) + w * kPerWorker + u * kWarp + lane;
             Cand& x = d.c[u];
             x.kind = 0;
             x.e = 0;
             x.lx = 0.0f;
-            if (c < nchunks && pp < total) {
+            if (c < nchunks && pp < bound) {
                 while (st.cum[li + 1] <= pp)
                     ++li;
                 x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
-                x.kind = pp < p.k ? 1u : 2u; // seeds (ivf.hpp:264-271): always evaluated
+                // seeds (ivf.hpp:264-271) are always evaluated; beyond chunk 0 they
+                // occur only when k > 224, where nothing is skipped
+                const uint32_t orig = c == 0 ? pp : pp + kChunkW;
+                x.kind = orig < p.k ? 1u : 2u;
                 if (x.kind == 2u) {
                     x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
                     x.lx = __ldg(ix.lx + x.e);
@@ -457,7 +577,15 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         mbar_arrive(full + s);
     };
     fetch(0, sa);
-    for (uint32_t c = 0; c < nchunks; c += 2) {
+    process(0, sa);
+    if (nchunks0 <= 1)
+        return;
+    mbar_wait(plan, 0); // the compacted stream (chunks >= 1)
+    bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
+    nchunks = 1 + (bound + kChunkW - 1) / kChunkW;
+    li = 0;
+    fetch(1, sa);
+    for (uint32_t c = 1; c < nchunks; c += 2) {
         fetch(c + 1, sb); // prefetch: loads in flight while chunk c is filtered
         process(c, sa);
         if (c + 1 >= nchunks)
@@ -905,6 +1033,61 @@ trim_merge_kernel(const float* dist, const uint32_t* ids, uint32_t nshards, uint
         ids_out[static_cast<size_t>(q) * k + i] = key == ~0ull ? kInvalidId : static_cast<uint32_t>(key);
         dist_out[static_cast<size_t>(q) * k + i] =
             key == ~0ull ? __int_as_float(0x7f800000) : __uint_as_float(static_cast<uint32_t>(key >> 32));
+    }
+}
+
+// Per inverted list (one CTA each): R_l >= max_x |c_l - landmark(x)|, where
+// landmark(x) is the PQ reconstruction of x's code (the point lx measures to,
+// ivf.hpp:137-145), computed in fp64 and rounded up; and [xmin, xmax] of the
+// stored lx. Feeds list_lower_bound. Empty lists get R = 0, xmin = +inf,
+// xmax = -inf (they contribute no positions).
+__global__ void __launch_bounds__(kThreads)
+trim_list_meta_kernel(DevIndex ix, float* list_R, float* list_xmin, float* list_xmax) {
+    __shared__ double s_r[kWarps];
+    __shared__ float s_lo[kWarps], s_hi[kWarps];
+    const uint32_t l = blockIdx.x;
+    const uint64_t b = ix.list_offsets[l], e = ix.list_offsets[l + 1];
+    const float* c = ix.coarse + static_cast<size_t>(l) * ix.dim_stride;
+    double r2 = 0.0;
+    float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const uint8_t* code = ix.codes + i * ix.code_stride;
+        double acc = 0.0;
+        for (uint32_t j = 0; j < ix.m; ++j) {
+            const uint32_t sd = ix.sub_dims[j], so = ix.sub_offsets[j];
+            const float* cen = ix.centroids + static_cast<size_t>(ix.ksub) * so + static_cast<size_t>(code[j]) * sd;
+            for (uint32_t t = 0; t < sd; ++t) {
+                const double d = static_cast<double>(cen[t]) - static_cast<double>(c[so + t]);
+                acc += d * d;
+            }
+        }
+        r2 = fmax(r2, acc);
+        const float x = ix.lx[i];
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        r2 = fmax(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_r[warp] = r2;
+        s_lo[warp] = lo;
+        s_hi[warp] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kWarps; ++w) {
+            r2 = fmax(r2, s_r[w]);
+            lo = fminf(lo, s_lo[w]);
+            hi = fmaxf(hi, s_hi[w]);
+        }
+        // fp64 sum of <= 2^12 squares: relative error < 2^-40; the margin covers it
+        list_R[l] = __double2float_ru(sqrt(r2) * (1.0 + 1e-9));
+        list_xmin[l] = lo;
+        list_xmax[l] = hi;
     }
 }
 

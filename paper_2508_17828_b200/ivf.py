@@ -171,6 +171,13 @@ class GpuIvfIndex:
         _lib.check(_lib.load().trim_index_get_info(self._h, C.byref(inf)), "trim_index_get_info")
         return {f: getattr(inf, f) for f, _ in _lib.TrimIndexInfo._fields_}
 
+    def skipped_positions(self, reset: bool = False) -> int:
+        """Stream positions pruned as whole lists by the kNN kernel's list-level
+        bound (trim_index_skip_stats); a diagnostic, results are unaffected."""
+        v = C.c_uint64(0)
+        _lib.check(_lib.load().trim_index_skip_stats(self._h, C.byref(v), int(reset)), "trim_index_skip_stats")
+        return int(v.value)
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.load().trim_index_destroy(self._h)

@@ -217,3 +217,36 @@ def test_config1_full_scale_parity(config1, gamma):
     prune = ct[2] / (ct[2] + ct[0])
     if gamma == 0.0:
         assert abs(prune - 0.97871) < 1e-4  # SURVEY.md §6 probe value
+
+
+# ------------------------------------------- list-level bound (whole-list skips)
+@pytest.fixture(scope="module")
+def clustered():
+    # well-separated blobs, many lists: most probed lists are provably pruned
+    # as a whole after the first chunk (trim_kernels.cuh: list_lower_bound)
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefOracle()
+    centers = ref.make_normal(32, 48, 11)
+    base = ref.make_blobs(centers, 60000, 0.3, 12)
+    qs = ref.make_blobs(centers, 200, 0.3, 13)
+    hix = make_reference_index(ref, base, m=16, c=256, iters=10, pq_seed=14, nlist=64, ivf_seed=15)
+    return hix, qs, G.GpuIvfIndex(G.IvfArrays.from_any(hix))
+
+
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 1.0, 1.5, 2.5])
+@pytest.mark.parametrize("k", [10, 100, 250])
+def test_list_skip_parity(clustered, gamma, k):
+    hix, qs, gix = clustered
+    gix.skipped_positions(reset=True)
+    want = co.search_knn(hix, qs, k, 32, gamma)
+    got = G.search_trim_ivf_knn_batch(gix, G.PruningProfile.manual(gamma), qs, k, 32)
+    np.testing.assert_array_equal(got[0], want[0])
+    assert_bits(got[1], want[1])
+    np.testing.assert_array_equal(got[2][:, :5], want[2])
+    skipped = gix.skipped_positions()
+    assert skipped <= int(want[2][:, 2].sum())  # skipped positions are pruned positions
+    if k > 224 or gamma >= 2.0:
+        assert skipped == 0  # no plan beyond the seeds / no bound for γ(2-γ) <= 0
+    elif gamma in (0.5, 1.0) and k == 10:
+        assert skipped > 0

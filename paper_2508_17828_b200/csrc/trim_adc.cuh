@@ -66,10 +66,68 @@ __host__ __device__ inline size_t lut_bytes(int /*M_template*/, uint32_t m) { re
 
 // pq::build_distance_table (pq.hpp:158-172) into the blocked layout. Entry
 // values are the reference's euclidean_sq, bit for bit.
+// Entry (j, c) = euclidean_sq of a 2- or 4-wide subspace, the reference's
+// four-accumulator order collapsed: acc_i = 0 + d_i^2 exactly, unused
+// accumulators are +0.0f.
+template <uint32_t SD>
+__device__ __forceinline__ float sub_dist(const float* q, const float* c) {
+    if (SD == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(c));
+        const float d0 = __fsub_rn(q[0], v.x), d1 = __fsub_rn(q[1], v.y);
+        return __fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1));
+    } else {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(c));
+        const float d0 = __fsub_rn(q[0], v.x), d1 = __fsub_rn(q[1], v.y);
+        const float d2 = __fsub_rn(q[2], v.z), d3 = __fsub_rn(q[3], v.w);
+        return __fadd_rn(__fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1)),
+                         __fadd_rn(__fmul_rn(d2, d2), __fmul_rn(d3, d3)));
+    }
+}
+
+// Uniform 2- or 4-wide subspaces: entries are independent, so each thread
+// keeps 8 centroid loads in flight (the generic loop below is latency-bound).
+template <uint32_t SD>
+__device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const float* q_smem, float* lut,
+                                                  const LutShape& sh) {
+    const uint32_t hrow = sh.half_row_bytes() / 4;
+    float* hblk = lut + sh.nfull * (kFullBytes / 4);
+    const uint32_t total = ix.m * ix.ksub;
+    for (uint32_t i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
+            v[u] = i < total ? sub_dist<SD>(q_smem + j * SD, ix.centroids + (static_cast<size_t>(ix.ksub) * j + c) * SD)
+                             : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            if (i >= total)
+                break;
+            const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
+            const uint32_t b = j >> 5, t = j & 31u;
+            if (b < sh.nfull) {
+                lut[b * (kFullBytes / 4) + c * 32 + t] = v[u];
+            } else {
+                hblk[c * hrow + t] = v[u];
+                if (sh.hdup)
+                    hblk[c * hrow + t + 16] = v[u];
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const float* q_smem, float* lut) {
     const LutShape sh = LutShape::of(ix.m);
     const uint32_t hrow = sh.half_row_bytes() / 4;          // floats per HALF row
     float* hblk = lut + sh.nfull * (kFullBytes / 4);
+    if (ix.sd_uniform == 2)
+        build_lut_uniform<2>(ix, q_smem, lut, sh);
+    else if (ix.sd_uniform == 4)
+        build_lut_uniform<4>(ix, q_smem, lut, sh);
+    else
     for (uint32_t j = 0; j < ix.m; ++j) {
         const uint32_t sd = ix.sub_dims[j];
         const uint32_t off = ix.sub_offsets[j];
@@ -456,6 +514,40 @@ __device__ __forceinline__ float est_lower_bound(float a, float glx, float two_g
         e_lo = __fmul_rd(d_hi, d_hi);
     const float t_lo = __fmul_rd(__fmul_rd(two_gamma, g_lo), glx);
     return __fadd_rd(e_lo, t_lo);
+}
+
+// Upper bound on the same est (mirror image of est_lower_bound): every
+// reference operation is monotone in its inputs, so the largest inputs with
+// upward rounding bound each intermediate from above.
+__device__ __forceinline__ float est_upper_bound(float a, float glx, float two_gamma, float eps) {
+    const float a_lo = __fmul_rd(a, 1.0f - eps);
+    const float a_hi = __fmul_ru(a, 1.0f + eps);
+    const float g_lo = __fmul_rd(sqrt_approx(a_lo), 1.0f - 1.0f / 65536.0f);
+    const float g_hi = __fmul_ru(sqrt_approx(a_hi), 1.0f + 1.0f / 65536.0f);
+    const float d_lo = __fsub_rd(g_lo, glx);
+    const float d_hi = __fsub_ru(g_hi, glx);
+    const float e_hi = fmaxf(__fmul_ru(d_lo, d_lo), __fmul_ru(d_hi, d_hi));
+    const float t_hi = __fmul_ru(__fmul_ru(two_gamma, g_hi), glx);
+    return __fadd_ru(e_hi, t_hi);
+}
+
+// pq::adc_lookup (pq.hpp:186-192) by one thread over the blocked LUT:
+// sequential fp32 sum in the reference order j = 0..m-1. For the rare
+// candidates whose est interval straddles the live threshold.
+template <int M>
+__device__ __forceinline__ float adc_serial(const uint8_t* __restrict__ code, uint32_t m) {
+    const uint32_t mm = M > 0 ? static_cast<uint32_t>(M) : m;
+    const LutShape sh = LutShape::of(mm);
+    const uint32_t base = lut_saddr();
+    const uint32_t hbase = base + sh.nfull * kFullBytes, hrow = sh.half_row_bytes();
+    float acc = 0.0f;
+    for (uint32_t j = 0; j < mm; ++j) {
+        const uint32_t c = __ldg(code + j);
+        const uint32_t b = j >> 5, t = j & 31u;
+        const uint32_t a = b < sh.nfull ? base + b * kFullBytes + c * 128u + 4u * t : hbase + c * hrow + 4u * t;
+        acc = __fadd_rn(acc, lds_f32(a));
+    }
+    return acc;
 }
 
 } // namespace trimgpu

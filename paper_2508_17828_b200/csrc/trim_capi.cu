@@ -227,12 +227,24 @@ float omg_round_down(float gamma) {
     return f;
 }
 
-// TRIM_LIST_SKIP=0 disables the list-level bound (A/B measurement only; results
-// and counters are identical either way).
-const bool g_list_skip = [] {
+// Test/measurement knobs, read per call (results and counters are identical
+// for every setting):
+//   TRIM_LIST_SKIP=0     disables the kNN list-level bound (A/B timing);
+//   TRIM_EPS_SCALE=x>=1  widens the any-order ADC error interval x-fold, so the
+//                        exact (reference-order) resolution paths run often.
+bool list_skip_enabled() {
     const char* e = std::getenv("TRIM_LIST_SKIP");
     return !(e && e[0] == '0');
-}();
+}
+float filter_eps(uint32_t m) {
+    float eps = adc_rel_eps(m);
+    if (const char* e = std::getenv("TRIM_EPS_SCALE")) {
+        const double x = std::atof(e);
+        if (x > 1.0 && x * eps < 0.25)
+            eps = static_cast<float>(x * eps);
+    }
+    return eps;
+}
 
 // The kernel specialisation (m template value) launch_* will pick.
 int dispatch_m(const DevIndex& ix) {
@@ -328,7 +340,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.np = np;
     p.probe = d_probe;
     p.two_gamma = 2.0f * gamma;
-    p.adc_eps = adc_rel_eps(ix->dev.m);
+    p.adc_eps = filter_eps(ix->dev.m);
     p.omg_hi = omg_round_up(gamma);
     p.ids_out = d_ids;
     p.dist_out = d_dist;
@@ -346,7 +358,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         p.kq2 = std::nextafter(static_cast<float>(kq2), 0.0f);
         p.kest = std::nextafter(static_cast<float>(kest), 0.0f);
         p.omg_lo = omg_round_down(gamma);
-        p.skip_lists = g_list_skip ? 1u : 0u;
+        p.skip_lists = list_skip_enabled() ? 1u : 0u;
         p.skipped = ix->d_skipped;
     }
     // grid.x is limited to 2^31-1; process huge batches in slices
@@ -557,6 +569,10 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
         v.ksub = d->ksub;
         v.code_stride = round_up(d->m, 16);
         v.nlist = d->nlist;
+        v.sd_uniform = sub.empty() ? 0u : sub[0];
+        for (uint32_t j = 1; j < d->m; ++j)
+            if (sub[j] != sub[0])
+                v.sd_uniform = 0;
         v.n = d->n;
         v.id_base = d->id_base;
         ix->code_stride_host = d->code_stride;
@@ -807,7 +823,7 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
             RangeParams p{};
             p.np = np;
             p.two_gamma = 2.0f * gamma;
-            p.adc_eps = adc_rel_eps(ix->dev.m);
+            p.adc_eps = filter_eps(ix->dev.m);
             p.omg_hi = omg_round_up(gamma);
             p.slice = slice;
             p.cap = cap;

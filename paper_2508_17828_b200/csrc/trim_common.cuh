@@ -22,6 +22,7 @@ struct DevIndex {
     uint32_t ksub;
     uint32_t code_stride; // bytes per code row (m rounded up to 16)
     uint32_t nlist;
+    uint32_t sd_uniform; // common sub-dimension when every subspace has it, else 0
     uint64_t n;
     uint64_t id_base;
     const uint32_t* sub_dims;    // m

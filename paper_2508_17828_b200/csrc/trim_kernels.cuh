@@ -207,7 +207,8 @@ constexpr uint32_t kWorkers = kWarps - 1;          // 7
 constexpr uint32_t kLaneU = 1;                     // candidates per worker lane per chunk
 constexpr uint32_t kPerWorker = kWarp * kLaneU;    // 32 stream positions per worker per chunk
 constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per chunk
-constexpr uint32_t kRing = 8;                      // chunk buffers in flight
+constexpr uint32_t kRing = 6;                      // chunk buffers in flight
+static_assert(kLaneU == 1, "bin_mask records one ballot per worker chunk");
 
 __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
                                                  uint32_t np) {
@@ -217,8 +218,8 @@ __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t di
     b += sizeof(uint32_t) * (np + 1);            // cum
     b += sizeof(float) * np;                     // per-list lower bounds
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint32_t) * kRing * kChunkW * 3; // superset bins: entry/id, est, d
-    b += sizeof(uint32_t) * kRing * kWorkers;    // bin counts
+    b += sizeof(uint32_t) * kRing * kChunkW * 4; // superset bins: id, est_lo, est_hi, d
+    b += sizeof(uint32_t) * kRing * kWorkers * 2; // bin counts, bin lane masks
     b = (b + 15) & ~size_t(15);
     b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan barrier
     b += 16;                                     // published threshold, plan length
@@ -293,12 +294,14 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // of 224 positions (warp w, lane l: position c*224 + (w-1)*32 + l), each with
 // the latest threshold T the replay warp has published — any published T is
 // >= the reference's running threshold at every later position, because the
-// threshold only decreases. A worker keeps the superset {est_lower_bound < T}
-// (the any-order ADC's rigorous interval, trim_adc.cuh), recomputes the
-// reference-order ADC and est for those, and computes exact L2 for every
-// member with est < T. Warp 0 replays the chunk's members in stream order
-// with the live threshold: evaluate iff est < T_live (prune on tie,
-// ivf.hpp:275), replace iff (d, id) < top (ivf.hpp:277-282). The evaluate /
+// threshold only decreases. From the any-order ADC a worker derives a
+// rigorous interval [lo, hi] around the reference's est (trim_adc.cuh), keeps
+// the members {lo < T} and computes their exact L2. Warp 0 replays the
+// chunk's members in stream order with the live threshold: evaluate iff
+// est < T_live (prune on tie, ivf.hpp:275) — decided by lo >= T_live (prune)
+// or hi < T_live (evaluate), and only when the interval straddles T_live by
+// the reference-order ADC itself (adc_serial) — and replace iff
+// (d, id) < top (ivf.hpp:277-282). The evaluate /
 // prune decisions, counters and result set are therefore the reference's,
 // for any gamma. Chunks flow through a ring of kRing buffers guarded by
 // mbarriers (full: 224 worker-lane arrivals; empty: 32 replay-lane arrivals),
@@ -335,12 +338,14 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     float* s_lb = reinterpret_cast<float*>(smem + off); // [np] list lower bounds
     off += sizeof(float) * p.np;
     off = (off + 15) & ~size_t(15);
-    uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);  // [kRing][kChunkW]: entry, then id
-    float* s_est = reinterpret_cast<float*>(s_e + kRing * kChunkW);
-    float* s_d = s_est + kRing * kChunkW;
+    uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);  // [kRing][kChunkW]: id
+    float* s_lo = reinterpret_cast<float*>(s_e + kRing * kChunkW); // est interval
+    float* s_hi = s_lo + kRing * kChunkW;
+    float* s_d = s_hi + kRing * kChunkW;
     uint32_t* bin_cnt = reinterpret_cast<uint32_t*>(s_d + kRing * kChunkW); // [kRing][kWorkers]
+    uint32_t* bin_mask = bin_cnt + kRing * kWorkers; // lanes of the members, [kRing][kWorkers]
     // (bins: worker w of ring slot s owns s_*[s*kChunkW + w*kPerWorker ...], in stream order)
-    off = reinterpret_cast<unsigned char*>(bin_cnt + kRing * kWorkers) - smem;
+    off = reinterpret_cast<unsigned char*>(bin_mask + kRing * kWorkers) - smem;
     off = (off + 15) & ~size_t(15);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
     uint64_t* empty = full + kRing;
@@ -389,6 +394,26 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         topk.init(p.k);
         uint64_t dc = 0;
         uint32_t nchunks = nchunks0;
+        uint32_t ncum = p.np; // lists in the current cum/base layout
+        // The reference-order est of a member whose interval straddles the live
+        // threshold (rare): its stream position from the bin's lane mask, its
+        // entry from the cum/base layout, then pq::adc_lookup + relaxed_lb.
+        auto exact_est = [&](uint32_t c, uint32_t w, uint32_t i, uint32_t mask) -> float {
+            for (uint32_t r = 0; r < i; ++r)
+                mask &= mask - 1;
+            const uint32_t pp = (c == 0 ? 0u : (c - 1) * kChunkW) + w * kPerWorker + (__ffs(mask) - 1);
+            uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (st.cum[mid] <= pp)
+                    lo = mid;
+                else
+                    hi = mid;
+            }
+            const uint64_t e = st.base[lo] + (pp - st.cum[lo]);
+            const float a = adc_serial<M>(ix.codes + e * ix.code_stride, m);
+            return relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
+        };
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t s = c % kRing;
             mbar_wait(full + s, (c / kRing) & 1u);
@@ -400,10 +425,15 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 const uint32_t cnt = cnts[w];
                 const uint32_t g0 = s * kChunkW + w * kPerWorker;
                 for (uint32_t i = 0; i < cnt; ++i) {
-                    const float est = s_est[g0 + i];
-                    if (est < topk.wd) { // ivf.hpp:275 — prune on tie
-                        ++dc;
-                        topk.offer(s_d[g0 + i], s_e[g0 + i]);
+                    const float lo = s_lo[g0 + i];
+                    if (lo < topk.wd) { // else est >= lo >= T_live: pruned (ivf.hpp:275)
+                        bool ev = true; // seeds (lo = -inf) and hi < T_live: est < T_live
+                        if (lo != kNegInf && !(s_hi[g0 + i] < topk.wd))
+                            ev = exact_est(c, w, i, bin_mask[s * kWorkers + w]) < topk.wd;
+                        if (ev) {
+                            ++dc;
+                            topk.offer(s_d[g0 + i], s_e[g0 + i]);
+                        }
                     }
                 }
             }
@@ -451,6 +481,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                         atomicAdd(p.skipped, static_cast<unsigned long long>(total - kChunkW - carry));
                 }
                 nchunks = 1 + (carry + kChunkW - 1) / kChunkW;
+                ncum = nk;
                 __syncwarp();
                 mbar_arrive(plan);
             }
@@ -536,44 +567,37 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             T = ld_volatile(s_T);
         }
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
-        uint32_t n = 0;
-#pragma unroll
-        for (uint32_t u = 0; u < kLaneU; ++u) {
-            Cand& x = cur.c[u];
-            const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
-            const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
-            bool keep = x.kind == 1u;
-            if (x.kind == 2u && a >= 0.0f)
-                keep = est_lower_bound(a, x.lx, p.two_gamma, p.adc_eps) < T;
-            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const uint32_t r = n + __popc(bal & ((1u << lane) - 1u));
-                s_e[g0 + r] = x.e;
-                s_est[g0 + r] = x.kind == 1u ? kNegInf : 0.0f;
-            }
-            n += __popc(bal);
+        Cand& x = cur.c[0];
+        const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
+        const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
+        // member = seed, or a candidate whose est interval [lo, hi] starts below T
+        float lo = kNegInf, hi = kNegInf;
+        bool keep = x.kind == 1u;
+        if (x.kind == 2u && a >= 0.0f) {
+            lo = est_lower_bound(a, x.lx, p.two_gamma, p.adc_eps);
+            keep = lo < T;
+            if (keep)
+                hi = est_upper_bound(a, x.lx, p.two_gamma, p.adc_eps);
         }
-        __syncwarp();
-        for (uint32_t i = lane; i < n; i += kWarp) {
-            // reference-order ADC + est (conflict-free rotation over active lanes), exact L2
-            const uint32_t e = s_e[g0 + i];
-            float est = s_est[g0 + i];
-            if (est != kNegInf) {
-                const float a = adc_exact<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
-                est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
-            }
-            if (est < T) {
-                const uint32_t id = __ldg(ix.list_ids + e);
-                const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
-                s_d[g0 + i] = euclid_sq_vec4(qv, row, ix.dim);
-                s_e[g0 + i] = id;
-                s_est[g0 + i] = est;
-            } else {
-                s_est[g0 + i] = kInf; // pruned even at the published threshold
-            }
+        uint32_t id = 0;
+        float d = 0.0f;
+        if (keep) { // exact L2 (ivf.hpp:276) of every member the replay may evaluate
+            id = __ldg(ix.list_ids + x.e);
+            const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
+            d = euclid_sq_vec4(qv, row, ix.dim);
         }
-        if (lane == 0)
-            bin_cnt[s * kWorkers + w] = n;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const uint32_t r = __popc(bal & ((1u << lane) - 1u));
+            s_e[g0 + r] = id;
+            s_lo[g0 + r] = lo;
+            s_hi[g0 + r] = hi;
+            s_d[g0 + r] = d;
+        }
+        if (lane == 0) {
+            bin_cnt[s * kWorkers + w] = __popc(bal);
+            bin_mask[s * kWorkers + w] = bal;
+        }
         mbar_arrive(full + s);
     };
     fetch(0, sa);
@@ -704,18 +728,26 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
             }
             const StageCheck ck{glx, p.two_gamma, p.omg_hi, p.adc_eps, r2_excl};
             const float a = fc.sum_staged(m, la, ck, valid); // warp-collective: every lane calls
+            // evaluate iff est <= r^2 (ivf.hpp:331): decided by the rigorous interval
+            // [lo, hi] around the reference's est, or, when it straddles r^2 (rare),
+            // by the reference-order ADC itself
             if (valid && a >= 0.0f && est_lower_bound(a, glx, p.two_gamma, p.adc_eps) <= r2) {
-                const uint32_t slot = atomicAdd(&scal[0], 1u);
-                s_e[slot] = e;
+                bool ev = est_upper_bound(a, glx, p.two_gamma, p.adc_eps) <= r2;
+                if (!ev) {
+                    const float ax = adc_serial<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m);
+                    ev = relaxed_lb(__fsqrt_rn(ax), glx, p.two_gamma) <= r2;
+                }
+                if (ev) {
+                    const uint32_t slot = atomicAdd(&scal[0], 1u);
+                    s_e[slot] = e;
+                }
             }
         }
         __syncthreads();
         const uint32_t ns = scal[0];
         for (uint32_t i = tid; i < ns; i += kThreads) {
             const uint32_t e = s_e[i];
-            const float a = adc_exact<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m, lane);
-            const float est = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
-            if (est <= r2) { // ivf.hpp:331
+            {
                 ++dc_local;
                 const uint32_t id = __ldg(ix.list_ids + e);
                 const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;

@@ -120,6 +120,10 @@ struct trim_index {
     uint64_t max_list = 0;
     uint32_t max_sub_dim = 0;
     unsigned long long* d_skipped = nullptr; // trim_index_skip_stats
+    // tensor-core probe (trim_probe_mma.cuh): pre-tiled centroids and norms
+    float4* coarse_t = nullptr;
+    float* cn2 = nullptr;
+    float* cn = nullptr;
     uint64_t bytes = 0;
     std::vector<void*> allocs;
 
@@ -257,9 +261,37 @@ int dispatch_m(const DevIndex& ix) {
 // the effective per-query probe count; d_probe is null when nlist == 1.
 // probe_order for a batch into d_out (nq*np): the tiled kernel when np and the
 // distance table fit its shared-memory plan, else the one-query bitonic kernel.
+// TRIM_PROBE_MMA=0 forces the SIMT probe kernels (A/B and parity tests).
+bool probe_mma_enabled() {
+    const char* e = std::getenv("TRIM_PROBE_MMA");
+    return !(e && e[0] == '0');
+}
+
 void launch_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t np, uint32_t* d_out,
                   cudaStream_t st) {
     const DevIndex& v = ix->dev;
+    const size_t per_warp = probe_select_smem_per_warp(v.nlist);
+    if (ix->coarse_t && np <= kProbeMaxNp && v.nlist >= 256 && per_warp <= kSmemLimit && probe_mma_enabled()) {
+        const uint32_t K = mma_k(v.dim);
+        const uint32_t ntiles = (v.nlist + kMmaN - 1) / kMmaN;
+        const size_t ld = mma_ld(v.nlist);
+        DevBuf approx(sizeof(float) * nq * ld, st);
+        const size_t smem = probe_mma_smem(K);
+        CK(cudaFuncSetAttribute(trim_probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        const dim3 grid(static_cast<unsigned>((nq + kMmaM - 1) / kMmaM), (ntiles + kMmaTilesPerCta - 1) / kMmaTilesPerCta);
+        trim_probe_mma_kernel<<<grid, kMmaThreads, smem, st>>>(d_q, nq, v.dim_stride, K, ix->coarse_t, ix->cn2,
+                                                                v.nlist, approx.as<float>());
+        CK(cudaGetLastError());
+        const uint32_t warps = static_cast<uint32_t>(std::min<size_t>(kSelWarps, kSmemLimit / per_warp));
+        const size_t ssmem = per_warp * warps;
+        CK(cudaFuncSetAttribute(trim_probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(ssmem)));
+        trim_probe_select_kernel<<<static_cast<unsigned>((nq + warps - 1) / warps), warps * 32, ssmem, st>>>(
+            v, d_q, nq, np, approx.as<float>(), ix->cn2, ix->cn, d_out);
+        CK(cudaGetLastError());
+        return;
+    }
     if (np <= kProbeMaxNp) {
         for (uint32_t tile = 128; tile >= 32; tile >>= 1) {
             const size_t smem = probe_tiled_smem(v.nlist, v.dim_stride, tile);
@@ -496,6 +528,13 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
         const bool host = d->memory == TRIM_MEM_HOST;
         const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         DeviceGuard g(d->device);
+        { // keep stream-ordered workspaces (probe scratch, results) cached in the pool
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
         auto* ix = new trim_index;
         ix->device = d->device;
         // host copies of the small arrays (sub_dims, offsets)
@@ -628,6 +667,16 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
             ix->d_skipped = ix->alloc<unsigned long long>(1);
             CK(cudaMemset(ix->d_skipped, 0, sizeof(unsigned long long)));
             trim_list_meta_kernel<<<d->nlist, kThreads>>>(v, lr, lxmin, lxmax);
+            CK(cudaGetLastError());
+            if (mma_k(v.dim) <= kMmaMaxK) {
+                const uint32_t K = mma_k(v.dim), ntiles = (d->nlist + kMmaN - 1) / kMmaN;
+                ix->coarse_t = ix->alloc<float4>(static_cast<size_t>(ntiles) * (K / 4) * kMmaN);
+                ix->cn2 = ix->alloc<float>(d->nlist);
+                ix->cn = ix->alloc<float>(d->nlist);
+                trim_coarse_tile_kernel<<<ntiles, kThreads>>>(v, K, ix->coarse_t);
+                CK(cudaGetLastError());
+                trim_coarse_norm_kernel<<<(d->nlist + kThreads - 1) / kThreads, kThreads>>>(v, ix->cn2, ix->cn);
+            }
             CK(cudaGetLastError());
             CK(cudaDeviceSynchronize());
         } catch (...) {

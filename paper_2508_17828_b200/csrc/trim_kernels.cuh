@@ -772,6 +772,9 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
 }
 
 #ifndef TRIM_M // non-template kernels: compiled once, in trim_capi.cu
+} // namespace trimgpu
+#include "trim_probe_mma.cuh"
+namespace trimgpu {
 // --------------------------------------------------------------------------
 // trim_probe_kernel — probe_order (ivf.hpp:173-187): coarse distances in the
 // reference's arithmetic, sorted by (dist, list id) in shared memory, first

@@ -270,8 +270,8 @@ bool probe_mma_enabled() {
 void launch_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t np, uint32_t* d_out,
                   cudaStream_t st) {
     const DevIndex& v = ix->dev;
-    const size_t per_warp = probe_select_smem_per_warp(v.nlist);
-    if (ix->coarse_t && np <= kProbeMaxNp && v.nlist >= 256 && per_warp <= kSmemLimit && probe_mma_enabled()) {
+    const size_t ssmem = probe_select_smem(v.nlist, v.dim_stride);
+    if (ix->coarse_t && np <= kProbeMaxNp && v.nlist >= 256 && ssmem <= kSmemLimit && probe_mma_enabled()) {
         const uint32_t K = mma_k(v.dim);
         const uint32_t ntiles = (v.nlist + kMmaN - 1) / kMmaN;
         const size_t ld = mma_ld(v.nlist);
@@ -283,11 +283,9 @@ void launch_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t 
         trim_probe_mma_kernel<<<grid, kMmaThreads, smem, st>>>(d_q, nq, v.dim_stride, K, ix->coarse_t, ix->cn2,
                                                                 v.nlist, approx.as<float>());
         CK(cudaGetLastError());
-        const uint32_t warps = static_cast<uint32_t>(std::min<size_t>(kSelWarps, kSmemLimit / per_warp));
-        const size_t ssmem = per_warp * warps;
         CK(cudaFuncSetAttribute(trim_probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(ssmem)));
-        trim_probe_select_kernel<<<static_cast<unsigned>((nq + warps - 1) / warps), warps * 32, ssmem, st>>>(
+        trim_probe_select_kernel<<<static_cast<unsigned>(nq), kPSelThreads, ssmem, st>>>(
             v, d_q, nq, np, approx.as<float>(), ix->cn2, ix->cn, d_out);
         CK(cudaGetLastError());
         return;

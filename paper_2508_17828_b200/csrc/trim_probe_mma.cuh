@@ -14,13 +14,14 @@
 //     (relative input error <= 2^-10, so |dot error| <= 2^-8.9 |q||c| by
 //     Cauchy-Schwarz, accumulation included), the fp32 epilogue and norms
 //     are far inside the second term; both terms carry a 2x margin.
-//  2. trim_probe_select_kernel (one warp per query): tau = np-th smallest
-//     upper bound U_c = D~_c + E_c; every list the exact order can place in
-//     the first np has L_c = D~_c - E_c <= tau (np lists have d <= tau, a list
-//     with L_c > tau has d > tau: strictly worse than all of them). Those
+//  2. trim_probe_select_kernel (one CTA per query): tau >= the np-th
+//     smallest upper bound U_c = D~_c + E_c (two 11-bit radix passes, bucket
+//     upper edge); every list the exact order can place in the first np has
+//     L_c = D~_c - E_c <= tau (np lists have d <= tau, a list with L_c > tau
+//     has d > tau: strictly worse than all of them). Those
 //     candidates get the exact reference-order distance and are sorted by
 //     (d, id); the first np are the reference's probe order. If more than
-//     kSelCap lists survive (degenerate data), the warp computes every exact
+//     kSelCap lists survive (degenerate data), the CTA computes every exact
 //     distance and selects among them directly — same result, slower.
 #pragma once
 
@@ -34,7 +35,6 @@ constexpr uint32_t kMmaTilesPerCta = 2;
 constexpr uint32_t kMmaThreads = 192;  // warp 0: loads, warp 1: MMA, warps 2-5: epilogue
 constexpr uint32_t kMmaMaxK = 128;     // K = dim rounded up to 8
 constexpr uint32_t kSelCap = 512;      // exact-distance candidates per query
-constexpr uint32_t kSelWarps = 8;
 
 __host__ __device__ inline uint32_t mma_k(uint32_t dim) { return (dim + 7u) & ~7u; }
 __host__ __device__ inline size_t mma_tile_bytes(uint32_t K) { return size_t(kMmaN) * K * 4u; }
@@ -353,117 +353,218 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* sq, uint32_t n2, uint32_t
         }
 }
 
-__host__ __device__ inline size_t probe_select_smem_per_warp(uint32_t nlist) {
-    return sizeof(uint32_t) * nlist + sizeof(uint32_t) * 256 + sizeof(uint64_t) * kSelCap;
+constexpr uint32_t kPSelThreads = 256;
+
+__host__ __device__ inline size_t probe_select_smem(uint32_t nlist, uint32_t dim_stride) {
+    return sizeof(uint64_t) * kSelCap + sizeof(uint32_t) * nlist + sizeof(uint32_t) * 2048 +
+           sizeof(float) * dim_stride + 64;
 }
 
-// One warp per query; warps per CTA = blockDim.x / 32.
-__global__ void trim_probe_select_kernel(DevIndex ix, const float* __restrict__ queries, uint64_t nq, uint32_t np,
-                                         const float* __restrict__ approx, const float* __restrict__ cn2,
-                                         const float* __restrict__ cn, uint32_t* __restrict__ probe_out) {
-    extern __shared__ __align__(16) unsigned char ps_smem[];
+// Block-wide exclusive scan of one value per thread (kPSelThreads threads);
+// returns the exclusive prefix, *total the sum. ws: 8 words of scratch.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<uint32_t>(o))
+            incl += t;
+    }
+    if (lane == 31)
+        ws[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < kPSelThreads / 32; ++w) {
+        const uint32_t x = ws[w];
+        before += w < warp ? x : 0u;
+        tot += x;
+    }
+    __syncthreads();
+    *total = tot;
+    return before + incl - v;
+}
+
+// Block radix select over keys[0..n) (shared memory): digits of 11, 11 and 10
+// bits from the top. Returns the key prefix after `passes` passes; with 3
+// passes that is the rank-th smallest key (1-based) itself.
+__device__ __forceinline__ uint32_t block_radix_select(const uint32_t* keys, uint32_t n, uint32_t rank,
+                                                       uint32_t* hist, uint32_t* sc, int passes) {
+    const uint32_t tid = threadIdx.x;
+    uint32_t prefix = 0, pmask = 0;
+    for (int p = 0; p < passes; ++p) {
+        const uint32_t shift = p == 0 ? 21u : (p == 1 ? 10u : 0u);
+        const uint32_t nb = p < 2 ? 2048u : 1024u;
+        for (uint32_t i = tid; i < nb; i += kPSelThreads)
+            hist[i] = 0;
+        __syncthreads();
+        for (uint32_t c = tid; c < n; c += kPSelThreads) {
+            const uint32_t kk = keys[c];
+            if ((kk & pmask) == prefix)
+                atomicAdd(&hist[(kk >> shift) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        const uint32_t per = nb / kPSelThreads; // 8 or 4 bins per thread
+        uint32_t s = 0;
+        for (uint32_t i = 0; i < per; ++i)
+            s += hist[tid * per + i];
+        uint32_t tot;
+        const uint32_t excl = block_excl_scan(s, sc + 8, &tot);
+        if (excl < rank && rank <= excl + s) {
+            uint32_t cum = excl;
+            for (uint32_t i = 0; i < per; ++i) {
+                const uint32_t h = hist[tid * per + i];
+                if (cum + h >= rank) {
+                    sc[0] = tid * per + i;
+                    sc[1] = cum;
+                    break;
+                }
+                cum += h;
+            }
+        }
+        __syncthreads();
+        prefix |= sc[0] << shift;
+        pmask |= (nb - 1) << shift;
+        rank -= sc[1];
+        __syncthreads();
+    }
+    return prefix;
+}
+
+// Block bitonic sort of n2 (power of two) u64 keys in shared memory, ascending.
+__device__ __forceinline__ void block_bitonic(uint64_t* sq, uint32_t n2) {
+    for (uint32_t size = 2; size <= n2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < n2 / 2; i += kPSelThreads) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = sq[lo], b = sq[hi];
+                if ((a > b) == up) {
+                    sq[lo] = b;
+                    sq[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// One CTA (kPSelThreads) per query.
+__global__ void __launch_bounds__(kPSelThreads)
+trim_probe_select_kernel(DevIndex ix, const float* __restrict__ queries, uint64_t nq, uint32_t np,
+                         const float* __restrict__ approx, const float* __restrict__ cn2,
+                         const float* __restrict__ cn, uint32_t* __restrict__ probe_out) {
+    extern __shared__ __align__(16) unsigned char ps_smem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
     if (q >= nq)
         return;
     const uint32_t nlist = ix.nlist;
-    unsigned char* base = ps_smem + probe_select_smem_per_warp(nlist) * warp;
-    uint64_t* sq = reinterpret_cast<uint64_t*>(base);                    // [kSelCap]
-    uint32_t* keys = reinterpret_cast<uint32_t*>(sq + kSelCap);          // [nlist]
-    uint32_t* h = keys + nlist;                                          // [256]
+    uint64_t* sq = reinterpret_cast<uint64_t*>(ps_smem);          // [kSelCap]
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sq + kSelCap);   // [nlist]
+    uint32_t* hist = keys + nlist;                                // [2048]
+    float* qv = reinterpret_cast<float*>(hist + 2048);            // [dim_stride]
+    uint32_t* sc = reinterpret_cast<uint32_t*>(qv + ix.dim_stride); // [16] scalars
     const float* qrow = queries + q * ix.dim_stride;
     const float* arow = approx + q * mma_ld(nlist);
 
-    float qn2 = 0.0f;
-    for (uint32_t i = lane; i < ix.dim; i += 32)
-        qn2 = __fadd_ru(qn2, __fmul_ru(qrow[i], qrow[i]));
-    for (int o = 16; o > 0; o >>= 1)
-        qn2 = __fadd_ru(qn2, __shfl_xor_sync(0xffffffffu, qn2, o));
-    qn2 = __fmul_ru(qn2, 1.0f + 1.0f / 65536.0f);
-    const float qn = __fsqrt_ru(qn2);
-    auto err = [&](uint32_t c) {
-        return __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(cn + c)), 1.0f / 64.0f),
-                         __fmul_ru(__fadd_ru(qn2, __ldg(cn2 + c)), 1.0f / 16384.0f));
-    };
-    for (uint32_t c = lane; c < nlist; c += 32)
-        keys[c] = f2key(__fadd_ru(arow[c], err(c)));
-    __syncwarp();
-    const float tau = key2f(warp_radix_select(keys, nlist, np, h, lane));
-    // candidates: lower bound <= tau
-    uint32_t ncand = 0;
-    bool over = false;
-    for (uint32_t c0 = 0; c0 < nlist; c0 += 32) {
-        const uint32_t c = c0 + lane;
-        const bool in = c < nlist && __fsub_rd(arow[c], err(c)) <= tau;
-        const uint32_t bal = __ballot_sync(0xffffffffu, in);
-        if (ncand + __popc(bal) > kSelCap) {
-            over = true;
-            break;
-        }
-        if (in)
-            keys[ncand + __popc(bal & ((1u << lane) - 1u))] = c;
-        ncand += __popc(bal);
+    float qp = 0.0f;
+    for (uint32_t i = tid; i < ix.dim_stride; i += kPSelThreads) {
+        const float x = qrow[i];
+        qv[i] = x;
+        qp = __fadd_ru(qp, __fmul_ru(x, x));
     }
-    __syncwarp();
+    for (int o = 16; o > 0; o >>= 1)
+        qp = __fadd_ru(qp, __shfl_xor_sync(0xffffffffu, qp, o));
+    if (lane == 0)
+        hist[warp] = __float_as_uint(qp);
+    __syncthreads();
+    float qn2 = 0.0f;
+    for (uint32_t w = 0; w < kPSelThreads / 32; ++w)
+        qn2 = __fadd_ru(qn2, __uint_as_float(hist[w]));
+    qn2 = __fmul_ru(qn2, 1.0f + 1.0f / 65536.0f); // >= |q|^2
+    const float qn = __fsqrt_ru(qn2);
+    __syncthreads();
+
+    // upper bounds U_c = D~_c + E_c as orderable keys
+    for (uint32_t c = tid; c < nlist; c += kPSelThreads) {
+        const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(cn + c)), 1.0f / 64.0f),
+                                  __fmul_ru(__fadd_ru(qn2, __ldg(cn2 + c)), 1.0f / 16384.0f));
+        keys[c] = f2key(__fadd_ru(arow[c], e));
+    }
+    __syncthreads();
+    // tau' >= np-th smallest U: the top 22 key bits, bucket upper edge
+    const float tau = key2f(block_radix_select(keys, nlist, np, hist, sc, 2) | 0x3FFu);
+    if (tid == 0)
+        sc[2] = 0;
+    __syncthreads();
+    // candidates: lower bound L_c = D~_c - E_c <= tau'
+    for (uint32_t c = tid; c < nlist; c += kPSelThreads) {
+        const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(cn + c)), 1.0f / 64.0f),
+                                  __fmul_ru(__fadd_ru(qn2, __ldg(cn2 + c)), 1.0f / 16384.0f));
+        if (__fsub_rd(arow[c], e) <= tau) {
+            const uint32_t slot = atomicAdd(&sc[2], 1u);
+            if (slot < kSelCap)
+                keys[slot] = c; // (U keys are no longer needed)
+        }
+    }
+    __syncthreads();
+    const uint32_t ncand = sc[2];
     uint32_t* out = probe_out + q * np;
-    if (!over) {
+    if (ncand <= kSelCap) {
         uint32_t n2 = 1;
         while (n2 < ncand)
             n2 <<= 1;
-        for (uint32_t i = lane; i < n2; i += 32) {
+        for (uint32_t i = tid; i < n2; i += kPSelThreads) {
             uint64_t kk = ~0ull;
             if (i < ncand) {
                 const uint32_t c = keys[i];
-                const float d = euclid_sq_vec4(qrow, ix.coarse + static_cast<size_t>(c) * ix.dim_stride, ix.dim);
+                const float d = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(c) * ix.dim_stride, ix.dim);
                 kk = (static_cast<uint64_t>(__float_as_uint(d)) << 32) | c;
             }
             sq[i] = kk;
         }
-        __syncwarp();
-        warp_bitonic(sq, n2, lane);
-        for (uint32_t i = lane; i < np; i += 32)
+        __syncthreads();
+        block_bitonic(sq, n2);
+        for (uint32_t i = tid; i < np; i += kPSelThreads)
             out[i] = static_cast<uint32_t>(sq[i] & 0xffffffffu);
         return;
     }
-    // degenerate: exact distances of every list, exact selection
-    for (uint32_t c = lane; c < nlist; c += 32)
-        keys[c] = __float_as_uint(
-            euclid_sq_vec4(qrow, ix.coarse + static_cast<size_t>(c) * ix.dim_stride, ix.dim));
-    __syncwarp();
-    const uint32_t kth = warp_radix_select(keys, nlist, np, h, lane);
-    uint32_t n_lt = 0, n_eq = 0, need_eq = 0;
-    for (uint32_t c0 = 0; c0 < nlist; c0 += 32) { // count keys below kth
-        const uint32_t c = c0 + lane;
-        n_lt += __popc(__ballot_sync(0xffffffffu, c < nlist && keys[c] < kth));
-    }
-    need_eq = np - n_lt;
-    n_lt = 0;
-    for (uint32_t c0 = 0; c0 < nlist; c0 += 32) {
-        const uint32_t c = c0 + lane;
-        const uint32_t kk = c < nlist ? keys[c] : 0xFFFFFFFFu;
-        const bool lt = c < nlist && kk < kth;
-        const bool eq = c < nlist && kk == kth;
-        const uint32_t blt = __ballot_sync(0xffffffffu, lt);
-        const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-        const uint32_t below = (1u << lane) - 1u;
-        if (lt)
-            sq[n_lt + __popc(blt & below)] = (static_cast<uint64_t>(kk) << 32) | c;
-        if (eq) {
-            const uint32_t r = n_eq + __popc(beq & below);
-            if (r < need_eq)
-                sq[np - need_eq + r] = (static_cast<uint64_t>(kk) << 32) | c;
+    // degenerate (too many candidates): exact distances of every list
+    for (uint32_t c = tid; c < nlist; c += kPSelThreads)
+        keys[c] = __float_as_uint(euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(c) * ix.dim_stride, ix.dim));
+    __syncthreads();
+    const uint32_t kth = block_radix_select(keys, nlist, np, hist, sc, 3);
+    if (tid == 0)
+        sc[2] = 0;
+    __syncthreads();
+    for (uint32_t c = tid; c < nlist; c += kPSelThreads) // keys below the np-th: fewer than np
+        if (keys[c] < kth)
+            sq[atomicAdd(&sc[2], 1u)] = (static_cast<uint64_t>(keys[c]) << 32) | c;
+    __syncthreads();
+    const uint32_t n_lt = sc[2];
+    if (warp == 0) { // ties at the np-th distance: the lowest list ids, in order
+        uint32_t n_eq = 0;
+        const uint32_t need = np - n_lt;
+        for (uint32_t c0 = 0; c0 < nlist && n_eq < need; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            const bool eq = c < nlist && keys[c] == kth;
+            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+            const uint32_t r = n_eq + __popc(beq & ((1u << lane) - 1u));
+            if (eq && r < need)
+                sq[n_lt + r] = (static_cast<uint64_t>(kth) << 32) | c;
+            n_eq += __popc(beq);
         }
-        n_lt += __popc(blt);
-        n_eq += __popc(beq);
     }
     uint32_t n2 = 1;
     while (n2 < np)
         n2 <<= 1;
-    for (uint32_t i = np + lane; i < n2; i += 32)
+    for (uint32_t i = np + tid; i < n2; i += kPSelThreads)
         sq[i] = ~0ull;
-    __syncwarp();
-    warp_bitonic(sq, n2, lane);
-    for (uint32_t i = lane; i < np; i += 32)
+    __syncthreads();
+    block_bitonic(sq, n2);
+    for (uint32_t i = tid; i < np; i += kPSelThreads)
         out[i] = static_cast<uint32_t>(sq[i] & 0xffffffffu);
 }
 

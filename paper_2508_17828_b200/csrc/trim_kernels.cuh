@@ -221,7 +221,7 @@ __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t di
     b += sizeof(uint32_t) * kRing * kChunkW * 4; // superset bins: id, est_lo, est_hi, d
     b += sizeof(uint32_t) * kRing * kWorkers * 2; // bin counts, bin lane masks
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan barrier
+    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan + seed barriers
     b += 16;                                     // published threshold, plan length
     return b;
 }
@@ -309,13 +309,15 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // next chunk's codes are prefetched into registers while the current one is
 // filtered.
 //
-// After chunk 0 (positions [0, 224), which hold every seed when k <= 224) the
-// replay warp plans the rest of the stream: a probed list that starts at
-// position >= 224 and whose list_lower_bound is >= the published T is pruned
-// as a whole (every entry has est >= L >= T >= T_live: the reference prunes
-// each of them, ivf.hpp:275), and the remaining positions are compacted in
-// place into cum/base. Chunks c >= 1 walk the compacted stream. Counters are
-// unchanged: skipped entries are evaluated-and-pruned positions.
+// The replay warp first evaluates the k seeds (ivf.hpp:264-271) itself and
+// publishes the seeded threshold, so no chunk is filtered against +inf.
+// After chunk 0 (positions [0, 224)) it plans the rest of the stream from
+// p0 = max(224, k): a probed list that starts at or after p0 and whose
+// list_lower_bound is >= the published T is pruned as a whole (every entry
+// has est >= L >= T >= T_live: the reference prunes each of them,
+// ivf.hpp:275), and the remaining positions are compacted in place into
+// cum/base. Chunks c >= 1 walk the compacted stream. Counters are unchanged:
+// skipped entries are evaluated-and-pruned positions.
 // --------------------------------------------------------------------------
 template <int M, int KS, int S>
 __global__ void __launch_bounds__(kThreads, (M == 0 || M > 64) ? 2 : 3)
@@ -350,6 +352,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
     uint64_t* empty = full + kRing;
     uint64_t* plan = empty + kRing;
+    uint64_t* seedbar = plan + 1;
     float* s_T = reinterpret_cast<float*>(plan + 2);
     uint32_t* s_total2 = reinterpret_cast<uint32_t*>(s_T + 1);
 
@@ -365,6 +368,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             mbar_init(empty + s, kWarp);
         }
         mbar_init(plan, kWarp);
+        mbar_init(seedbar, kWarp);
         *s_T = kInf;
     }
     __syncthreads();
@@ -375,12 +379,41 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
 
     if (warp == 0) {
         // ------------------------------------------------ replay warp
-        const bool skip = p.skip_lists && p.probe && p.k <= kChunkW && nchunks0 > 1;
+        WarpTopK<S> topk;
+        topk.init(p.k);
+        // seeds (ivf.hpp:264-271): the first min(k, total) positions are evaluated
+        // unconditionally; done here, before any chunk, so every worker filters
+        // with the seeded threshold (max_dis after the seeds)
+        const uint32_t nseed = min(p.k, total);
+        for (uint32_t b0 = 0; b0 < nseed; b0 += kWarp) {
+            const uint32_t i = b0 + lane;
+            float d = 0.0f;
+            uint32_t id = 0;
+            if (i < nseed) {
+                uint32_t li = 0;
+                while (st.cum[li + 1] <= i)
+                    ++li;
+                const uint64_t e = st.base[li] + (i - st.cum[li]);
+                id = __ldg(ix.list_ids + e);
+                d = euclid_sq_vec4(qv, ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride, ix.dim);
+            }
+            const uint32_t cnt = min(static_cast<uint32_t>(kWarp), nseed - b0);
+            for (uint32_t j = 0; j < cnt; ++j)
+                topk.offer(__shfl_sync(0xffffffffu, d, j), __shfl_sync(0xffffffffu, id, j));
+        }
+        if (lane == 0)
+            *reinterpret_cast<volatile float*>(s_T) = topk.wd;
+        __syncwarp();
+        mbar_arrive(seedbar);
+        // the stream after chunk 0 and the seeds starts at p0; the plan may skip
+        // whole lists from there on
+        const uint32_t p0 = max(kChunkW, p.k);
+        const bool skip = p.skip_lists && p.probe && total > p0;
         if (skip) { // T-independent part of the plan, overlapped with chunk 0
             const uint32_t* pl = p.probe + static_cast<size_t>(q) * p.np;
             for (uint32_t i = lane; i < p.np; i += kWarp) {
                 float lb = 0.0f;
-                if (st.cum[i] >= kChunkW) {
+                if (st.cum[i] >= p0) {
                     const uint32_t l = __ldg(pl + i);
                     const float dq = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(l) * ix.dim_stride,
                                                     ix.dim);
@@ -390,9 +423,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 s_lb[i] = lb;
             }
         }
-        WarpTopK<S> topk;
-        topk.init(p.k);
-        uint64_t dc = 0;
+        uint64_t dc = nseed;
         uint32_t nchunks = nchunks0;
         uint32_t ncum = p.np; // lists in the current cum/base layout
         // The reference-order est of a member whose interval straddles the live
@@ -427,8 +458,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 for (uint32_t i = 0; i < cnt; ++i) {
                     const float lo = s_lo[g0 + i];
                     if (lo < topk.wd) { // else est >= lo >= T_live: pruned (ivf.hpp:275)
-                        bool ev = true; // seeds (lo = -inf) and hi < T_live: est < T_live
-                        if (lo != kNegInf && !(s_hi[g0 + i] < topk.wd))
+                        bool ev = true; // hi < T_live: est < T_live
+                        if (!(s_hi[g0 + i] < topk.wd))
                             ev = exact_est(c, w, i, bin_mask[s * kWorkers + w]) < topk.wd;
                         if (ev) {
                             ++dc;
@@ -450,8 +481,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     uint64_t bs = 0;
                     if (i < p.np) {
                         const uint32_t c0 = st.cum[i], c1 = st.cum[i + 1];
-                        if (c1 > kChunkW && !(skip && c0 >= kChunkW && s_lb[i] >= T)) {
-                            const uint32_t s0 = max(c0, kChunkW);
+                        if (c1 > p0 && !(skip && c0 >= p0 && s_lb[i] >= T)) {
+                            const uint32_t s0 = max(c0, p0);
                             len = c1 - s0;
                             bs = st.base[i] + (s0 - c0);
                         }
@@ -477,8 +508,9 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 if (lane == 0) {
                     st.cum[nk] = carry;
                     *s_total2 = carry;
-                    if (p.skipped && total - kChunkW != carry)
-                        atomicAdd(p.skipped, static_cast<unsigned long long>(total - kChunkW - carry));
+                    const uint32_t rest = total > p0 ? total - p0 : 0u;
+                    if (p.skipped && rest != carry)
+                        atomicAdd(p.skipped, static_cast<unsigned long long>(rest - carry));
                 }
                 nchunks = 1 + (carry + kChunkW - 1) / kChunkW;
                 ncum = nk;
@@ -524,14 +556,14 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         FastCode<M> fc;
         float lx;
         uint32_t e;
-        uint32_t kind; // 0: past the end, 1: seed, 2: candidate
+        uint32_t kind; // 0: past the end or a seed, 2: candidate
     };
     struct Slot {
         Cand c[kLaneU];
     };
     Slot sa, sb; // double buffer in registers (static names: no local-memory indexing)
-    // chunk 0: original positions [0, 224); chunk c >= 1: compacted positions
-    // (c-1)*224 + ... (original position >= 224 + that, equal when nothing is skipped)
+    // chunk 0: original positions [0, 224) (seeds excluded); chunk c >= 1:
+    // compacted positions (c-1)*224 + ..., the kept stream from p0 = max(224, k)
     auto fetch = [&](uint32_t c, Slot& d) {
 #pragma unroll
         for (uint32_t u = 0; u < kLaneU; ++u) {
@@ -544,10 +576,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 while (st.cum[li + 1] <= pp)
                     ++li;
                 x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
-                // seeds (ivf.hpp:264-271) are always evaluated; beyond chunk 0 they
-                // occur only when k > 224, where nothing is skipped
-                const uint32_t orig = c == 0 ? pp : pp + kChunkW;
-                x.kind = orig < p.k ? 1u : 2u;
+                // the seeds (positions < k) were evaluated by the replay warp
+                x.kind = (c == 0 && pp < p.k) ? 0u : 2u;
                 if (x.kind == 2u) {
                     x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
                     x.lx = __ldg(ix.lx + x.e);
@@ -561,18 +591,14 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         const uint32_t s = c % kRing;
         if (c >= kRing)
             mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
-        float T = ld_volatile(s_T);
-        if (T == kInf && c >= 1) { // the seeds are not replayed yet: wait for chunk c-1
-            mbar_wait(empty + (c - 1) % kRing, ((c - 1) / kRing) & 1u);
-            T = ld_volatile(s_T);
-        }
+        const float T = ld_volatile(s_T);
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
         Cand& x = cur.c[0];
         const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
         const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
         // member = seed, or a candidate whose est interval [lo, hi] starts below T
         float lo = kNegInf, hi = kNegInf;
-        bool keep = x.kind == 1u;
+        bool keep = false;
         if (x.kind == 2u && a >= 0.0f) {
             lo = est_lower_bound(a, x.lx, p.two_gamma, p.adc_eps);
             keep = lo < T;
@@ -601,6 +627,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         mbar_arrive(full + s);
     };
     fetch(0, sa);
+    mbar_wait(seedbar, 0); // the seeded threshold is published
     process(0, sa);
     if (nchunks0 <= 1)
         return;

@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrim_b200.so")
+# TRIM_B200_LIB selects another build of the library (the perf-probe build
+# libtrim_b200_tl.so, profiles/knn_timeline.py); default: the production build.
+LIB_PATH = os.environ.get("TRIM_B200_LIB") or os.path.join(HERE, "libtrim_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "trim_gpu.h")
 
 TRIM_OK, TRIM_EINVAL, TRIM_EDATA, TRIM_ECUDA, TRIM_ENCCL, TRIM_ENOMEM = range(6)

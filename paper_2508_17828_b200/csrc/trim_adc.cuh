@@ -88,22 +88,22 @@ __device__ __forceinline__ float sub_dist(const float* q, const float* c) {
 // keeps 8 centroid loads in flight (the generic loop below is latency-bound).
 template <uint32_t SD>
 __device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const float* q_smem, float* lut,
-                                                  const LutShape& sh) {
+                                                  const LutShape& sh, uint32_t t0, uint32_t nt) {
     const uint32_t hrow = sh.half_row_bytes() / 4;
     float* hblk = lut + sh.nfull * (kFullBytes / 4);
     const uint32_t total = ix.m * ix.ksub;
-    for (uint32_t i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
+    for (uint32_t i0 = t0; i0 < total; i0 += 8 * nt) {
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const uint32_t i = i0 + u * blockDim.x;
+            const uint32_t i = i0 + u * nt;
             const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
             v[u] = i < total ? sub_dist<SD>(q_smem + j * SD, ix.centroids + (static_cast<size_t>(ix.ksub) * j + c) * SD)
                              : 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const uint32_t i = i0 + u * blockDim.x;
+            const uint32_t i = i0 + u * nt;
             if (i >= total)
                 break;
             const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
@@ -119,21 +119,23 @@ __device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const floa
     }
 }
 
-__device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const float* q_smem, float* lut) {
+// Threads t0 (of nt participating) build the table; defaults: the whole CTA.
+__device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const float* q_smem, float* lut,
+                                                  uint32_t t0 = threadIdx.x, uint32_t nt = blockDim.x) {
     const LutShape sh = LutShape::of(ix.m);
     const uint32_t hrow = sh.half_row_bytes() / 4;          // floats per HALF row
     float* hblk = lut + sh.nfull * (kFullBytes / 4);
     if (ix.sd_uniform == 2)
-        build_lut_uniform<2>(ix, q_smem, lut, sh);
+        build_lut_uniform<2>(ix, q_smem, lut, sh, t0, nt);
     else if (ix.sd_uniform == 4)
-        build_lut_uniform<4>(ix, q_smem, lut, sh);
+        build_lut_uniform<4>(ix, q_smem, lut, sh, t0, nt);
     else
     for (uint32_t j = 0; j < ix.m; ++j) {
         const uint32_t sd = ix.sub_dims[j];
         const uint32_t off = ix.sub_offsets[j];
         const float* cb = ix.centroids + static_cast<size_t>(ix.ksub) * off;
         const uint32_t b = j >> 5, t = j & 31u;
-        for (uint32_t c = threadIdx.x; c < ix.ksub; c += blockDim.x) {
+        for (uint32_t c = t0; c < ix.ksub; c += nt) {
             const float v = euclid_sq_generic(q_smem + off, cb + c * sd, sd);
             if (b < sh.nfull) {
                 lut[b * (kFullBytes / 4) + c * 32 + t] = v;
@@ -150,7 +152,7 @@ __device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const floa
     if (rem) {
         const uint32_t width = sh.half ? 16u : 32u;
         const uint32_t pad = width - rem;
-        for (uint32_t i = threadIdx.x; i < 256 * pad; i += blockDim.x) {
+        for (uint32_t i = t0; i < 256 * pad; i += nt) {
             const uint32_t c = i / pad, t = rem + i % pad;
             if (sh.half) {
                 hblk[c * hrow + t] = 0.0f;

@@ -27,6 +27,9 @@ using namespace trimgpu;
 namespace {
 
 thread_local std::string g_err;
+// Perf probe (profiles/knn_timeline.py): device buffer of nq*kTimeline u64 that the next kNN
+// launches on this thread fill with per-CTA phase timestamps; null disables.
+thread_local unsigned long long* g_timeline = nullptr;
 
 int set_err(int code, const char* fmt, ...) {
     char buf[1024];
@@ -390,6 +393,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         p.omg_lo = omg_round_down(gamma);
         p.skip_lists = list_skip_enabled() ? 1u : 0u;
         p.skipped = ix->d_skipped;
+        p.timeline = g_timeline;
     }
     // grid.x is limited to 2^31-1; process huge batches in slices
     const uint64_t kMaxGrid = 1u << 30;
@@ -401,6 +405,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         pb.ids_out = d_ids + b * k;
         pb.dist_out = d_dist + b * k;
         pb.counters = d_ct ? d_ct + b * 6 : nullptr;
+        pb.timeline = p.timeline ? p.timeline + b * kTimeline : nullptr;
         launch_knn(ix->dev, pb, smem, st);
     }
     return TRIM_OK;
@@ -494,6 +499,8 @@ extern "C" {
 const char* trim_last_error(void) { return g_err.c_str(); }
 
 void trim__set_last_error(const char* msg) { g_err = msg; }
+
+void trim__set_knn_timeline(void* d_buf) { g_timeline = static_cast<unsigned long long*>(d_buf); }
 
 int trim_abi_version(void) { return TRIM_ABI_VERSION; }
 

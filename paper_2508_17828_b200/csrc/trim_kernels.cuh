@@ -200,7 +200,22 @@ struct KnnParams {
     float kq2;               // 1 - relative error bound of sqrt(reference ADC)
     float kest;              // 1 - relative error bound of relaxed_lb's evaluation
     unsigned long long* skipped; // positions skipped by the list bound (diagnostic)
+    unsigned long long* timeline; // nq*kTimeline phase stamps/cycle counts (perf probe only), or null
 };
+
+constexpr uint32_t kTimeline = 16;
+// Phase instrumentation of trim_knn_kernel, compiled only into the perf-probe
+// build of the library (make timeline -> libtrim_b200_tl.so).
+#ifdef TRIM_TIMELINE
+#define TRIM_TL(...) __VA_ARGS__
+#else
+#define TRIM_TL(...)
+#endif
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Warp-specialised pipeline: warp 0 replays, warps 1..kWorkers filter.
 constexpr uint32_t kWorkers = kWarps - 1;          // 7
@@ -216,12 +231,11 @@ __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t di
     b += sizeof(float) * dim_stride;             // query
     b += sizeof(uint64_t) * np;                  // base
     b += sizeof(uint32_t) * (np + 1);            // cum
-    b += sizeof(float) * np;                     // per-list lower bounds
     b = (b + 15) & ~size_t(15);
     b += sizeof(uint32_t) * kRing * kChunkW * 4; // superset bins: id, est_lo, est_hi, d
     b += sizeof(uint32_t) * kRing * kWorkers * 2; // bin counts, bin lane masks
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan + seed barriers
+    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan barrier (+pad)
     b += 16;                                     // published threshold, plan length
     return b;
 }
@@ -337,8 +351,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     off += sizeof(uint64_t) * p.np;
     st.cum = reinterpret_cast<uint32_t*>(smem + off);
     off += sizeof(uint32_t) * (p.np + 1);
-    float* s_lb = reinterpret_cast<float*>(smem + off); // [np] list lower bounds
-    off += sizeof(float) * p.np;
     off = (off + 15) & ~size_t(15);
     uint32_t* s_e = reinterpret_cast<uint32_t*>(smem + off);  // [kRing][kChunkW]: id
     float* s_lo = reinterpret_cast<float*>(s_e + kRing * kChunkW); // est interval
@@ -352,13 +364,19 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
     uint64_t* empty = full + kRing;
     uint64_t* plan = empty + kRing;
-    uint64_t* seedbar = plan + 1;
     float* s_T = reinterpret_cast<float*>(plan + 2);
     uint32_t* s_total2 = reinterpret_cast<uint32_t*>(s_T + 1);
 
     const float kInf = __int_as_float(0x7f800000);
     const float kNegInf = __int_as_float(0xff800000);
 
+    TRIM_TL(unsigned long long* tl = p.timeline ? p.timeline + static_cast<size_t>(q) * kTimeline : nullptr;
+            if (tl && tid == 0) {
+                uint32_t smid;
+                asm("mov.u32 %0, %smid;" : "=r"(smid));
+                tl[0] = gtime();
+                tl[6] = smid;
+            })
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = tid; i < ix.dim_stride; i += kThreads)
         qv[i] = qg[i];
@@ -368,23 +386,22 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             mbar_init(empty + s, kWarp);
         }
         mbar_init(plan, kWarp);
-        mbar_init(seedbar, kWarp);
         *s_T = kInf;
     }
     __syncthreads();
-    build_lut_blocked(ix, qv, lut);
     const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
                                        p.np, st); // ends with a barrier
-    const uint32_t nchunks0 = (total + kChunkW - 1) / kChunkW;
+    // seeds [0, nseed) are the replay warp's; the candidate stream is the kept
+    // part of [nseed, total), compacted into cum/base by the plan
+    const uint32_t nseed = min(p.k, total);
 
     if (warp == 0) {
         // ------------------------------------------------ replay warp
+        // (the worker warps build the LUT meanwhile)
+        TRIM_TL(if (tl && lane == 0) tl[1] = gtime();)
         WarpTopK<S> topk;
         topk.init(p.k);
-        // seeds (ivf.hpp:264-271): the first min(k, total) positions are evaluated
-        // unconditionally; done here, before any chunk, so every worker filters
-        // with the seeded threshold (max_dis after the seeds)
-        const uint32_t nseed = min(p.k, total);
+        // seeds (ivf.hpp:264-271): evaluated unconditionally, in stream order
         for (uint32_t b0 = 0; b0 < nseed; b0 += kWarp) {
             const uint32_t i = b0 + lane;
             float d = 0.0f;
@@ -401,38 +418,73 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             for (uint32_t j = 0; j < cnt; ++j)
                 topk.offer(__shfl_sync(0xffffffffu, d, j), __shfl_sync(0xffffffffu, id, j));
         }
-        if (lane == 0)
-            *reinterpret_cast<volatile float*>(s_T) = topk.wd;
-        __syncwarp();
-        mbar_arrive(seedbar);
-        // the stream after chunk 0 and the seeds starts at p0; the plan may skip
-        // whole lists from there on
-        const uint32_t p0 = max(kChunkW, p.k);
-        const bool skip = p.skip_lists && p.probe && total > p0;
-        if (skip) { // T-independent part of the plan, overlapped with chunk 0
-            const uint32_t* pl = p.probe + static_cast<size_t>(q) * p.np;
-            for (uint32_t i = lane; i < p.np; i += kWarp) {
-                float lb = 0.0f;
-                if (st.cum[i] >= p0) {
+        const float T0 = topk.wd; // max_dis after the seeds
+        TRIM_TL(if (tl && lane == 0) tl[2] = gtime();)
+        // plan: drop every probed list after the seeds whose list_lower_bound
+        // is >= T0 (>= T_live at all its positions), compact the rest in place
+        const bool skip = p.skip_lists && p.probe && total > nseed;
+        const uint32_t* pl = p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr;
+        uint32_t carry = 0, nk = 0;
+        for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) {
+            const uint32_t i = b0 + lane;
+            uint32_t len = 0;
+            uint64_t bs = 0;
+            if (i < p.np) {
+                const uint32_t c0 = st.cum[i], c1 = st.cum[i + 1];
+                bool drop = c1 <= nseed;
+                if (!drop && skip && c0 >= nseed) {
                     const uint32_t l = __ldg(pl + i);
-                    const float dq = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(l) * ix.dim_stride,
-                                                    ix.dim);
-                    lb = list_lower_bound(dq, __ldg(ix.list_R + l), __ldg(ix.list_xmin + l),
-                                          __ldg(ix.list_xmax + l), p);
+                    const float dq = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(l) * ix.dim_stride, ix.dim);
+                    drop = list_lower_bound(dq, __ldg(ix.list_R + l), __ldg(ix.list_xmin + l),
+                                            __ldg(ix.list_xmax + l), p) >= T0;
                 }
-                s_lb[i] = lb;
+                if (!drop) {
+                    const uint32_t s0 = max(c0, nseed);
+                    len = c1 - s0;
+                    bs = st.base[i] + (s0 - c0);
+                }
             }
+            const uint32_t keep = __ballot_sync(0xffffffffu, len != 0);
+            uint32_t v = len;
+#pragma unroll
+            for (int o = 1; o < kWarp; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= static_cast<uint32_t>(o))
+                    v += t;
+            }
+            __syncwarp(); // this batch's reads precede its (lower-index) writes
+            if (len != 0) {
+                const uint32_t j = nk + __popc(keep & ((1u << lane) - 1u));
+                st.base[j] = bs;
+                st.cum[j] = carry + v - len;
+            }
+            carry += __shfl_sync(0xffffffffu, v, kWarp - 1);
+            nk += __popc(keep);
+            __syncwarp();
         }
+        if (lane == 0) {
+            st.cum[nk] = carry;
+            *s_total2 = carry;
+            *reinterpret_cast<volatile float*>(s_T) = T0;
+            const uint32_t rest = total - nseed;
+            if (p.skipped && rest != carry)
+                atomicAdd(p.skipped, static_cast<unsigned long long>(rest - carry));
+        }
+        const uint32_t nchunks = (carry + kChunkW - 1) / kChunkW;
+        const uint32_t ncum = nk;
+        TRIM_TL(if (tl && lane == 0) tl[3] = gtime();)
+        __syncwarp();
+        mbar_arrive(plan);
+
         uint64_t dc = nseed;
-        uint32_t nchunks = nchunks0;
-        uint32_t ncum = p.np; // lists in the current cum/base layout
+        TRIM_TL(uint32_t members = 0;)
         // The reference-order est of a member whose interval straddles the live
-        // threshold (rare): its stream position from the bin's lane mask, its
-        // entry from the cum/base layout, then pq::adc_lookup + relaxed_lb.
+        // threshold (rare): its compacted position from the bin's lane mask, its
+        // entry from cum/base, then pq::adc_lookup + relaxed_lb.
         auto exact_est = [&](uint32_t c, uint32_t w, uint32_t i, uint32_t mask) -> float {
             for (uint32_t r = 0; r < i; ++r)
                 mask &= mask - 1;
-            const uint32_t pp = (c == 0 ? 0u : (c - 1) * kChunkW) + w * kPerWorker + (__ffs(mask) - 1);
+            const uint32_t pp = c * kChunkW + w * kPerWorker + (__ffs(mask) - 1);
             uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
             while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
@@ -445,9 +497,12 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             const float a = adc_serial<M>(ix.codes + e * ix.code_stride, m);
             return relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
         };
+        TRIM_TL(unsigned long long cyc_wait = 0, cyc_busy = 0;)
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t s = c % kRing;
+            TRIM_TL(const unsigned long long k0 = tl ? clock64() : 0;)
             mbar_wait(full + s, (c / kRing) & 1u);
+            TRIM_TL(const unsigned long long k1 = tl ? clock64() : 0;)
             const uint32_t* cnts = bin_cnt + s * kWorkers;
             uint32_t bins = __ballot_sync(0xffffffffu, lane < kWorkers && cnts[lane] != 0);
             while (bins) {
@@ -455,6 +510,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 bins &= bins - 1;
                 const uint32_t cnt = cnts[w];
                 const uint32_t g0 = s * kChunkW + w * kPerWorker;
+                TRIM_TL(members += cnt;)
                 for (uint32_t i = 0; i < cnt; ++i) {
                     const float lo = s_lo[g0 + i];
                     if (lo < topk.wd) { // else est >= lo >= T_live: pruned (ivf.hpp:275)
@@ -468,58 +524,22 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     }
                 }
             }
-            const float T = topk.wd;
             if (lane == 0)
-                *reinterpret_cast<volatile float*>(s_T) = T;
-            if (c == 0 && nchunks0 > 1) {
-                // plan: compact the positions >= kChunkW of the lists that are kept
-                // (workers read cum/base again only after the plan barrier)
-                uint32_t carry = 0, nk = 0;
-                for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) {
-                    const uint32_t i = b0 + lane;
-                    uint32_t len = 0;
-                    uint64_t bs = 0;
-                    if (i < p.np) {
-                        const uint32_t c0 = st.cum[i], c1 = st.cum[i + 1];
-                        if (c1 > p0 && !(skip && c0 >= p0 && s_lb[i] >= T)) {
-                            const uint32_t s0 = max(c0, p0);
-                            len = c1 - s0;
-                            bs = st.base[i] + (s0 - c0);
-                        }
-                    }
-                    const uint32_t keep = __ballot_sync(0xffffffffu, len != 0);
-                    uint32_t v = len;
-#pragma unroll
-                    for (int o = 1; o < kWarp; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
-                        if (lane >= static_cast<uint32_t>(o))
-                            v += t;
-                    }
-                    __syncwarp(); // this batch's reads precede its (lower-index) writes
-                    if (len != 0) {
-                        const uint32_t j = nk + __popc(keep & ((1u << lane) - 1u));
-                        st.base[j] = bs;
-                        st.cum[j] = carry + v - len;
-                    }
-                    carry += __shfl_sync(0xffffffffu, v, kWarp - 1);
-                    nk += __popc(keep);
-                    __syncwarp();
-                }
-                if (lane == 0) {
-                    st.cum[nk] = carry;
-                    *s_total2 = carry;
-                    const uint32_t rest = total > p0 ? total - p0 : 0u;
-                    if (p.skipped && rest != carry)
-                        atomicAdd(p.skipped, static_cast<unsigned long long>(rest - carry));
-                }
-                nchunks = 1 + (carry + kChunkW - 1) / kChunkW;
-                ncum = nk;
-                __syncwarp();
-                mbar_arrive(plan);
-            }
+                *reinterpret_cast<volatile float*>(s_T) = topk.wd;
             __syncwarp();
             mbar_arrive(empty + s);
+            TRIM_TL(if (tl) {
+                cyc_wait += k1 - k0;
+                cyc_busy += clock64() - k1;
+            })
         }
+        TRIM_TL(if (tl && lane == 0) {
+            tl[4] = gtime();
+            tl[5] = nchunks;
+            tl[7] = members;
+            tl[8] = cyc_wait;
+            tl[9] = cyc_busy;
+        })
         uint32_t* io = p.ids_out + static_cast<size_t>(q) * p.k;
         float* dout = p.dist_out + static_cast<size_t>(q) * p.k;
         if (total < p.k) {
@@ -535,9 +555,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         if (lane == 0 && p.counters) {
             unsigned long long* cc = p.counters + static_cast<size_t>(q) * 6;
             const uint64_t evaluated = total;
-            const uint64_t seeds = min(static_cast<uint64_t>(p.k), evaluated);
             cc[0] = dc;                // dc
-            cc[1] = evaluated - seeds; // edc
+            cc[1] = evaluated - nseed; // edc
             cc[2] = evaluated - dc;    // pruned (including skipped lists)
             cc[3] = evaluated;         // evaluated
             cc[4] = 0;                 // hops
@@ -547,27 +566,42 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     }
 
     // ---------------------------------------------------- worker warps
+    TRIM_TL(const bool wtl = tl && tid == kWarp; // worker 0, lane 0 records
+            unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
+            unsigned long long wk = wtl ? clock64() : 0;)
+    build_lut_blocked(ix, qv, lut, tid - kWarp, kThreads - kWarp);
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - kWarp) : "memory"); // workers only
     const uint32_t w = warp - 1;
     LaneAdc la;
     la.init(lane, LutShape::of(m));
+    TRIM_TL(if (wtl) {
+        const unsigned long long t = clock64();
+        wc[0] = t - wk;
+        wk = t;
+    })
+    mbar_wait(plan, 0); // seeds done, compacted stream ready
+    TRIM_TL(if (wtl) {
+        const unsigned long long t = clock64();
+        wc[1] = t - wk;
+        wk = t;
+    })
+    const uint32_t bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
+    const uint32_t nchunks = (bound + kChunkW - 1) / kChunkW;
     uint32_t li = 0; // list cursor (positions of a lane only increase)
-    uint32_t nchunks = nchunks0, bound = total;
     struct Cand {
         FastCode<M> fc;
         float lx;
         uint32_t e;
-        uint32_t kind; // 0: past the end or a seed, 2: candidate
+        uint32_t kind; // 0: past the end, 2: candidate
     };
     struct Slot {
         Cand c[kLaneU];
     };
     Slot sa, sb; // double buffer in registers (static names: no local-memory indexing)
-    // chunk 0: original positions [0, 224) (seeds excluded); chunk c >= 1:
-    // compacted positions (c-1)*224 + ..., the kept stream from p0 = max(224, k)
     auto fetch = [&](uint32_t c, Slot& d) {
 #pragma unroll
         for (uint32_t u = 0; u < kLaneU; ++u) {
-            const uint32_t pp = (c == 0 ? 0u : (c - 1) * kChunkW) + w * kPerWorker + u * kWarp + lane;
+            const uint32_t pp = c * kChunkW + w * kPerWorker + u * kWarp + lane;
             Cand& x = d.c[u];
             x.kind = 0;
             x.e = 0;
@@ -576,35 +610,37 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 while (st.cum[li + 1] <= pp)
                     ++li;
                 x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
-                // the seeds (positions < k) were evaluated by the replay warp
-                x.kind = (c == 0 && pp < p.k) ? 0u : 2u;
-                if (x.kind == 2u) {
-                    x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
-                    x.lx = __ldg(ix.lx + x.e);
-                }
-            }
-            if (x.kind != 2u) // dead lanes still step through the schedule: valid rows
+                x.kind = 2u;
+                x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
+                x.lx = __ldg(ix.lx + x.e);
+            } else { // dead lanes still step through the schedule: valid rows
                 x.fc.zero(m);
+            }
         }
     };
     auto process = [&](uint32_t c, Slot& cur) {
         const uint32_t s = c % kRing;
+        TRIM_TL(const unsigned long long k0 = wtl ? clock64() : 0;)
         if (c >= kRing)
             mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
+        if (c == 1) // filter the rest against the threshold after chunk 0, not the seeds'
+            mbar_wait(empty, 0);
         const float T = ld_volatile(s_T);
+        TRIM_TL(const unsigned long long k1 = wtl ? clock64() : 0;)
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
         Cand& x = cur.c[0];
         const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
         const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
-        // member = seed, or a candidate whose est interval [lo, hi] starts below T
+        // member = a candidate whose est interval [lo, hi] starts below T
         float lo = kNegInf, hi = kNegInf;
         bool keep = false;
         if (x.kind == 2u && a >= 0.0f) {
             lo = est_lower_bound(a, x.lx, p.two_gamma, p.adc_eps);
-            keep = lo < T;
+            keep = lo < ld_volatile(s_T); // the freshest published threshold
             if (keep)
                 hi = est_upper_bound(a, x.lx, p.two_gamma, p.adc_eps);
         }
+        TRIM_TL(const unsigned long long k2 = wtl ? clock64() : 0;)
         uint32_t id = 0;
         float d = 0.0f;
         if (keep) { // exact L2 (ivf.hpp:276) of every member the replay may evaluate
@@ -625,18 +661,14 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             bin_mask[s * kWorkers + w] = bal;
         }
         mbar_arrive(full + s);
+        TRIM_TL(if (wtl) {
+            wc[2] += k1 - k0;
+            wc[3] += k2 - k1;
+            wc[4] += clock64() - k2;
+        })
     };
     fetch(0, sa);
-    mbar_wait(seedbar, 0); // the seeded threshold is published
-    process(0, sa);
-    if (nchunks0 <= 1)
-        return;
-    mbar_wait(plan, 0); // the compacted stream (chunks >= 1)
-    bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
-    nchunks = 1 + (bound + kChunkW - 1) / kChunkW;
-    li = 0;
-    fetch(1, sa);
-    for (uint32_t c = 1; c < nchunks; c += 2) {
+    for (uint32_t c = 0; c < nchunks; c += 2) {
         fetch(c + 1, sb); // prefetch: loads in flight while chunk c is filtered
         process(c, sa);
         if (c + 1 >= nchunks)
@@ -644,6 +676,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         fetch(c + 2, sa);
         process(c + 1, sb);
     }
+    TRIM_TL(if (wtl) {
+        wc[5] = clock64() - wk;
+        for (int i = 0; i < 6; ++i)
+            tl[10 + i] = wc[i];
+    })
 }
 
 // --------------------------------------------------------------------------

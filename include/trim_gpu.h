@@ -117,6 +117,10 @@ int trim_index_get_info(trim_index_t index, trim_index_info* info);
  * (they are counted as pruned in trim_counters, exactly as the reference
  * prunes them one by one). Synchronises the index's device. */
 int trim_index_skip_stats(trim_index_t index, uint64_t* skipped_positions, int reset);
+/* Kernels trim_probe / trim_probe_device launch per call at this nprobe
+ * (2 on the tensor-core path: distance bounds + select; 1 otherwise; 0 when
+ * nlist == 1). For launch accounting. */
+int trim_probe_launches(trim_index_t index, uint32_t nprobe, uint32_t* launches);
 
 /*
  * ivf::search_trim_ivf_knn (ivf/ivf.hpp:243-304), for nq queries.

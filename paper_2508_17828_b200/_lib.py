@@ -57,6 +57,7 @@ SIGNATURES = {
     "trim_index_destroy": (C.c_int, [C.c_void_p]),
     "trim_index_get_info": (C.c_int, [C.c_void_p, C.POINTER(TrimIndexInfo)]),
     "trim_index_skip_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
+    "trim_probe_launches": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "trim_search_knn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
                                   C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
     "trim_search_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,

@@ -270,11 +270,17 @@ bool probe_mma_enabled() {
     return !(e && e[0] == '0');
 }
 
+bool probe_uses_mma(const trim_index* ix, uint32_t np) {
+    const DevIndex& v = ix->dev;
+    return ix->coarse_t && np <= kProbeMaxNp && v.nlist >= 256 &&
+           probe_select_smem(v.nlist, v.dim_stride) <= kSmemLimit && probe_mma_enabled();
+}
+
 void launch_probe(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t np, uint32_t* d_out,
                   cudaStream_t st) {
     const DevIndex& v = ix->dev;
     const size_t ssmem = probe_select_smem(v.nlist, v.dim_stride);
-    if (ix->coarse_t && np <= kProbeMaxNp && v.nlist >= 256 && ssmem <= kSmemLimit && probe_mma_enabled()) {
+    if (probe_uses_mma(ix, np)) {
         const uint32_t K = mma_k(v.dim);
         const uint32_t ntiles = (v.nlist + kMmaN - 1) / kMmaN;
         const size_t ld = mma_ld(v.nlist);
@@ -727,6 +733,14 @@ int trim_index_skip_stats(trim_index_t ix, uint64_t* skipped, int reset) {
         *skipped = v;
         return TRIM_OK;
     });
+}
+
+int trim_probe_launches(trim_index_t ix, uint32_t nprobe, uint32_t* launches) {
+    if (!ix || !launches)
+        return set_err(TRIM_EINVAL, "trim_probe_launches: null argument");
+    const uint32_t np = std::min(nprobe, ix->dev.nlist);
+    *launches = (ix->dev.nlist == 1 || np == 0) ? 0u : (probe_uses_mma(ix, np) ? 2u : 1u);
+    return TRIM_OK;
 }
 
 int trim_search_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t k,

@@ -39,11 +39,20 @@ CONFIGS = {
     "c2": dict(workload="ivfpq_trim_knn_10M_d96_nlist4096_nprobe64", n=10_000_000, dim=96,
                n_centers=1024, sigma=0.3, nq=10_000, batch=1024, m=48, nlist=4096, nprobe=64,
                k=10, gammas=[0.6, 0.8, 1.0], gamma=0.8),
+    # BASELINE.json configs[2]: flat range search, one calibrated radius
+    "c3": dict(kind="range", workload="flat_trim_range_10M_d128", n=10_000_000, dim=128,
+               n_centers=256, sigma=0.3, nq=10_000, batch=1024, m=32, nlist=1, nprobe=1, k=0,
+               gammas=[0.0, 0.8], gamma=0.8, result_size=100),
     # BASELINE.json configs[0] (CPU-runnable reference case; parity + extra line)
     "c1": dict(workload="flat_trim_knn_100k_d128", n=100_000, dim=128, n_centers=64, sigma=0.3,
                nq=1000, batch=1000, m=16, nlist=1, nprobe=1, k=10, gammas=[0.0, 0.605, 1.0],
                gamma=0.0),
 }
+
+
+def metric_name(cfg):
+    what = "range filter, flat" if cfg.get("kind") == "range" else "kNN filter"
+    return f"candidates filtered/sec (TRIM {what}; QPS, %HBM roofline, prune ratio alongside)"
 
 
 def log(*a):
@@ -354,8 +363,7 @@ def run_ours(args, cfg):
     total_cand = evaluated * args.steps
     value = total_cand / (ms / 1e3)
     qps = nq * args.steps / (ms / 1e3)
-    out = dict(metric="candidates filtered/sec (TRIM kNN filter; QPS, %HBM roofline, prune "
-                      "ratio alongside)",
+    out = dict(metric=metric_name(cfg),
                value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic")
@@ -498,12 +506,18 @@ class RefTimer:
 
     def run(self, qsub):
         """-> (seconds, evaluated, dc, pruned) for one parallel batch."""
+        rng = self.cfg.get("kind") == "range"
         if self.kind == "reference":
-            sec, ct = self.ref.session_run(self.sess, 0, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma)
+            sec, ct = self.ref.session_run(self.sess, 1 if rng else 0, qsub, self.cfg["k"], self.cfg["nprobe"],
+                                           self.gamma, arg=self.cfg.get("radius", 0.0))
             return sec, int(ct[3]), int(ct[0]), int(ct[2])
         t0 = time.perf_counter()
-        _, _, ct, _ = self.co.search_knn(self.hix, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma,
-                                         threads=self.threads)
+        if rng:
+            _, _, _, ct, _ = self.co.search_range(self.hix, qsub, self.cfg["radius"], self.cfg["nprobe"],
+                                                  self.gamma, threads=self.threads)
+        else:
+            _, _, ct, _ = self.co.search_knn(self.hix, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma,
+                                             threads=self.threads)
         return time.perf_counter() - t0, int(ct[:, 3].sum()), int(ct[:, 0].sum()), int(ct[:, 2].sum())
 
     def close(self):
@@ -533,6 +547,192 @@ def cpu_baseline(arrays, queries, cfg, gamma, args):
                 qps=n / sec, prune_ratio=pr / max(1, pr + dc))
 
 
+# ------------------------------------------------------ config 3: range
+def calibrate_radius(arrays, queries, cfg):
+    """bench::pick_radius_for_fraction (bench/radius.hpp:20-55): the
+    e_fraction = result_size/N quantile (EmpiricalCdf: linear between order
+    statistics) of pooled query-to-row distances over 20,000 sampled rows x 200
+    sampled queries (the reference's Fisher-Yates sampler, seeds 1 and 2).
+    Distances by torch.cdist (a workload parameter, not a parity value)."""
+    import torch
+
+    from paper_2508_17828_b200 import builder as B
+    x = arrays.vectors
+    rows = torch.from_numpy(B.sample_rows(x.shape[0], min(20000, x.shape[0]), 1).astype(np.int64)).to(x.device)
+    qi = torch.from_numpy(B.sample_rows(queries.shape[0], min(200, queries.shape[0]), 2).astype(np.int64)).to(x.device)
+    d = torch.cdist(queries[qi].double(), x[rows].double()).reshape(-1)
+    d, _ = torch.sort(d)
+    p = cfg["result_size"] / x.shape[0]
+    pos = p * (d.numel() - 1)
+    lo = int(pos)
+    if lo + 1 >= d.numel():
+        return float(d[-1])
+    return float(d[lo] + (pos - lo) * (d[lo + 1] - d[lo]))
+
+
+def run_ours_range(args, cfg):
+    import ctypes as C
+
+    import torch
+
+    from paper_2508_17828_b200 import _lib
+    from paper_2508_17828_b200 import ivf as G
+
+    world, rank, local = dist_env()
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    arrays, queries = build_workload(cfg, rank, world, local, False)
+    gix = G.GpuIvfIndex(arrays, device=local)
+    lib = _lib.load()
+    radius = calibrate_radius(arrays, queries, cfg)
+    cfg["radius"] = radius
+    nq, B, cap = cfg["nq"], cfg["batch"], 4096
+    d_rad = torch.full((nq,), radius, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(max(1, args.streams) - 1)]
+    shs = [C.c_void_p(x.cuda_stream) for x in streams]
+    counts = torch.zeros(nq, dtype=torch.int32, device=dev)
+    ids = torch.empty((nq, cap), dtype=torch.int32, device=dev)
+    dist = torch.empty((nq, cap), dtype=torch.float32, device=dev)
+    cts = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    batches = [(b, min(B, nq - b)) for b in range(0, nq, B)]
+    P = lambda t, off=0: C.c_void_p(t.data_ptr() + off)
+
+    def step(gamma, ev=None):
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for x in streams[1:]:
+            x.wait_event(fork)
+        for i, (b0, nb) in enumerate(batches):
+            st_, sh_ = streams[i % len(streams)], shs[i % len(streams)]
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(st_)
+            _lib.check(lib.trim_search_range_device(
+                gix.handle, P(queries, b0 * cfg["dim"] * 4), nb, P(d_rad, b0 * 4), cfg["nprobe"],
+                float(np.float32(gamma)), cap, P(counts, b0 * 4), P(ids, b0 * cap * 4), P(dist, b0 * cap * 4),
+                P(cts, b0 * 48), P(status), sh_), "range")
+            if ev is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(st_)
+                ev.append((e0, e1))
+        for x in streams[1:]:
+            j = torch.cuda.Event()
+            j.record(x)
+            stream.wait_event(j)
+        return len(batches) * 6  # r2, range, seg, cub (2 kernels), finish
+
+    def timed(gamma, steps, warmup, clocks=None):
+        for _ in range(warmup):
+            step(gamma)
+        torch.cuda.synchronize()
+        ev = []
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        launches = 0
+        with (clocks if clocks is not None else _Null()):
+            s0.record(stream)
+            for _ in range(steps):
+                launches += step(gamma, ev)
+            s1.record(stream)
+            torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1)
+        iv = sorted((s0.elapsed_time(a), s0.elapsed_time(b)) for a, b in ev)
+        busy, cur = 0.0, None
+        for a, b in iv:
+            if cur is None or a > cur[1]:
+                if cur is not None:
+                    busy += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        if cur is not None:
+            busy += cur[1] - cur[0]
+        return ms, busy, len(ev), cts.sum(0).cpu().numpy(), launches
+
+    head = args.gamma if args.gamma is not None else cfg["gamma"]
+    # size the per-query result slots: the largest result set over the gammas run
+    gams = [head] if args.gamma is not None else cfg["gammas"]
+    mx = 0
+    for g in set(gams) | {head}:
+        status.zero_()
+        step(g)
+        torch.cuda.synchronize()
+        mx = max(mx, int(counts.max()))
+    if mx > cap:
+        cap = (mx * 5 // 4 + 127) // 128 * 128
+        ids = torch.empty((nq, cap), dtype=torch.int32, device=dev)
+        dist = torch.empty((nq, cap), dtype=torch.float32, device=dev)
+    status.zero_()
+    sweep = {}
+    for g in gams:
+        if g == head:
+            continue
+        ms, _, _, ct, _ = timed(g, 1, 1)
+        sweep[str(g)] = dict(ms_per_step=ms, cand_per_s=float(ct[3]) / (ms / 1e3), qps=nq / (ms / 1e3),
+                             prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])),
+                             mean_result_size=float(counts.double().mean()))
+    clk = ClockSampler(local)
+    ms, busy, nl, ct, launches = timed(head, args.steps, args.warmup, clk)
+    assert int(status.item()) & 1 == 0, "range result larger than cap"
+    evaluated, dc = float(ct[3]), float(ct[0])
+    value = evaluated * args.steps / (ms / 1e3)
+    out = dict(metric=metric_name(cfg),
+               value=value, unit="candidates/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+               ms_per_step=ms / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+               dtype="f32 (u8 PQ codes)", data="synthetic")
+    out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"], queries=nq, batch=B,
+                         m=cfg["m"], nlist=1, gamma=head, radius=radius,
+                         radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)",
+                         parallelism="single", l2="index > L2 (no flush needed)",
+                         data_gen="device Philox blobs, seeds centers=0 base=1 queries=2")
+    out["qps"] = nq * args.steps / (ms / 1e3)
+    out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
+    out["mean_result_size"] = float(counts.double().mean())
+    qt = gix.info()["range_query_tile"]
+    peak, peak_src = measured_peaks()
+    m, D = cfg["m"], cfg["dim"]
+    # the flat scan streams codes + lx once per query tile; survivors read their row
+    alg = (nq + qt - 1) // qt * cfg["n"] * (m + 4) + dc * (4 * D + 4)
+    achieved = alg / (busy / args.steps / 1e3) / 1e9
+    out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                           traffic=ncu_traffic(cfg["workload"]), kernel="trim_range_flat_kernel",
+                           bytes_per_step=alg, query_tile=qt, peak_source=peak_src,
+                           pair_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4)) / (busy / args.steps / 1e3) / 1e9)
+    out["gpu_launches"] = launches
+    out["clocks"] = clk.summary()
+    out["sweep"] = sweep
+    # e2e: the host C-ABI call per batch from two client threads
+    hq = queries.cpu().pin_memory().numpy()
+    prof = G.PruningProfile.manual(head)
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max(1, args.streams))
+
+    def one(b):
+        offs, _, _, c = G.search_trim_ivf_range_batch(gix, prof, hq[b:b + B], radius, 1)
+        return int(c[:, 3].sum()), int(offs[-1])
+
+    def once():
+        r = list(pool.map(one, range(0, nq, B)))
+        return sum(x[0] for x in r), sum(x[1] for x in r)
+    once()
+    t0 = time.perf_counter()
+    reps = max(1, min(args.steps, 2))
+    tot = 0
+    for _ in range(reps):
+        c, nres = once()
+        tot += c
+    sec = time.perf_counter() - t0
+    out["e2e"] = dict(value=tot / sec, unit="candidates/s", qps=nq * reps / sec,
+                      h2d_bytes_per_step=nq * D * 4 + nq * 4,
+                      d2h_bytes_per_step=nres * 8 + (nq + 1) * 8 + nq * 48,
+                      api=f"trim_search_range (C ABI, host buffers; {max(1, args.streams)} client threads)")
+    if rank == 0 and not args.skip_cpu:
+        out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
+    print(json.dumps(out), flush=True)
+
+
 # ------------------------------------------------------ reference CPU arm
 def run_reference(args, cfg):
     world, rank, local = dist_env()
@@ -543,10 +743,12 @@ def run_reference(args, cfg):
     arrays, queries = build_workload(cfg, 0, 1, local)
     hix = _host_index(arrays)
     qs = queries.cpu().numpy()
-    del arrays
-    torch.cuda.empty_cache()
+    arrays_r = arrays
     threads = os.cpu_count() or 1
     head = args.gamma if args.gamma else cfg["gamma"]
+    if cfg.get("kind") == "range":
+        import torch as _t
+        cfg["radius"] = calibrate_radius(arrays_r, queries, cfg)
     rt = RefTimer(hix, cfg, head, threads)
     qps = rt.calibrate(qs)
     per_step_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
@@ -563,8 +765,7 @@ def run_reference(args, cfg):
             evs += ev
     rt.close()
     value = evs / secs
-    out = dict(metric="candidates filtered/sec (TRIM kNN filter; QPS, %HBM roofline, prune "
-                      "ratio alongside)",
+    out = dict(metric=metric_name(cfg),
                value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=secs * 1e3 / args.steps, higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic",
@@ -608,6 +809,8 @@ def main():
         log("note: the contract asks for >= 3 warm-up steps")
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("kind") == "range":
+        run_ours_range(args, cfg)
     else:
         run_ours(args, cfg)
 

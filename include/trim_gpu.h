@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define TRIM_ABI_VERSION 1
+#define TRIM_ABI_VERSION 2
 
 typedef enum {
     TRIM_OK = 0,
@@ -102,6 +102,7 @@ typedef struct {
     uint64_t max_list_size;
     uint64_t device_bytes;
     int device;
+    uint32_t range_query_tile; /* queries sharing one code stream in the flat range scan */
 } trim_index_info;
 
 const char* trim_last_error(void);
@@ -175,6 +176,19 @@ int trim_search_knn_preassigned_device(trim_index_t index, const float* d_querie
                                        float gamma, uint32_t* d_ids, float* d_dist,
                                        trim_counters* d_counters, uint32_t* d_status,
                                        void* stream);
+
+/* ivf::search_trim_ivf_range (ivf/ivf.hpp:308-347), device-resident. d_queries
+ * nq*dim, d_radius nq (device). Query i's members, sorted by (dist_sq, id) like
+ * ivf.hpp:341, are d_ids/d_dist[i*cap .. i*cap + min(count, cap)); d_counts[i]
+ * = the true member count. Bit 0 of *d_status: some query had more than cap
+ * members (its slots then hold an arbitrary sorted subset of cap of them: call
+ * again with cap >= max count); bit 1: some
+ * radius was negative (the host API's TRIM_EINVAL; that query returns nothing).
+ * dim must be a multiple of 4. */
+int trim_search_range_device(trim_index_t index, const float* d_queries, uint64_t nq,
+                             const float* d_radius, uint32_t nprobe, float gamma, uint32_t cap,
+                             uint32_t* d_counts, uint32_t* d_ids, float* d_dist,
+                             trim_counters* d_counters, uint32_t* d_status, void* stream);
 
 /* pq::build_distance_table (pq/pq.hpp:158-172) for nq queries: lut_out is
  * nq*m*ksub floats (host), j-major like DistanceTable::entries. */

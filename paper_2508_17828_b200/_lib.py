@@ -46,7 +46,7 @@ class TrimIndexInfo(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("m", C.c_uint32), ("ksub", C.c_uint32),
                 ("nlist", C.c_uint32), ("n", C.c_uint64), ("total_entries", C.c_uint64),
                 ("id_base", C.c_uint64), ("max_list_size", C.c_uint64),
-                ("device_bytes", C.c_uint64), ("device", C.c_int)]
+                ("device_bytes", C.c_uint64), ("device", C.c_int), ("range_query_tile", C.c_uint32)]
 
 
 # name -> (restype, argtypes); must cover every function include/trim_gpu.h declares
@@ -71,6 +71,9 @@ SIGNATURES = {
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "trim_probe_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
                                     C.c_void_p]),
+    "trim_search_range_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
+                                            C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p]),
     "trim_search_knn_preassigned_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                                      C.c_void_p, C.c_uint32, C.c_float, C.c_void_p,
                                                      C.c_void_p, C.c_void_p, C.c_void_p,

@@ -319,29 +319,44 @@ struct FastCode {
         }
     }
 
+    // Apply the lane's word permutation to every block once (for callers that
+    // run several LUTs over the same code: sum_staged<false>).
+    __device__ __forceinline__ void permute_all(uint32_t m, const LaneAdc& la) {
+        const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
+#pragma unroll
+        for (uint32_t b = 0; b < kMaxB; ++b) {
+            if (b < sh.nfull)
+                permute_block<false>(w[b], la.l);
+            else if (b == sh.nfull && sh.half)
+                permute_block<true>(w[b], la.l);
+        }
+    }
+
     // One FULL block B (compile-time), two 16-step stages. Returns true when
-    // the whole warp is provably pruned.
-    template <uint32_t B>
+    // the whole warp is provably pruned. lofs: byte offset of the LUT used.
+    template <uint32_t B, bool PERM>
     __device__ __forceinline__ bool full_block(const LutShape& sh, const LaneAdc& la, const StageCheck& ck,
-                                               float part[4], bool& live) {
+                                               float part[4], bool& live, uint32_t lofs) {
         if (B >= sh.nfull)
             return false;
-        permute_block<false>(w[B], la.l);
+        if (PERM)
+            permute_block<false>(w[B], la.l);
+        const uint32_t lb = la.lf + lofs;
         if (B == 0) { // an extra early stage after 8 lookups: ~2/3 of config-2 warps stop here
-            block_fast<0, 8, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+            block_fast<0, 8, 128u, B * kFullBytes>(lb, w[B], la, part);
             if (live && ck.pruned(sum4(part)))
                 live = false;
             if (!__any_sync(0xffffffffu, live))
                 return true;
-            block_fast<8, 16, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+            block_fast<8, 16, 128u, B * kFullBytes>(lb, w[B], la, part);
         } else {
-            block_fast<0, 16, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+            block_fast<0, 16, 128u, B * kFullBytes>(lb, w[B], la, part);
         }
         if (live && ck.pruned(sum4(part)))
             live = false;
         if (!__any_sync(0xffffffffu, live))
             return true;
-        block_fast<16, 32, 128u, B * kFullBytes>(la.lf, w[B], la, part);
+        block_fast<16, 32, 128u, B * kFullBytes>(lb, w[B], la, part);
         if (B + 1 == sh.nfull && !sh.half)
             return false; // last block: the caller's full check decides
         if (live && ck.pruned(sum4(part)))
@@ -352,19 +367,20 @@ struct FastCode {
     // Full any-order sum, or a negative value if a stage proved est >= T for
     // this lane. `alive` = this lane has a candidate; dead lanes still step
     // along (their lookups keep the schedule conflict-free) but never vote.
-    // Warp-collective.
+    // Warp-collective. PERM = false: the words were permuted by permute_all.
+    template <bool PERM = true>
     __device__ __forceinline__ float sum_staged(uint32_t m, const LaneAdc& la, const StageCheck& ck,
-                                                bool alive) {
+                                                bool alive, uint32_t lofs = 0) {
         const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
         float part[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         bool live = alive;
-        if (full_block<0>(sh, la, ck, part, live))
+        if (full_block<0, PERM>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 1 && full_block<(kMaxB > 1 ? 1u : 0u)>(sh, la, ck, part, live))
+        if (kMaxB > 1 && full_block<(kMaxB > 1 ? 1u : 0u), PERM>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 2 && full_block<(kMaxB > 2 ? 2u : 0u)>(sh, la, ck, part, live))
+        if (kMaxB > 2 && full_block<(kMaxB > 2 ? 2u : 0u), PERM>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 3 && full_block<(kMaxB > 3 ? 3u : 0u)>(sh, la, ck, part, live))
+        if (kMaxB > 3 && full_block<(kMaxB > 3 ? 3u : 0u), PERM>(sh, la, ck, part, live, lofs))
             return -1.0f;
         if (sh.half) {
             const uint32_t hb = sh.nfull;
@@ -373,16 +389,18 @@ struct FastCode {
             for (uint32_t b = 1; b < kMaxB; ++b)
                 if (b == hb)
                     wh = w[b];
-            permute_block<true>(wh, la.l);
+            if (PERM)
+                permute_block<true>(wh, la.l);
+            const uint32_t hl = la.lh + lofs;
             if (sh.hdup) { // the only block (m <= 16): one early check after 8 steps
-                block_fast<0, 8, 128u, 0u>(la.lh, wh, la, part);
+                block_fast<0, 8, 128u, 0u>(hl, wh, la, part);
                 if (live && ck.pruned(sum4(part)))
                     live = false;
                 if (!__any_sync(0xffffffffu, live))
                     return -1.0f;
-                block_fast<8, 16, 128u, 0u>(la.lh, wh, la, part);
+                block_fast<8, 16, 128u, 0u>(hl, wh, la, part);
             } else {
-                block_fast<0, 16, 64u, 0u>(la.lh, wh, la, part);
+                block_fast<0, 16, 64u, 0u>(hl, wh, la, part);
             }
         }
         return live ? sum4(part) : -1.0f;
@@ -537,10 +555,10 @@ __device__ __forceinline__ float est_upper_bound(float a, float glx, float two_g
 // sequential fp32 sum in the reference order j = 0..m-1. For the rare
 // candidates whose est interval straddles the live threshold.
 template <int M>
-__device__ __forceinline__ float adc_serial(const uint8_t* __restrict__ code, uint32_t m) {
+__device__ __forceinline__ float adc_serial(const uint8_t* __restrict__ code, uint32_t m, uint32_t lofs = 0) {
     const uint32_t mm = M > 0 ? static_cast<uint32_t>(M) : m;
     const LutShape sh = LutShape::of(mm);
-    const uint32_t base = lut_saddr();
+    const uint32_t base = lut_saddr() + lofs;
     const uint32_t hbase = base + sh.nfull * kFullBytes, hrow = sh.half_row_bytes();
     float acc = 0.0f;
     for (uint32_t j = 0; j < mm; ++j) {

@@ -208,6 +208,11 @@ void launch_range(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t sm
     TRIM_DISPATCH(launch_range_, ix, p, grid, smem, st);
 }
 
+void launch_range_flat(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem, uint32_t qt,
+                       cudaStream_t st) {
+    TRIM_DISPATCH(launch_range_flat_, ix, p, grid, smem, qt, st);
+}
+
 void launch_bl_est(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,
                    cudaStream_t st) {
     TRIM_DISPATCH(launch_bl_est_, ix, p, grid, smem, st);
@@ -265,6 +270,12 @@ int dispatch_m(const DevIndex& ix) {
 // probe_order for a batch into d_out (nq*np): the tiled kernel when np and the
 // distance table fit its shared-memory plan, else the one-query bitonic kernel.
 // TRIM_PROBE_MMA=0 forces the SIMT probe kernels (A/B and parity tests).
+// TRIM_RANGE_TILED=0 forces the one-query range kernel for flat indexes.
+bool probe_mma_enabled_range() {
+    const char* e = std::getenv("TRIM_RANGE_TILED");
+    return !(e && e[0] == '0');
+}
+
 bool probe_mma_enabled() {
     const char* e = std::getenv("TRIM_PROBE_MMA");
     return !(e && e[0] == '0');
@@ -346,6 +357,69 @@ DevBuf upload_queries(const trim_index* ix, const float* q, uint64_t nq, cudaMem
         CK(cudaMemcpyAsync(d.p, q, sizeof(float) * nq * dim, kind, st));
     }
     return d;
+}
+
+// Query-tile size of the flat range kernel: as many LUTs as fit while two
+// CTAs stay resident per SM (1 = no tiling).
+uint32_t range_flat_qt(const DevIndex& v) {
+    if (v.nlist != 1 || !probe_mma_enabled_range())
+        return 1;
+    const int mt = dispatch_m(v);
+    uint32_t qt = kFlatMaxQ; // one 16-warp CTA per SM
+    while (qt > 1 && range_flat_smem(mt, v.m, v.dim_stride, qt) > kSmemLimit)
+        --qt;
+    return qt;
+}
+
+// ivf::search_trim_ivf_range's filter for nb padded device queries: members
+// as (d, id) keys into per-query pools of `cap`, counts, dc and evaluated.
+void range_launch(const trim_index* ix, const float* d_q, uint64_t nq, const float* d_r2, uint32_t np,
+                  const uint32_t* d_probe, float gamma, uint32_t cap, unsigned long long* d_keys,
+                  unsigned int* d_cnt, unsigned long long* d_dc, unsigned long long* d_eval, cudaStream_t st) {
+    const DevIndex& v = ix->dev;
+    RangeParams p{};
+    p.np = np;
+    p.two_gamma = 2.0f * gamma;
+    p.adc_eps = filter_eps(v.m);
+    p.omg_hi = omg_round_up(gamma);
+    p.cap = cap;
+    const uint64_t bound = ix->stream_bound(np);
+    const uint32_t qt = d_probe ? 1u : range_flat_qt(v);
+    if (qt > 1) { // flat scan, query-tiled; at most 65535 slices (grid.y)
+        uint64_t slice = 64 * kFlatThreads;
+        if ((bound + slice - 1) / slice > 65535)
+            slice = ((bound + 65534) / 65535 + kFlatThreads - 1) / kFlatThreads * kFlatThreads;
+        const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);
+        p.slice = static_cast<uint32_t>(slice);
+        p.queries = d_q;
+        p.nq = nq;
+        p.radius_sq = d_r2;
+        p.probe = nullptr;
+        p.keys = d_keys;
+        p.count = d_cnt;
+        p.dc = d_dc;
+        p.evaluated = d_eval;
+        const uint64_t tiles = (nq + qt - 1) / qt;
+        launch_range_flat(v, p, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(nslices)),
+                          range_flat_smem(dispatch_m(v), v.m, v.dim_stride, qt), qt, st);
+        return;
+    }
+    const size_t smem = range_smem_bytes(dispatch_m(v), v.m, v.dim_stride, np);
+    const uint32_t slice = 32 * kRangeChunk;
+    const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);
+    p.slice = slice;
+    for (uint64_t b = 0; b < nq; b += 65535) {
+        const uint64_t nb = std::min<uint64_t>(65535, nq - b);
+        p.queries = d_q + b * v.dim_stride;
+        p.nq = nb;
+        p.radius_sq = d_r2 + b;
+        p.probe = d_probe ? d_probe + b * np : nullptr;
+        p.keys = d_keys + b * cap;
+        p.count = d_cnt + b;
+        p.dc = d_dc + b;
+        p.evaluated = d_eval + b;
+        launch_range(v, p, dim3(static_cast<unsigned>(nslices), static_cast<unsigned>(nb)), smem, st);
+    }
 }
 
 int validate_knn(uint32_t k, float gamma) {
@@ -717,6 +791,7 @@ int trim_index_get_info(trim_index_t ix, trim_index_info* info) {
     info->max_list_size = ix->max_list;
     info->device_bytes = ix->bytes;
     info->device = ix->device;
+    info->range_query_tile = range_flat_qt(ix->dev);
     return TRIM_OK;
 }
 
@@ -875,9 +950,6 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
         if (smem > kSmemLimit)
             return set_err(TRIM_EINVAL,
                            "search_trim_ivf_range: per-query state (%zu B) exceeds 227 KB", smem);
-        const uint64_t bound = ix->stream_bound(np);
-        const uint32_t slice = 32 * kRangeChunk;
-        const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);
         DevBuf d_cnt(sizeof(unsigned int) * nq, st), d_dc(sizeof(unsigned long long) * nq, st),
             d_eval(sizeof(unsigned long long) * nq, st);
         uint32_t cap = 1024;
@@ -888,26 +960,9 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
             CK(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned int) * nq, st));
             CK(cudaMemsetAsync(d_dc.p, 0, sizeof(unsigned long long) * nq, st));
             CK(cudaMemsetAsync(d_eval.p, 0, sizeof(unsigned long long) * nq, st));
-            RangeParams p{};
-            p.np = np;
-            p.two_gamma = 2.0f * gamma;
-            p.adc_eps = filter_eps(ix->dev.m);
-            p.omg_hi = omg_round_up(gamma);
-            p.slice = slice;
-            p.cap = cap;
-            for (uint64_t b = 0; b < nq; b += 65535) {
-                const uint64_t nb = std::min<uint64_t>(65535, nq - b);
-                p.queries = d_q.as<float>() + b * ix->dev.dim_stride;
-                p.nq = nb;
-                p.radius_sq = d_r2.as<float>() + b;
-                p.probe = d_probe.p ? d_probe.as<uint32_t>() + b * np : nullptr;
-                p.keys = d_keys.as<unsigned long long>() + b * cap;
-                p.count = d_cnt.as<unsigned int>() + b;
-                p.dc = d_dc.as<unsigned long long>() + b;
-                p.evaluated = d_eval.as<unsigned long long>() + b;
-                launch_range(ix->dev, p, dim3(static_cast<unsigned>(nslices), static_cast<unsigned>(nb)),
-                             smem, st);
-            }
+            range_launch(ix, d_q.as<float>(), nq, d_r2.as<float>(), np, d_probe.p ? d_probe.as<uint32_t>() : nullptr,
+                         gamma, cap, d_keys.as<unsigned long long>(), d_cnt.as<unsigned int>(),
+                         d_dc.as<unsigned long long>(), d_eval.as<unsigned long long>(), st);
             CK(cudaMemcpyAsync(cnt.data(), d_cnt.p, sizeof(unsigned int) * nq,
                                cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -981,6 +1036,62 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
         }
         *ids_out = hid;
         *dist_out = hd;
+        return TRIM_OK;
+    });
+}
+
+int trim_search_range_device(trim_index_t ix, const float* d_queries, uint64_t nq, const float* d_radius,
+                             uint32_t nprobe, float gamma, uint32_t cap, uint32_t* d_counts, uint32_t* d_ids,
+                             float* d_dist, trim_counters* d_counters, uint32_t* d_status, void* stream) {
+    if (!ix || (nq && (!d_queries || !d_radius || !d_counts || !d_ids || !d_dist)))
+        return set_err(TRIM_EINVAL, "search_trim_ivf_range: null argument");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_ivf_range: uncalibrated pruning profile");
+    if (cap == 0)
+        return set_err(TRIM_EINVAL, "trim_search_range_device: cap must be positive");
+    if (ix->dev.dim_stride != ix->dev.dim)
+        return set_err(TRIM_EINVAL, "trim_search_range_device: dim must be a multiple of 4");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const unsigned g1 = static_cast<unsigned>((nq + 255) / 256);
+        DevBuf d_r2(sizeof(float) * nq, st);
+        trim_range_r2_kernel<<<g1, 256, 0, st>>>(d_radius, nq, d_r2.as<float>(), d_status);
+        CK(cudaGetLastError());
+        DevBuf d_probe;
+        const uint32_t np = run_probe(ix, d_queries, nq, nprobe, d_probe, st);
+        if (np == 0)
+            return set_err(TRIM_EINVAL, "search_trim_ivf_range: nprobe must be positive");
+        DevBuf d_cnt(sizeof(unsigned int) * nq, st), d_dc(sizeof(unsigned long long) * nq, st),
+            d_eval(sizeof(unsigned long long) * nq, st), d_keys(sizeof(unsigned long long) * nq * cap, st);
+        CK(cudaMemsetAsync(d_cnt.p, 0, sizeof(unsigned int) * nq, st));
+        CK(cudaMemsetAsync(d_dc.p, 0, sizeof(unsigned long long) * nq, st));
+        CK(cudaMemsetAsync(d_eval.p, 0, sizeof(unsigned long long) * nq, st));
+        range_launch(ix, d_queries, nq, d_r2.as<float>(), np, d_probe.p ? d_probe.as<uint32_t>() : nullptr, gamma,
+                     cap, d_keys.as<unsigned long long>(), d_cnt.as<unsigned int>(), d_dc.as<unsigned long long>(),
+                     d_eval.as<unsigned long long>(), st);
+        DevBuf d_beg(sizeof(uint64_t) * nq, st), d_end(sizeof(uint64_t) * nq, st),
+            d_sorted(sizeof(unsigned long long) * nq * cap, st);
+        trim_range_seg_kernel<<<g1, 256, 0, st>>>(d_cnt.as<unsigned int>(), nq, cap, d_beg.as<uint64_t>(),
+                                                  d_end.as<uint64_t>(), d_status);
+        CK(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, d_keys.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(),
+                                              static_cast<int64_t>(nq * cap), static_cast<int64_t>(nq),
+                                              d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        DevBuf d_tmp(tmp_bytes, st);
+        CK(cub::DeviceSegmentedSort::SortKeys(d_tmp.p, tmp_bytes, d_keys.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(),
+                                              static_cast<int64_t>(nq * cap), static_cast<int64_t>(nq),
+                                              d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        trim_range_finish_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(
+            d_sorted.as<unsigned long long>(), d_cnt.as<unsigned int>(), d_dc.as<unsigned long long>(),
+            d_eval.as<unsigned long long>(), nq, cap, ix->dev.nlist, d_counts, d_ids, d_dist,
+            reinterpret_cast<unsigned long long*>(d_counters));
+        CK(cudaGetLastError());
         return TRIM_OK;
     });
 }

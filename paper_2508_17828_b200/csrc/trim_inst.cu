@@ -19,13 +19,17 @@ namespace trimgpu {
 
 namespace {
 template <typename K, typename... A>
-cudaError_t launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+cudaError_t launch_t(K kern, dim3 grid, uint32_t threads, size_t smem, cudaStream_t st, A... args) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess)
         return e;
-    kern<<<grid, kThreads, smem, st>>>(args...);
+    kern<<<grid, threads, smem, st>>>(args...);
     return cudaGetLastError();
+}
+template <typename K, typename... A>
+cudaError_t launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+    return launch_t(kern, grid, kThreads, smem, st, args...);
 }
 } // namespace
 
@@ -45,6 +49,11 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
 cudaError_t TRIM_CAT(launch_range_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,
                                             size_t smem, cudaStream_t st) {
     return launch(trim_range_kernel<TRIM_M, TRIM_KS>, grid, smem, st, ix, p);
+}
+
+cudaError_t TRIM_CAT(launch_range_flat_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,
+                                                 size_t smem, uint32_t qt, cudaStream_t st) {
+    return launch_t(trim_range_flat_kernel<TRIM_M, TRIM_KS>, grid, kFlatThreads, smem, st, ix, p, qt);
 }
 
 cudaError_t TRIM_CAT(launch_bl_est_, TRIM_M)(const DevIndex& ix, const BlParams& p, dim3 grid,

@@ -835,6 +835,124 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
         atomicAdd(p.dc + q, static_cast<unsigned long long>(dc_local));
 }
 
+// --------------------------------------------------------------------------
+// trim_range_flat_kernel — the flat scan (nlist = 1: every query's stream is
+// the whole single list, ivf.hpp:318-320) with query tiling: a CTA holds the
+// LUTs of up to kFlatMaxQ queries and evaluates each code it streams against
+// all of them, so the codes are read from HBM once per query tile instead of
+// once per query. Per (candidate, query) the decisions are trim_range_kernel's.
+// grid (ceil(nq / qt), slices): consecutive CTAs are different query tiles
+// over the same slice, so a slice's codes are read from HBM about once per
+// wave of resident CTAs and served from L2 to the rest.
+// --------------------------------------------------------------------------
+constexpr uint32_t kFlatMaxQ = 8;
+constexpr uint32_t kFlatThreads = 512; // 16 warps: one CTA per SM holds up to 6 LUTs of 32 KB
+
+__host__ __device__ inline size_t range_flat_smem(int mt, uint32_t m, uint32_t dim_stride, uint32_t qt) {
+    size_t b = lut_bytes(mt, m) * qt;            // LUTs (multiples of 128 B) at offset 0
+    b += sizeof(float) * dim_stride * qt;        // query rows
+    b += sizeof(uint32_t) * (2 * kFlatMaxQ);     // r^2, dc per query
+    return b;
+}
+
+template <int M, int KS>
+__global__ void __launch_bounds__(kFlatThreads)
+trim_range_flat_kernel(DevIndex ix, RangeParams p, uint32_t qt) {
+    unsigned char* smem = trim_dyn_smem;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m;
+    const uint64_t q0 = static_cast<uint64_t>(blockIdx.x) * qt;
+    const uint32_t nqt = static_cast<uint32_t>(min(static_cast<uint64_t>(qt), p.nq - q0));
+    const uint32_t lutb = static_cast<uint32_t>(lut_bytes(M, m));
+    float* qvs = reinterpret_cast<float*>(smem + static_cast<size_t>(lutb) * qt);
+    float* s_r2 = qvs + ix.dim_stride * qt;
+    uint32_t* s_dc = reinterpret_cast<uint32_t*>(s_r2 + kFlatMaxQ);
+
+    for (uint32_t i = tid; i < ix.dim_stride * qt; i += kFlatThreads) {
+        const uint32_t t = i / ix.dim_stride;
+        qvs[i] = t < nqt ? p.queries[(q0 + t) * ix.dim_stride + i % ix.dim_stride] : 0.0f;
+    }
+    if (tid < kFlatMaxQ) {
+        s_r2[tid] = tid < nqt ? p.radius_sq[q0 + tid] : -1.0f;
+        s_dc[tid] = 0;
+    }
+    const uint64_t lbeg = ix.list_offsets[0];
+    const uint32_t total = static_cast<uint32_t>(ix.list_offsets[1] - lbeg);
+    if (blockIdx.y == 0 && tid < nqt)
+        p.evaluated[q0 + tid] = total;
+    const uint32_t begin = blockIdx.y * p.slice;
+    if (begin >= total)
+        return;
+    const uint32_t end = min(total, begin + p.slice);
+    __syncthreads();
+    for (uint32_t t = 0; t < nqt; ++t)
+        build_lut_blocked(ix, qvs + t * ix.dim_stride, reinterpret_cast<float*>(smem + static_cast<size_t>(t) * lutb));
+    __syncthreads();
+    LaneAdc la;
+    la.init(lane, LutShape::of(m));
+
+    FastCode<M> fa, fb;
+    float xa = 0.0f, xb = 0.0f;
+    auto fetch = [&](uint32_t pos, FastCode<M>& fc, float& glx) {
+        const uint32_t pp = pos + tid;
+        if (pp < end) {
+            const uint64_t e = lbeg + pp;
+            fc.load(ix.codes + e * ix.code_stride, m, lane);
+            glx = __ldg(ix.lx + e);
+        } else {
+            fc.zero(m);
+            glx = 0.0f;
+        }
+    };
+    // No block barriers in the scan: a member (rare) is evaluated by its own lane
+    // at once — exact L2 (ivf.hpp:332), then kept iff d <= r^2 (ivf.hpp:334).
+    auto step = [&](uint32_t pos, FastCode<M>& fc, float glx) {
+        const bool valid = pos + tid < end;
+        const uint64_t e = lbeg + pos + tid;
+        fc.permute_all(m, la);
+#pragma unroll 1
+        for (uint32_t t = 0; t < nqt; ++t) {
+            const float r2 = s_r2[t];
+            const float r2x = __int_as_float(__float_as_int(r2) + 1); // smallest float > r^2
+            const StageCheck ck{glx, p.two_gamma, p.omg_hi, p.adc_eps, r2x};
+            const float a = fc.template sum_staged<false>(m, la, ck, valid, t * lutb); // warp-collective
+            // evaluate iff est <= r^2 (ivf.hpp:331): the interval decides, or the
+            // reference-order ADC when it straddles r^2
+            if (valid && a >= 0.0f && est_lower_bound(a, glx, p.two_gamma, p.adc_eps) <= r2) {
+                bool ev = est_upper_bound(a, glx, p.two_gamma, p.adc_eps) <= r2;
+                if (!ev) {
+                    const float ax = adc_serial<M>(ix.codes + e * ix.code_stride, m, t * lutb);
+                    ev = relaxed_lb(__fsqrt_rn(ax), glx, p.two_gamma) <= r2;
+                }
+                if (ev) {
+                    atomicAdd(s_dc + t, 1u);
+                    const uint32_t id = __ldg(ix.list_ids + e);
+                    const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
+                    const float d = euclid_sq_vec4(qvs + t * ix.dim_stride, row, ix.dim);
+                    if (d <= r2) {
+                        const uint64_t q = q0 + t;
+                        const uint32_t slot = atomicAdd(p.count + q, 1u);
+                        if (slot < p.cap)
+                            p.keys[q * p.cap + slot] = scored_key(d, id);
+                    }
+                }
+            }
+        }
+    };
+    fetch(begin, fa, xa);
+    for (uint32_t pos = begin; pos < end; pos += 2 * kFlatThreads) {
+        fetch(pos + kFlatThreads, fb, xb); // next step's codes in flight
+        step(pos, fa, xa);
+        if (pos + kFlatThreads >= end)
+            break;
+        fetch(pos + 2 * kFlatThreads, fa, xa);
+        step(pos + kFlatThreads, fb, xb);
+    }
+    __syncthreads();
+    if (tid < nqt && s_dc[tid])
+        atomicAdd(p.dc + q0 + tid, static_cast<unsigned long long>(s_dc[tid]));
+}
+
 #ifndef TRIM_M // non-template kernels: compiled once, in trim_capi.cu
 } // namespace trimgpu
 #include "trim_probe_mma.cuh"
@@ -1090,6 +1208,61 @@ __global__ void trim_unpack_keys_kernel(const unsigned long long* keys, uint32_t
         const unsigned long long key = keys[static_cast<size_t>(q) * cap + i];
         ids[o + i] = static_cast<uint32_t>(key & 0xffffffffu);
         dist[o + i] = __uint_as_float(static_cast<uint32_t>(key >> 32));
+    }
+}
+
+// trim_search_range_device helpers. r^2 = r*r in fp32 (ivf.hpp:315).
+__global__ void trim_range_r2_kernel(const float* radius, uint64_t nq, float* r2, uint32_t* status) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nq)
+        return;
+    const float r = radius[i];
+    if (r < 0.0f) { // ivf.hpp:311-312 throws; here: empty result + status bit 1
+        r2[i] = -1.0f;
+        if (status)
+            atomicOr(status, 2u);
+    } else {
+        r2[i] = __fmul_rn(r, r);
+    }
+}
+
+// Segment bounds of the per-query pools for the segmented sort.
+__global__ void trim_range_seg_kernel(const unsigned int* cnt, uint64_t nq, uint32_t cap, uint64_t* beg,
+                                      uint64_t* end, uint32_t* status) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nq)
+        return;
+    const unsigned int c = cnt[i];
+    beg[i] = i * cap;
+    end[i] = i * cap + min(c, cap);
+    if (c > cap && status)
+        atomicOr(status, 1u);
+}
+
+// Sorted (d, id) keys -> per-query slots; counts and counters
+// (ivf.hpp:327-338: evaluated = stream length, edc = evaluated, dc exact).
+__global__ void trim_range_finish_kernel(const unsigned long long* sorted, const unsigned int* cnt,
+                                         const unsigned long long* dc, const unsigned long long* ev,
+                                         uint64_t nq, uint32_t cap, uint32_t nlist, uint32_t* counts,
+                                         uint32_t* ids, float* dist, unsigned long long* counters) {
+    const uint64_t q = blockIdx.x;
+    const uint32_t n = min(cnt[q], cap);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long key = sorted[q * cap + i];
+        ids[q * cap + i] = static_cast<uint32_t>(key & 0xffffffffu);
+        dist[q * cap + i] = __uint_as_float(static_cast<uint32_t>(key >> 32));
+    }
+    if (threadIdx.x == 0) {
+        counts[q] = cnt[q];
+        if (counters) {
+            unsigned long long* c = counters + q * 6;
+            c[0] = dc[q];
+            c[1] = ev[q];
+            c[2] = ev[q] - dc[q];
+            c[3] = ev[q];
+            c[4] = 0;
+            c[5] = nlist;
+        }
     }
 }
 

@@ -18,6 +18,8 @@ struct BlParams;
                                 cudaStream_t st);                                                 \
     cudaError_t launch_range_##MV(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,\
                                   cudaStream_t st);                                               \
+    cudaError_t launch_range_flat_##MV(const DevIndex& ix, const RangeParams& p, dim3 grid,        \
+                                       size_t smem, uint32_t qt, cudaStream_t st);                 \
     cudaError_t launch_bl_est_##MV(const DevIndex& ix, const BlParams& p, dim3 grid, size_t smem,  \
                                    cudaStream_t st);
 

@@ -329,3 +329,30 @@ def search_trim_ivf_knn_device(ix: GpuIvfIndex, profile: PruningProfile, d_queri
         C.c_void_p(d_status.data_ptr()) if d_status is not None else None, C.c_void_p(sh))
     _lib.check(rc, "search_trim_ivf_knn")
     return d_ids, d_dist
+
+
+def search_trim_ivf_range_device(ix: GpuIvfIndex, profile: PruningProfile, d_queries, d_radius,
+                                 nprobe: int, cap: int = 1024, d_counters=None, d_status=None,
+                                 stream=None):
+    """ivf::search_trim_ivf_range (ivf.hpp:308-347) on device tensors
+    (trim_search_range_device). Returns (counts[nq] int32, ids[nq,cap] int32,
+    dist[nq,cap] f32): query i's members are ids[i, :min(counts[i], cap)],
+    sorted by (dist, id). Bit 0 of d_status: some query exceeded cap."""
+    import torch
+
+    nq = d_queries.shape[0]
+    dev = d_queries.device
+    counts = torch.zeros(nq, dtype=torch.int32, device=dev)
+    ids = torch.empty((nq, cap), dtype=torch.int32, device=dev)
+    dist = torch.empty((nq, cap), dtype=torch.float32, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    rc = _lib.load().trim_search_range_device(
+        ix.handle, C.c_void_p(d_queries.data_ptr()), nq, C.c_void_p(d_radius.data_ptr()), nprobe,
+        profile.gamma_f32(), cap, C.c_void_p(counts.data_ptr()), C.c_void_p(ids.data_ptr()),
+        C.c_void_p(dist.data_ptr()),
+        C.c_void_p(d_counters.data_ptr()) if d_counters is not None else None,
+        C.c_void_p(d_status.data_ptr()) if d_status is not None else None, C.c_void_p(sh))
+    _lib.check(rc, "search_trim_ivf_range")
+    return counts, ids, dist

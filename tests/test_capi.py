@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _lib.load().trim_abi_version() == 1
+    assert _lib.load().trim_abi_version() == 2
 
 
 def _desc(**kw):

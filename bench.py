@@ -43,6 +43,10 @@ CONFIGS = {
     "c3": dict(kind="range", workload="flat_trim_range_10M_d128", n=10_000_000, dim=128,
                n_centers=256, sigma=0.3, nq=10_000, batch=1024, m=32, nlist=1, nprobe=1, k=0,
                gammas=[0.0, 0.8], gamma=0.8, result_size=100),
+    # BASELINE.json configs[3]: high-dimensional stress, flat kNN, uniform + L2-normalised
+    "c4": dict(workload="flat_trim_knn_1M_d960_k100", n=1_000_000, dim=960, data="uniform_normalized",
+               n_centers=0, sigma=0.0, nq=1000, batch=1000, m=120, nlist=1, nprobe=1, k=100,
+               gammas=[0.5, 0.7, 0.9], gamma=0.9),
     # BASELINE.json configs[0] (CPU-runnable reference case; parity + extra line)
     "c1": dict(workload="flat_trim_knn_100k_d128", n=100_000, dim=128, n_centers=64, sigma=0.3,
                nq=1000, batch=1000, m=16, nlist=1, nprobe=1, k=10, gammas=[0.0, 0.605, 1.0],
@@ -173,9 +177,13 @@ def build_workload(cfg, rank: int, world: int, device: int, sharded: bool = Fals
     dev = torch.device(f"cuda:{device}")
     torch.cuda.set_device(dev)
     t0 = time.time()
-    centers = B.synth_normal(cfg["n_centers"], cfg["dim"], seed=0, device=device)
-    base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1 + 7919 * rank)
-    queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
+    if cfg.get("data") == "uniform_normalized":  # dataset.hpp:44-56 normalize_rows
+        base = B.synth_uniform(cfg["n"], cfg["dim"], seed=1 + 7919 * rank, device=device)
+        queries = B.synth_uniform(cfg["nq"], cfg["dim"], seed=2, device=device)
+    else:
+        centers = B.synth_normal(cfg["n_centers"], cfg["dim"], seed=0, device=device)
+        base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1 + 7919 * rank)
+        queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
     p = B.BuildParams(m=cfg["m"], nlist=cfg["nlist"], pq_seed=3, ivf_seed=4)
     if not sharded:
         arrays = B.build_ivf(base, p)
@@ -373,7 +381,7 @@ def run_ours(args, cfg):
                          parallelism=f"id-shard x{world}" if world > 1 else "single",
                          l2="index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
                          else "index fits L2; reported as-is",
-                         data_gen="device Philox blobs, seeds centers=0 base=1 queries=2")
+                         data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))
     out["qps"] = qps
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
     out["candidates_per_query"] = evaluated / (nq * (world if False else 1))
@@ -686,7 +694,7 @@ def run_ours_range(args, cfg):
                          m=cfg["m"], nlist=1, gamma=head, radius=radius,
                          radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)",
                          parallelism="single", l2="index > L2 (no flush needed)",
-                         data_gen="device Philox blobs, seeds centers=0 base=1 queries=2")
+                         data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))
     out["qps"] = nq * args.steps / (ms / 1e3)
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
     out["mean_result_size"] = float(counts.double().mean())

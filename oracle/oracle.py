@@ -318,6 +318,17 @@ class RefOracle:
         L.ref_search_baseline_batch.argtypes = [C.POINTER(_FlatIndex), _f32p, C.c_uint64,
                                                 C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _f32p,
                                                 _u64p]
+        cp = C.c_char_p
+        L.ref_ivf_save.argtypes = [C.POINTER(_FlatIndex), C.c_double, C.c_uint64, C.c_uint32, cp]
+        L.ref_ivf_load_sizes.argtypes = [cp, _u64p, _u64p, _u32p, _u32p, _u64p]
+        L.ref_ivf_load.argtypes = [cp, _u32p, _f32p, _f32p, _u64p, _u32p, _u8p, _f32p, _f64p, _u64p, _u32p]
+        L.ref_landmarks_save.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _f32p, C.c_uint64,
+                                         _u8p, _f32p, cp]
+        L.ref_landmarks_load.argtypes = [cp, C.c_uint64, _u8p, _f32p]
+        L.ref_profile_save.argtypes = [C.c_double, C.c_double, cp]
+        L.ref_profile_load.argtypes = [cp, _f64p, _f64p]
+        L.ref_write_fvecs.argtypes = [_f32p, C.c_uint64, C.c_uint32, cp]
+        L.ref_load_fvecs.argtypes = [cp, C.c_uint64, C.c_uint32, _f32p]
         L.ref_session_create.restype = C.c_void_p
         L.ref_session_create.argtypes = [C.POINTER(_FlatIndex)]
         L.ref_session_destroy.argtypes = [C.c_void_p]
@@ -424,6 +435,65 @@ class RefOracle:
                           _ptr(ix.list_offsets, _u64p), _ptr(ix.list_ids, _u32p),
                           _ptr(ix.list_codes, _u8p), ix.code_stride, _ptr(ix.list_lx, _f32p),
                           ix.n, _ptr(ix.vectors, _f32p))
+
+    # -- on-disk formats (the reference's own save/load) --
+    def ivf_save(self, ix: HostIndex, path: str, mse=0.0, seed=0, iters=0):
+        fi = self._flat(ix)
+        self._err(self.lib.ref_ivf_save(C.byref(fi), mse, seed, iters, path.encode()), "IvfIndex::save")
+
+    def ivf_load(self, path: str) -> dict:
+        dim, nlist, tot = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        m, c = C.c_uint32(), C.c_uint32()
+        self._err(self.lib.ref_ivf_load_sizes(path.encode(), C.byref(dim), C.byref(nlist), C.byref(m),
+                                              C.byref(c), C.byref(tot)), "IvfIndex::load")
+        d, nl, mm, cc, t = dim.value, nlist.value, m.value, c.value, tot.value
+        sub = np.zeros(mm, np.uint32)
+        cent = np.zeros(cc * d, np.float32)
+        coarse = np.zeros(nl * d, np.float32)
+        offs = np.zeros(nl + 1, np.uint64)
+        ids = np.zeros(max(t, 1), np.uint32)
+        codes = np.zeros(max(t * mm, 1), np.uint8)
+        lx = np.zeros(max(t, 1), np.float32)
+        mse, seed, iters = C.c_double(), C.c_uint64(), C.c_uint32()
+        self._err(self.lib.ref_ivf_load(path.encode(), _ptr(sub, _u32p), _ptr(cent, _f32p), _ptr(coarse, _f32p),
+                                        _ptr(offs, _u64p), _ptr(ids, _u32p), _ptr(codes, _u8p), _ptr(lx, _f32p),
+                                        C.byref(mse), C.byref(seed), C.byref(iters)), "IvfIndex::load")
+        return dict(dim=d, nlist=nl, m=mm, ksub=cc, sub_dims=sub, centroids=cent, coarse=coarse,
+                    list_offsets=offs, list_ids=ids[:t], list_codes=codes[:t * mm].reshape(t, mm),
+                    list_lx=lx[:t], training_mse=mse.value, seed=seed.value, iters=iters.value)
+
+    def landmarks_save(self, dim, m, c, sub, cent, codes, lx, path: str):
+        codes = np.ascontiguousarray(codes, np.uint8)
+        lx = np.ascontiguousarray(lx, np.float32)
+        self._err(self.lib.ref_landmarks_save(dim, m, c, _ptr(np.ascontiguousarray(sub, np.uint32), _u32p),
+                                              _ptr(np.ascontiguousarray(cent, np.float32), _f32p), lx.size,
+                                              _ptr(codes, _u8p), _ptr(lx, _f32p), path.encode()),
+                  "LandmarkStore::save")
+
+    def landmarks_load(self, path: str, n: int, m: int):
+        codes = np.zeros(n * m, np.uint8)
+        lx = np.zeros(n, np.float32)
+        self._err(self.lib.ref_landmarks_load(path.encode(), n, _ptr(codes, _u8p), _ptr(lx, _f32p)),
+                  "LandmarkStore::load")
+        return codes.reshape(n, m), lx
+
+    def profile_save(self, p: float, gamma: float, path: str):
+        self._err(self.lib.ref_profile_save(p, gamma, path.encode()), "PruningProfile::save")
+
+    def profile_load(self, path: str):
+        p, g = C.c_double(), C.c_double()
+        self._err(self.lib.ref_profile_load(path.encode(), C.byref(p), C.byref(g)), "PruningProfile::load")
+        return p.value, g.value
+
+    def write_fvecs(self, x, path: str):
+        x = np.ascontiguousarray(x, np.float32)
+        self._err(self.lib.ref_write_fvecs(_ptr(x, _f32p), x.shape[0], x.shape[1], path.encode()),
+                  "write_fvecs")
+
+    def load_fvecs(self, path: str, n: int, dim: int):
+        out = np.zeros((n, dim), np.float32)
+        self._err(self.lib.ref_load_fvecs(path.encode(), n, dim, _ptr(out, _f32p)), "load_vecs")
+        return out
 
     # -- searches (ivf/ivf.hpp) --
     def search_knn(self, ix: HostIndex, qs, k, nprobe, gamma):

@@ -22,6 +22,7 @@
 #include "trimsearch/core/ground_truth.hpp"
 #include "trimsearch/core/parallel.hpp"
 #include "trimsearch/core/synthetic.hpp"
+#include "trimsearch/core/vecs_io.hpp"
 #include "trimsearch/ivf/ivf.hpp"
 #include "trimsearch/pq/pq.hpp"
 #include "trimsearch/trim/calibration.hpp"
@@ -389,6 +390,120 @@ int ref_session_run(void* p, int kind, const float* qs, std::uint64_t nq, std::u
         for (const auto& c : cs)
             tot += c;
         put_counters(counters_sum_out, tot, 0);
+    });
+}
+
+// ---- on-disk formats (test infrastructure: pins paper_2508_17828_b200/formats.py)
+// IvfIndex::save (ivf.hpp:53-76), with the codebook's bookkeeping fields set.
+int ref_ivf_save(const FlatIndex* f, double training_mse, std::uint64_t seed, std::uint32_t iters,
+                 const char* path) {
+    return guarded([&] {
+        auto ix = make_ivf(*f);
+        ix.codebook.training_mse = training_mse;
+        ix.codebook.params.seed = seed;
+        ix.codebook.params.kmeans_iters = iters;
+        ix.save(path);
+    });
+}
+
+// IvfIndex::load (ivf.hpp:78-107): sizes, then the arrays (concatenated lists).
+int ref_ivf_load_sizes(const char* path, std::uint64_t* dim, std::uint64_t* nlist, std::uint32_t* m,
+                       std::uint32_t* c, std::uint64_t* total) {
+    return guarded([&] {
+        const auto ix = ivf::IvfIndex::load(path);
+        *dim = ix.dim;
+        *nlist = ix.nlist;
+        *m = static_cast<std::uint32_t>(ix.codebook.m());
+        *c = static_cast<std::uint32_t>(ix.codebook.c());
+        std::uint64_t t = 0;
+        for (const auto& l : ix.lists)
+            t += l.size();
+        *total = t;
+    });
+}
+
+int ref_ivf_load(const char* path, std::uint32_t* sub_dims, float* centroids, float* coarse,
+                 std::uint64_t* offsets, std::uint32_t* ids, std::uint8_t* codes, float* lx,
+                 double* training_mse, std::uint64_t* seed, std::uint32_t* iters) {
+    return guarded([&] {
+        const auto ix = ivf::IvfIndex::load(path);
+        const auto& cb = ix.codebook;
+        std::size_t co = 0;
+        for (std::size_t j = 0; j < cb.m(); ++j) {
+            sub_dims[j] = static_cast<std::uint32_t>(cb.sub_dims[j]);
+            std::memcpy(centroids + co, cb.centroids[j].data(), sizeof(float) * cb.centroids[j].size());
+            co += cb.centroids[j].size();
+        }
+        std::memcpy(coarse, ix.coarse_centroids.data(), sizeof(float) * ix.coarse_centroids.size());
+        std::uint64_t e = 0;
+        offsets[0] = 0;
+        for (std::size_t l = 0; l < ix.lists.size(); ++l) {
+            const auto& L = ix.lists[l];
+            for (std::size_t i = 0; i < L.size(); ++i, ++e) {
+                ids[e] = L.ids[i];
+                std::memcpy(codes + e * cb.m(), L.codes.data() + i * cb.m(), cb.m());
+                lx[e] = L.lx_dist[i];
+            }
+            offsets[l + 1] = e;
+        }
+        *training_mse = cb.training_mse;
+        *seed = cb.params.seed;
+        *iters = static_cast<std::uint32_t>(cb.params.kmeans_iters);
+    });
+}
+
+// LandmarkStore::save / load (trim/landmarks.hpp:29-53).
+int ref_landmarks_save(std::uint32_t dim, std::uint32_t m, std::uint32_t c, const std::uint32_t* sub_dims,
+                       const float* centroids, std::uint64_t n, const std::uint8_t* codes, const float* lx,
+                       const char* path) {
+    return guarded([&] {
+        trim::LandmarkStore lm;
+        lm.codebook = make_cb(dim, m, c, sub_dims, centroids);
+        lm.count = n;
+        lm.codes.assign(codes, codes + n * m);
+        lm.lx_dist.assign(lx, lx + n);
+        lm.save(path);
+    });
+}
+
+int ref_landmarks_load(const char* path, std::uint64_t n_expected, std::uint8_t* codes, float* lx) {
+    return guarded([&] {
+        const auto lm = trim::LandmarkStore::load(path);
+        if (lm.count != n_expected)
+            throw DataError("landmark count mismatch");
+        std::memcpy(codes, lm.codes.data(), lm.codes.size());
+        std::memcpy(lx, lm.lx_dist.data(), sizeof(float) * lm.count);
+    });
+}
+
+// trim::PruningProfile::save / load (trim/calibration.hpp:234-288).
+int ref_profile_save(double p, double gamma, const char* path) {
+    return guarded([&] {
+        auto prof = trim::PruningProfile::manual(gamma);
+        prof.p = p;
+        prof.save(path);
+    });
+}
+
+int ref_profile_load(const char* path, double* p, double* gamma) {
+    return guarded([&] {
+        const auto prof = trim::PruningProfile::load(path);
+        *p = prof.p;
+        *gamma = prof.gamma;
+    });
+}
+
+// core/vecs_io.hpp: write_fvecs / load_vecs.
+int ref_write_fvecs(const float* data, std::uint64_t n, std::uint32_t dim, const char* path) {
+    return guarded([&] { write_fvecs(path, make_ds(data, n, dim)); });
+}
+
+int ref_load_fvecs(const char* path, std::uint64_t n_expected, std::uint32_t dim, float* out) {
+    return guarded([&] {
+        const auto ds = load_vecs(path, ElementKind::Float32);
+        if (ds.count != n_expected || ds.dim != dim)
+            throw DataError("fvecs shape mismatch");
+        std::memcpy(out, ds.data.data(), sizeof(float) * n_expected * dim);
     });
 }
 

@@ -23,6 +23,8 @@ from .ivf import (  # noqa: F401
     search_trim_ivf_knn_device,
     search_trim_ivf_range,
     search_trim_ivf_range_batch,
+    search_trim_ivf_range_device,
 )
+from . import formats  # noqa: F401  (reference on-disk formats)
 
 __version__ = "0.1.0"

@@ -226,8 +226,9 @@ def run_ours(args, cfg):
     from paper_2508_17828_b200 import ivf as G
 
     world, rank, local = dist_env()
-    sharded = world > 1 or args.force_shard
-    if sharded:
+    replicas = world > 1 and args.parallel == "replicas"
+    sharded = (world > 1 and not replicas) or args.force_shard
+    if sharded or replicas:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
@@ -235,8 +236,12 @@ def run_ours(args, cfg):
                                 device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    arrays, queries = build_workload(cfg, rank, world, local, sharded)
+    arrays, queries = build_workload(cfg, 0 if replicas else rank, 1 if replicas else world, local, sharded)
     gix = G.GpuIvfIndex(arrays, device=local)
+    q_lo, q_hi = 0, cfg["nq"]
+    if replicas:  # every rank: the whole index, a contiguous slice of the queries
+        from paper_2508_17828_b200.distributed import shard_bounds
+        q_lo, q_hi = shard_bounds(cfg["nq"], rank, world)
     lib = _lib.load()
     import ctypes as C
 
@@ -253,7 +258,7 @@ def run_ours(args, cfg):
     dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
     cts = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
-    batches = [(b, min(B, nq - b)) for b in range(0, nq, B)]
+    batches = [(b, min(B, q_hi - b)) for b in range(q_lo, q_hi, B)]
     if sharded:
         import torch.distributed as dist
         g_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
@@ -307,7 +312,7 @@ def run_ours(args, cfg):
         for _ in range(warmup):
             step(gamma)
         torch.cuda.synchronize()
-        if sharded:
+        if sharded or replicas:
             dist.barrier()
         torch.cuda.synchronize()
         ev = []
@@ -321,7 +326,7 @@ def run_ours(args, cfg):
                 launches += step(gamma, ev)
             s1.record(stream)
             torch.cuda.synchronize()
-        if sharded:
+        if sharded or replicas:
             dist.barrier()
         torch.cuda.synchronize()
         ms = s0.elapsed_time(s1)
@@ -338,8 +343,9 @@ def run_ours(args, cfg):
                 cur[1] = max(cur[1], b)
         if cur is not None:
             filt_ms += cur[1] - cur[0]
-        ct = cts.sum(0).cpu().numpy()  # identical every step
-        if sharded:
+        ct = cts[q_lo:q_hi].sum(0).cpu().numpy()  # identical every step
+        if sharded or replicas:
+            import torch.distributed as dist
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -360,7 +366,7 @@ def run_ours(args, cfg):
                              qps=nq * max(1, min(2, args.steps)) / (ms / 1e3),
                              prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])))
         if rank == 0:
-            sweep[str(g)]["recall@10"] = recall(arrays, queries, ids, k, args.recall_q, world)
+            sweep[str(g)][f"recall@{k}"] = recall(arrays, queries, ids, k, args.recall_q, world)
     clk = ClockSampler(local)
     for _ in range(args.warmup):
         step(head)
@@ -374,11 +380,13 @@ def run_ours(args, cfg):
     out = dict(metric=metric_name(cfg),
                value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
-               scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic")
+               scaling="strong" if replicas else "weak", vs_baseline=None, dtype="f32 (u8 PQ codes)",
+               data="synthetic")
     out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
                          queries=nq, batch=B, m=cfg["m"], nlist=cfg["nlist"],
                          nprobe=cfg["nprobe"], k=k, gamma=head,
-                         parallelism=f"id-shard x{world}" if world > 1 else "single",
+                         parallelism=(f"replicas x{world}" if replicas else f"id-shard x{world}") if world > 1
+                         else "single",
                          l2="index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
                          else "index fits L2; reported as-is",
                          data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))
@@ -411,7 +419,7 @@ def run_ours(args, cfg):
     out["clocks"] = clk.summary()
     out["sweep"] = sweep
     if rank == 0:
-        out["recall@10"] = recall(arrays, queries, ids, k, args.recall_q, world)
+        out[f"recall@{k}"] = recall(arrays, queries, ids, k, args.recall_q, world)
     # e2e through the C-ABI host call with pinned host buffers
     out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -805,6 +813,9 @@ def main():
     ap.add_argument("--recall-q", type=int, default=200)
     ap.add_argument("--streams", type=int, default=2,
                     help="streams that consecutive batches alternate between (1 = serial)")
+    ap.add_argument("--parallel", default="shard", choices=["shard", "replicas"],
+                    help="N>1 layout: id-sharded index (weak scaling, all-gather merge) or replicas "
+                         "(whole index per GPU, queries partitioned, strong scaling, no collective)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the id-sharded path (all-gather + device merge) even at N=1")
     args = ap.parse_args()

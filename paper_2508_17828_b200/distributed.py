@@ -12,8 +12,10 @@ the device by (dist_sq, id), the order ScoredId defines
 (core/ground_truth.hpp:39-50). Counters are summed with an all-reduce.
 
 A replicas layout (every rank holds the whole index and a slice of the
-queries) needs no collective; bench.py --gpus N measures the id-sharded
-layout with a full-size shard per GPU (weak scaling), DESIGN.md §6.
+queries, ReplicaIvfIndex) needs no data-path collective and reproduces the
+single run exactly; bench.py --gpus N measures the id-sharded layout with a
+full-size shard per GPU (weak scaling) by default and the replicas layout with
+--parallel replicas, DESIGN.md §6.
 """
 from __future__ import annotations
 
@@ -130,3 +132,63 @@ class ShardedIvfIndex:
         c = cts[:, :5].sum(0)
         dist.all_reduce(c, group=self.group)
         return mi, md, c
+
+
+class ReplicaIvfIndex:
+    """Replicas layout: every rank holds the whole index and
+    searches its contiguous slice [shard_bounds(nq, rank, world)) of each query
+    batch; per-query results and counters are exactly the single run's (each
+    query's stream is untouched). No collective on the data path;
+    gather() (rank-ordered all-gather) is a convenience for callers that want
+    every result on every rank.
+
+    searcher(queries, k, nprobe, gamma) -> (ids, dist, counters) as for
+    ShardedIvfIndex; the default is the GPU path over `arrays`."""
+
+    def __init__(self, arrays: IvfArrays, group=None, searcher: Optional[Callable] = None,
+                 device: Optional[int] = None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if searcher is None:
+            from .ivf import GpuIvfIndex, PruningProfile, search_trim_ivf_knn_device
+            self.gpu = GpuIvfIndex(arrays, device=device or 0)
+
+            def searcher(q, k, nprobe, gamma):
+                import torch
+                cts = torch.zeros((q.shape[0], 6), dtype=torch.int64, device=q.device)
+                ids, d = search_trim_ivf_knn_device(self.gpu, PruningProfile.manual(gamma), q, k, nprobe,
+                                                    d_counters=cts)
+                return ids, d, cts
+        self._search = searcher
+
+    def bounds(self, nq: int):
+        return shard_bounds(nq, self.rank, self.world)
+
+    def search_knn(self, queries, k: int, nprobe: int, gamma: float):
+        """This rank's slice: (lo, hi, ids[hi-lo,k], dist, counters[hi-lo,6])."""
+        lo, hi = self.bounds(queries.shape[0])
+        ids, d, cts = self._search(queries[lo:hi], k, nprobe, gamma)
+        return lo, hi, ids, d, cts
+
+    def gather(self, nq: int, part):
+        """All ranks' slices in query order (rows padded to the largest slice
+        for the all-gather, then trimmed)."""
+        import torch
+        import torch.distributed as dist
+
+        lo, hi, ids, d, cts = part
+        rows = max(shard_bounds(nq, r, self.world)[1] - shard_bounds(nq, r, self.world)[0]
+                   for r in range(self.world))
+        out = []
+        for t in (ids, d, cts):
+            pad = torch.zeros((rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            pad[:hi - lo] = t
+            g = torch.empty((self.world * rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(g, pad.contiguous(), group=self.group)
+            g = g.view(self.world, rows, *t.shape[1:])
+            out.append(torch.cat([g[r, :shard_bounds(nq, r, self.world)[1] - shard_bounds(nq, r, self.world)[0]]
+                                  for r in range(self.world)]))
+        return tuple(out)

@@ -122,3 +122,45 @@ def test_two_rank_gloo_search_and_merge():
             bf_ids, bf_d = co.brute_force_knn(ix.vectors, qs, k)
             np.testing.assert_array_equal(i0, bf_ids)
             np.testing.assert_array_equal(d0, bf_d)
+
+
+def _replica_worker(rank, port, results):
+    from oracle.oracle import COracle
+    from paper_2508_17828_b200.distributed import ReplicaIvfIndex
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        ix, qs, _ = goldens.load("ivf_fixture")
+        full = IvfArrays.from_any(ix)
+        h = host_index(full)
+        co = COracle()
+
+        def searcher(q, k, nprobe, gamma):
+            ids, d, ct, cdc = co.search_knn(h, q.numpy(), k, nprobe, gamma)
+            c6 = np.concatenate([ct.astype(np.int64), cdc.astype(np.int64)[:, None]], 1)
+            return (torch.from_numpy(ids.view(np.int32).copy()), torch.from_numpy(d), torch.from_numpy(c6))
+        rep = ReplicaIvfIndex(full, searcher=searcher)
+        q = torch.from_numpy(qs)
+        part = rep.search_knn(q, 10, 5, 0.35)
+        ids, d, cts = rep.gather(q.shape[0], part)
+        results[rank] = (part[0], part[1], ids.numpy().copy(), d.numpy().copy(), cts.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replicas_equal_single_run():
+    from oracle.oracle import COracle
+    ix, qs, _ = goldens.load("ivf_fixture")
+    h = host_index(IvfArrays.from_any(ix))
+    want_ids, want_d, want_ct, want_cdc = COracle().search_knn(h, qs, 10, 5, 0.35)
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_replica_worker, args=(_free_port(), results), nprocs=WORLD, join=True)
+    spans = sorted((results[r][0], results[r][1]) for r in range(WORLD))
+    assert spans[0][0] == 0 and spans[-1][1] == len(qs) and spans[0][1] == spans[1][0]
+    for r in range(WORLD):
+        _, _, ids, d, cts = results[r]
+        np.testing.assert_array_equal(ids.view(np.uint32), want_ids)
+        np.testing.assert_array_equal(d.view(np.uint32), want_d.view(np.uint32))
+        np.testing.assert_array_equal(cts[:, :5], want_ct.astype(np.int64))

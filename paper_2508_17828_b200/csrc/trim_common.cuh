@@ -71,6 +71,11 @@ __device__ __forceinline__ float euclid_sq_vec4(const float* __restrict__ q,
     const uint32_t nv = dim >> 2;
     const float4* q4 = reinterpret_cast<const float4*>(q);
     const float4* x4 = reinterpret_cast<const float4*>(x);
+    // long rows (>= 1 KB): the whole row in flight at once (one DRAM round trip);
+    // the loop below, which keeps only a few loads in flight, then hits L1
+    if (dim >= 256)
+        for (uint32_t o = 0; o < dim * 4u; o += 128u)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(x) + o));
 #pragma unroll 4
     for (uint32_t v = 0; v < nv; ++v) {
         const float4 a = q4[v];

@@ -253,10 +253,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     for (;;) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        // suspend-time hint: the warp sleeps in hardware until the phase
+        // completes (or the hint elapses) instead of spinning on issue slots
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done)
-                     : "r"(saddr(bar)), "r"(parity)
+                     : "r"(saddr(bar)), "r"(parity), "r"(1000000u)
                      : "memory");
         if (done)
             break;

@@ -127,6 +127,11 @@ struct trim_index {
     float4* coarse_t = nullptr;
     float* cn2 = nullptr;
     float* cn = nullptr;
+    // flat kNN distance bounds (trim_flat_mma.cuh): pre-tiled rows + norms, built on first use
+    std::mutex flat_mu;
+    float4* flat_tiles = nullptr;
+    float* xn = nullptr;
+    float* xn2 = nullptr;
     uint64_t bytes = 0;
     std::vector<void*> allocs;
 
@@ -433,6 +438,35 @@ int validate_knn(uint32_t k, float gamma) {
     return TRIM_OK;
 }
 
+// TRIM_FLAT_BOUNDS=0 disables the tensor-core distance bounds of flat kNN
+// scans (A/B and parity tests; results are identical either way).
+bool flat_bounds_enabled() {
+    const char* e = std::getenv("TRIM_FLAT_BOUNDS");
+    return !(e && e[0] == '0');
+}
+
+// Pre-tiled rows and row norms for trim_flat_dist_kernel, built once per index
+// on first use (flat indexes only; ~ the size of the vectors).
+bool ensure_flat_tiles(trim_index* ix) {
+    std::lock_guard<std::mutex> lk(ix->flat_mu);
+    if (ix->flat_tiles)
+        return true;
+    const DevIndex& v = ix->dev;
+    const uint32_t K = flat_kpad(v.dim);
+    const uint64_t nrt = (v.n + kMmaN - 1) / kMmaN;
+    ix->flat_tiles = ix->alloc<float4>(nrt * (K / kFlatKB) * 8 * kMmaN);
+    ix->xn = ix->alloc<float>(v.n);
+    ix->xn2 = ix->alloc<float>(v.n);
+    trim_flat_tile_kernel<<<static_cast<unsigned>(nrt), kThreads>>>(v.vectors, v.n, v.dim_stride, v.dim, K,
+                                                                     ix->flat_tiles);
+    CK(cudaGetLastError());
+    trim_row_norm_kernel<<<static_cast<unsigned>((v.n + 255) / 256), 256>>>(v.vectors, v.n, v.dim_stride, v.dim,
+                                                                           ix->xn2, ix->xn);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    return true;
+}
+
 // kNN filter launch over padded device queries and precomputed probe lists
 // (d_probe null => nlist == 1, the single list 0).
 int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t np,
@@ -475,11 +509,43 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         p.skipped = ix->d_skipped;
         p.timeline = g_timeline;
     }
-    // grid.x is limited to 2^31-1; process huge batches in slices
-    const uint64_t kMaxGrid = 1u << 30;
-    for (uint64_t b = 0; b < nq; b += kMaxGrid) {
+    // flat scans: tensor-core distance bounds for every (query, row), so only
+    // members that can enter the top-k get the exact distance
+    const bool flat_bounds = ix->dev.nlist == 1 && np == 1 && ix->dev.n > 0 && flat_bounds_enabled() &&
+                             ensure_flat_tiles(const_cast<trim_index*>(ix));
+    const uint64_t ld = flat_bounds ? (ix->dev.n + kMmaN - 1) / kMmaN * kMmaN : 0;
+    // slices: grid.x <= 2^31-1; with bounds, D~ of a slice (nq x ld floats) within ~8 GB
+    uint64_t slice = 1u << 30;
+    if (flat_bounds)
+        slice = std::max<uint64_t>(kMmaM, (8ull << 30) / (ld * 4) / kMmaM * kMmaM);
+    for (uint64_t b = 0; b < nq; b += slice) {
         KnnParams pb = p;
-        pb.nq = std::min<uint64_t>(kMaxGrid, nq - b);
+        pb.nq = std::min<uint64_t>(slice, nq - b);
+        DevBuf dap;
+        if (flat_bounds) {
+            const DevIndex& v = ix->dev;
+            const uint32_t K = flat_kpad(v.dim);
+            const uint64_t nqt = (pb.nq + kMmaM - 1) / kMmaM, nrt = ld / kMmaN;
+            const float* qb = d_q + b * v.dim_stride;
+            DevBuf qtiles(sizeof(float4) * nqt * (K / kFlatKB) * 8 * kMmaM, st), qn2(sizeof(float) * pb.nq, st);
+            trim_flat_tile_kernel<<<static_cast<unsigned>(nqt), kThreads, 0, st>>>(qb, pb.nq, v.dim_stride, v.dim, K,
+                                                                                   qtiles.as<float4>());
+            CK(cudaGetLastError());
+            trim_query_norm_kernel<<<static_cast<unsigned>((pb.nq + 255) / 256), 256, 0, st>>>(qb, pb.nq, v.dim_stride,
+                                                                                               v.dim, qn2.as<float>());
+            CK(cudaGetLastError());
+            dap = DevBuf(sizeof(float) * pb.nq * ld, st);
+            CK(cudaFuncSetAttribute(trim_flat_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(flat_mma_smem())));
+            trim_flat_dist_kernel<<<dim3(static_cast<unsigned>(nqt), static_cast<unsigned>(nrt)), kMmaThreads,
+                                    flat_mma_smem(), st>>>(qtiles.as<float4>(), qn2.as<float>(), pb.nq,
+                                                           ix->flat_tiles, ix->xn2, v.n, K, dap.as<float>(), ld);
+            CK(cudaGetLastError());
+            pb.dap = dap.as<float>();
+            pb.dap_ld = ld;
+            pb.xnorm = ix->xn;
+            pb.xnorm2 = ix->xn2;
+        }
         pb.queries = d_q + b * ix->dev.dim_stride;
         pb.probe = p.probe ? p.probe + b * np : nullptr;
         pb.ids_out = d_ids + b * k;

@@ -201,6 +201,11 @@ struct KnnParams {
     float kest;              // 1 - relative error bound of relaxed_lb's evaluation
     unsigned long long* skipped; // positions skipped by the list bound (diagnostic)
     unsigned long long* timeline; // nq*kTimeline phase stamps/cycle counts (perf probe only), or null
+    // flat scans: tensor-core distance bounds (trim_flat_mma.cuh), or null
+    const float* dap;      // nq x dap_ld: D~[q][row]
+    uint64_t dap_ld;
+    const float* xnorm;    // |x| per row, rounded up
+    const float* xnorm2;   // |x|^2 per row
 };
 
 constexpr uint32_t kTimeline = 16;
@@ -568,6 +573,13 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     }
 
     // ---------------------------------------------------- worker warps
+    // flat scans with tensor-core bounds: |q| and |q|^2 rounded up (for E)
+    float qn = 0.0f, qn2 = 0.0f;
+    if (p.dap) {
+        for (uint32_t i = 0; i < ix.dim; ++i)
+            qn2 = __fadd_ru(qn2, __fmul_ru(qv[i], qv[i]));
+        qn = __fsqrt_ru(qn2);
+    }
     TRIM_TL(const bool wtl = tl && tid == kWarp; // worker 0, lane 0 records
             unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
             unsigned long long wk = wtl ? clock64() : 0;)
@@ -647,8 +659,19 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         float d = 0.0f;
         if (keep) { // exact L2 (ivf.hpp:276) of every member the replay may evaluate
             id = __ldg(ix.list_ids + x.e);
-            const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
-            d = euclid_sq_vec4(qv, row, ix.dim);
+            const uint64_t rw = id - ix.id_base;
+            bool exact = true;
+            if (p.dap) { // d >= D~ - E > T_pub >= T_live: cannot replace the top (ivf.hpp:277)
+                const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(p.xnorm + rw)), 1.0f / 128.0f),
+                                          __fmul_ru(__fadd_ru(qn2, __ldg(p.xnorm2 + rw)), 1.0f / 16384.0f));
+                const float dl = __fsub_rd(__ldg(p.dap + static_cast<size_t>(q) * p.dap_ld + rw), e);
+                if (dl > ld_volatile(s_T)) {
+                    d = dl;
+                    exact = false;
+                }
+            }
+            if (exact)
+                d = euclid_sq_vec4(qv, ix.vectors + rw * ix.dim_stride, ix.dim);
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (keep) {
@@ -958,6 +981,7 @@ trim_range_flat_kernel(DevIndex ix, RangeParams p, uint32_t qt) {
 #ifndef TRIM_M // non-template kernels: compiled once, in trim_capi.cu
 } // namespace trimgpu
 #include "trim_probe_mma.cuh"
+#include "trim_flat_mma.cuh"
 namespace trimgpu {
 // --------------------------------------------------------------------------
 // trim_probe_kernel — probe_order (ivf.hpp:173-187): coarse distances in the

@@ -37,10 +37,12 @@ def assert_bits(a, b):
 # TRIM_EPS_SCALE widens the any-order ADC interval, so most members are
 # decided by the reference-order fallback (adc_serial) instead of the interval
 # — the rare path must be exact too.
-@pytest.fixture(params=["default", "wide_interval"])
+@pytest.fixture(params=["default", "wide_interval", "no_flat_bounds"])
 def filter_mode(request, monkeypatch):
     if request.param == "wide_interval":
         monkeypatch.setenv("TRIM_EPS_SCALE", "20000")
+    if request.param == "no_flat_bounds":  # flat kNN without the tensor-core distance bounds
+        monkeypatch.setenv("TRIM_FLAT_BOUNDS", "0")
     return request.param
 
 
@@ -216,7 +218,9 @@ def config1():
 
 
 @pytest.mark.parametrize("gamma", [0.0, 0.605, 1.0])
-def test_config1_full_scale_parity(config1, gamma):
+@pytest.mark.parametrize("bounds", ["1", "0"])
+def test_config1_full_scale_parity(config1, gamma, bounds, monkeypatch):
+    monkeypatch.setenv("TRIM_FLAT_BOUNDS", bounds)
     hix, qs, gix = config1
     want = co.search_knn(hix, qs, 10, 1, gamma)
     got = G.search_trim_ivf_knn_batch(gix, G.PruningProfile.manual(gamma), qs, 10, 1)

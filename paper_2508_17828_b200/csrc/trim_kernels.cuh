@@ -518,17 +518,37 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 const uint32_t cnt = cnts[w];
                 const uint32_t g0 = s * kChunkW + w * kPerWorker;
                 TRIM_TL(members += cnt;)
-                for (uint32_t i = 0; i < cnt; ++i) {
-                    const float lo = s_lo[g0 + i];
-                    if (lo < topk.wd) { // else est >= lo >= T_live: pruned (ivf.hpp:275)
-                        bool ev = true; // hi < T_live: est < T_live
-                        if (!(s_hi[g0 + i] < topk.wd))
-                            ev = exact_est(c, w, i, bin_mask[s * kWorkers + w]) < topk.wd;
-                        if (ev) {
-                            ++dc;
-                            topk.offer(s_d[g0 + i], s_e[g0 + i]);
-                        }
+                // Warp-parallel replay of the bin (members in stream order, lane i <->
+                // member i): with the live threshold T, a member is pruned iff
+                // lo >= T, evaluated iff hi < T (ivf.hpp:275) and replaces the top iff
+                // also (d, id) < top (ivf.hpp:277-282). Members up to the first one
+                // that replaces (or whose interval straddles T) are decided at once;
+                // that one is handled alone (it may lower T), then the rest again.
+                const bool valid = lane < cnt;
+                const float lo = valid ? s_lo[g0 + lane] : kInf;
+                const float hi = valid ? s_hi[g0 + lane] : kInf;
+                const float dd = valid ? s_d[g0 + lane] : kInf;
+                const uint32_t did = valid ? s_e[g0 + lane] : kInvalidId;
+                uint32_t start = 0;
+                while (start < cnt) {
+                    const bool mine = valid && lane >= start;
+                    const bool maybe = mine && lo < topk.wd;
+                    const bool sure = maybe && hi < topk.wd;
+                    const bool hard = maybe && (!sure || scored_less(dd, did, topk.wd, topk.wid));
+                    const uint32_t hb = __ballot_sync(0xffffffffu, hard);
+                    const uint32_t f = hb ? static_cast<uint32_t>(__ffs(hb) - 1) : cnt;
+                    dc += __popc(__ballot_sync(0xffffffffu, sure && lane < f));
+                    if (f >= cnt)
+                        break;
+                    const float hf = __shfl_sync(0xffffffffu, hi, f);
+                    bool ev = true;
+                    if (!(hf < topk.wd))
+                        ev = exact_est(c, w, f, bin_mask[s * kWorkers + w]) < topk.wd;
+                    if (ev) {
+                        ++dc;
+                        topk.offer(__shfl_sync(0xffffffffu, dd, f), __shfl_sync(0xffffffffu, did, f));
                     }
+                    start = f + 1;
                 }
             }
             if (lane == 0)

@@ -402,7 +402,13 @@ def run_ours(args, cfg):
     # code/lx: the kernel's algorithmic bytes count only the positions it scans
     skipped_all = skipped * (world if world > 1 else 1)
     scanned = evaluated - skipped_all
-    alg_bytes_step = scanned * (m + 4) + dc * (4 * D + 4)
+    flat_bounds = cfg["nlist"] == 1 and os.environ.get("TRIM_FLAT_BOUNDS") != "0"
+    if flat_bounds:
+        # flat scans read D~[q][row] (4 B) for evaluated candidates; exact rows only
+        # for the few members that can enter the top-k (not counted)
+        alg_bytes_step = scanned * (m + 4) + dc * 4
+    else:
+        alg_bytes_step = scanned * (m + 4) + dc * (4 * D + 4)
     per_launch_bytes = alg_bytes_step / max(1, nl // args.steps) / (world if world > 1 else 1)
     avg_launch_ms = fms / max(1, nl)  # filter-busy time per launch (overlap-aware)
     achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9
@@ -412,6 +418,7 @@ def run_ours(args, cfg):
                            bytes_per_candidate=bytes_per_cand, peak_source=peak_src,
                            filter_share_of_step=fms / ms,
                            list_skip_fraction=skipped_all / max(1.0, evaluated),
+                           flat_distance_bounds=flat_bounds,
                            stream_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4))
                            / max(1, nl // args.steps) / (world if world > 1 else 1)
                            / (avg_launch_ms / 1e3) / 1e9)

@@ -66,14 +66,15 @@ __device__ __forceinline__ float euclid_sq_generic(const float* a, const float* 
 // acc0..acc3 in exactly the CPU order. `q` lives in shared memory (all lanes
 // read the same address: broadcast), `x` in global memory.
 __device__ __forceinline__ float euclid_sq_vec4(const float* __restrict__ q,
-                                                const float* __restrict__ x, uint32_t dim) {
+                                                const float* __restrict__ x, uint32_t dim,
+                                                bool prefetch = false) {
     float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f, acc3 = 0.0f;
     const uint32_t nv = dim >> 2;
     const float4* q4 = reinterpret_cast<const float4*>(q);
     const float4* x4 = reinterpret_cast<const float4*>(x);
     // long rows (>= 1 KB): the whole row in flight at once (one DRAM round trip);
     // the loop below, which keeps only a few loads in flight, then hits L1
-    if (dim >= 256)
+    if (prefetch || dim >= 256)
         for (uint32_t o = 0; o < dim * 4u; o += 128u)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(x) + o));
 #pragma unroll 4

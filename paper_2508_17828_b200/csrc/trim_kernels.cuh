@@ -419,7 +419,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     ++li;
                 const uint64_t e = st.base[li] + (i - st.cum[li]);
                 id = __ldg(ix.list_ids + e);
-                d = euclid_sq_vec4(qv, ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride, ix.dim);
+                d = euclid_sq_vec4(qv, ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride, ix.dim,
+                                   true); // the whole row in one round trip: the seeds gate every chunk
             }
             const uint32_t cnt = min(static_cast<uint32_t>(kWarp), nseed - b0);
             for (uint32_t j = 0; j < cnt; ++j)

@@ -258,8 +258,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     for (;;) {
-        // suspend-time hint: the warp sleeps in hardware until the phase
-        // completes (or the hint elapses) instead of spinning on issue slots
+        // suspend-time hint: the warp may sleep in hardware until the phase completes
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done)
@@ -267,6 +266,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                      : "memory");
         if (done)
             break;
+    }
+}
+// For the long once-per-query waits (plan, chunk 0's replay): back off so the
+// waiting warps do not burn the issue slots the SM's other queries need.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(saddr(bar)), "r"(parity)
+                     : "memory");
+        if (done)
+            break;
+        __nanosleep(256u);
     }
 }
 __device__ __forceinline__ float ld_volatile(const float* p) {
@@ -614,7 +628,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         wc[0] = t - wk;
         wk = t;
     })
-    mbar_wait(plan, 0); // seeds done, compacted stream ready
+    mbar_wait_backoff(plan, 0); // seeds done, compacted stream ready
     TRIM_TL(if (wtl) {
         const unsigned long long t = clock64();
         wc[1] = t - wk;
@@ -659,7 +673,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         if (c >= kRing)
             mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
         if (c == 1) // filter the rest against the threshold after chunk 0, not the seeds'
-            mbar_wait(empty, 0);
+            mbar_wait_backoff(empty, 0);
         const float T = ld_volatile(s_T);
         TRIM_TL(const unsigned long long k1 = wtl ? clock64() : 0;)
         const uint32_t g0 = s * kChunkW + w * kPerWorker;

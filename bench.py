@@ -225,11 +225,12 @@ def run_ours(args, cfg):
     from paper_2508_17828_b200 import _lib
     from paper_2508_17828_b200 import ivf as G
 
+    import torch.distributed as dist
+
     world, rank, local = dist_env()
     replicas = world > 1 and args.parallel == "replicas"
     sharded = (world > 1 and not replicas) or args.force_shard
     if sharded or replicas:
-        import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=rank, world_size=world,
@@ -260,7 +261,6 @@ def run_ours(args, cfg):
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     batches = [(b, min(B, q_hi - b)) for b in range(q_lo, q_hi, B)]
     if sharded:
-        import torch.distributed as dist
         g_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
         g_d = torch.empty((world * nq, k), dtype=torch.float32, device=dev)
         m_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
@@ -345,7 +345,6 @@ def run_ours(args, cfg):
             filt_ms += cur[1] - cur[0]
         ct = cts[q_lo:q_hi].sum(0).cpu().numpy()  # identical every step
         if sharded or replicas:
-            import torch.distributed as dist
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())

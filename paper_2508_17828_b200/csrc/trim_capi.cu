@@ -577,7 +577,7 @@ int baseline_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_
         return set_err(TRIM_EINVAL, "search_baseline_ivfpq: k_prime > %u is not supported",
                        kSelSmemKeys);
     const uint64_t bound = std::max<uint64_t>(1, ix->stream_bound(np));
-    const uint32_t slice = 32 * kChunkMax;
+    const uint32_t slice = 32 * kBaselineSlice;
     const uint64_t nslices = (bound + slice - 1) / slice;
     const uint64_t qb = std::max<uint64_t>(1, std::min<uint64_t>({nq, 65535, (1ull << 31) / (bound * 8)}));
     size_t est_smem = lut_bytes(dispatch_m(ix->dev), ix->dev.m) + sizeof(float) * ix->dev.dim_stride;

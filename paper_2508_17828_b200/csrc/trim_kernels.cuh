@@ -18,9 +18,7 @@ namespace trimgpu {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / kWarp;
-constexpr int kChunkU = 2;                      // kNN: candidates per thread per chunk
-constexpr int kChunkMax = kThreads * kChunkU;   // 512 stream positions per kNN chunk
-constexpr int kBins = kChunkU * kWarps;         // 16 survivor bins of 32 slots
+constexpr int kBaselineSlice = 512;             // IVFPQ baseline: stream positions per slice unit
 constexpr int kRangeU = 4;                      // range: candidates per thread per chunk
 constexpr int kRangeChunk = kThreads * kRangeU; // 1024
 

@@ -391,7 +391,7 @@ void range_launch(const trim_index* ix, const float* d_q, uint64_t nq, const flo
     const uint64_t bound = ix->stream_bound(np);
     const uint32_t qt = d_probe ? 1u : range_flat_qt(v);
     if (qt > 1) { // flat scan, query-tiled; at most 65535 slices (grid.y)
-        uint64_t slice = 64 * kFlatThreads;
+        uint64_t slice = 512 * kFlatThreads; // 256k rows: the tile's LUT builds amortised over ~1.5M pairs
         if ((bound + slice - 1) / slice > 65535)
             slice = ((bound + 65534) / 65535 + kFlatThreads - 1) / kFlatThreads * kFlatThreads;
         const uint64_t nslices = std::max<uint64_t>(1, (bound + slice - 1) / slice);

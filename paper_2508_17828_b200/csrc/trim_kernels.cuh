@@ -986,7 +986,7 @@ trim_range_flat_kernel(DevIndex ix, RangeParams p, uint32_t qt) {
                     atomicAdd(s_dc + t, 1u);
                     const uint32_t id = __ldg(ix.list_ids + e);
                     const float* row = ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride;
-                    const float d = euclid_sq_vec4(qvs + t * ix.dim_stride, row, ix.dim);
+                    const float d = euclid_sq_vec4(qvs + t * ix.dim_stride, row, ix.dim, true);
                     if (d <= r2) {
                         const uint64_t q = q0 + t;
                         const uint32_t slot = atomicAdd(p.count + q, 1u);

@@ -38,7 +38,7 @@ CONFIGS = {
     # BASELINE.json configs[1] — the bench workload
     "c2": dict(workload="ivfpq_trim_knn_10M_d96_nlist4096_nprobe64", n=10_000_000, dim=96,
                n_centers=1024, sigma=0.3, nq=10_000, batch=1024, m=48, nlist=4096, nprobe=64,
-               k=10, gammas=[0.6, 0.8, 1.0], gamma=0.8),
+               k=10, gammas=[0.6, 0.8, 1.0], gamma=0.8, baseline_kprime=1000),
     # BASELINE.json configs[2]: flat range search, one calibrated radius
     "c3": dict(kind="range", workload="flat_trim_range_10M_d128", n=10_000_000, dim=128,
                n_centers=256, sigma=0.3, nq=10_000, batch=1024, m=32, nlist=1, nprobe=1, k=0,
@@ -428,6 +428,8 @@ def run_ours(args, cfg):
         out[f"recall@{k}"] = recall(arrays, queries, ids, k, args.recall_q, world)
     # e2e through the C-ABI host call with pinned host buffers
     out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
+    if cfg.get("baseline_kprime") and rank == 0 and world == 1:
+        out["baseline_ivfpq"] = baseline_line(gix, arrays, queries, cfg, args)
     if rank == 0 and world == 1 and not args.skip_cpu:
         out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
     if rank == 0:
@@ -495,6 +497,33 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
                 d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
                 api=f"trim_search_knn (C ABI, host buffers; pinned source; {max(1, args.streams)} client threads)",
                 shard_local=world > 1)
+
+
+def baseline_line(gix, arrays, queries, cfg, args):
+    """Config 2's comparison point: ivf::search_baseline_ivfpq (ivf.hpp:193-237,
+    ADC for every probed entry, refine pool k') through the C-ABI host call,
+    all queries, two client threads; QPS and recall@k alongside TRIM's."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2508_17828_b200 import ivf as G
+    nq, B, k, kp = cfg["nq"], cfg["batch"], cfg["k"], cfg["baseline_kprime"]
+    hq = queries.cpu().numpy()
+    pool = ThreadPoolExecutor(max(1, args.streams))
+    res = {}
+
+    def one(b):
+        ids, _, ct = G.search_baseline_ivfpq_batch(gix, hq[b:b + B], k, cfg["nprobe"], kp)
+        res[b] = ids
+        return int(ct[:, 3].sum())
+    sum(pool.map(one, range(0, min(nq, 2 * B), B)))  # warm-up
+    t0 = time.perf_counter()
+    ev = sum(pool.map(one, range(0, nq, B)))
+    sec = time.perf_counter() - t0
+    ids = np.concatenate([res[b] for b in range(0, nq, B)])
+    rec = recall(arrays, queries, torch.from_numpy(ids.view(np.int32)), k, args.recall_q, 1)
+    return dict(k_prime=kp, qps=nq / sec, cand_per_s=ev / sec, **{f"recall@{k}": rec},
+                api="trim_search_baseline_ivfpq (C ABI, host buffers)")
 
 
 def _host_index(arrays):

@@ -116,6 +116,62 @@ class ShardedIvfIndex:
                 return ids, d, cts
         self._search = searcher
 
+    def search_range(self, queries, radius, nprobe: int, gamma: float, range_searcher: Optional[Callable] = None,
+                     cap: int = 4096):
+        """Global range result: range search has no running
+        state (ivf.hpp:323-340), so the union of the shards' member sets is
+        exactly the single run's. Each rank's members (sorted slots) go through
+        an all-gather of the counts, then a padded all-gather of (dist, id)
+        keys, merged per query by (dist, id) (ivf.hpp:341).
+        range_searcher(queries, radius, nprobe, gamma, cap) -> (counts[nq],
+        ids[nq, cap], dist[nq, cap], counters[nq, 6]); default: the GPU path.
+        Returns (offsets[nq+1], ids, dist, summed counters[5])."""
+        import torch
+        import torch.distributed as dist
+
+        if range_searcher is None:
+            from .ivf import PruningProfile, search_trim_ivf_range_device
+
+            def range_searcher(q, r, npb, g, c):
+                cts = torch.zeros((q.shape[0], 6), dtype=torch.int64, device=q.device)
+                st = torch.zeros(1, dtype=torch.int32, device=q.device)
+                cnt, ids, d = search_trim_ivf_range_device(self.gpu, PruningProfile.manual(g), q, r, npb, cap=c,
+                                                           d_counters=cts, d_status=st)
+                if int(st.item()) & 1:
+                    raise RuntimeError("range result larger than cap")
+                return cnt, ids, d, cts
+        cnt, ids, d, cts = range_searcher(queries, radius, nprobe, gamma, cap)
+        nq = cnt.shape[0]
+        dev = cnt.device
+        mx = cnt.max().reshape(1).to(torch.int64) if nq else torch.zeros(1, dtype=torch.int64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.group)
+        w = max(1, int(mx.item()))
+        # (dist bits << 32 | id) sorts like (dist, id) for non-negative dist; padding sorts last
+        keys = torch.full((nq, w), -1, dtype=torch.int64, device=dev)
+        if nq:
+            j = torch.arange(w, device=dev).unsqueeze(0)
+            valid = j < cnt.unsqueeze(1).to(torch.int64)
+            kd = d[:, :w].contiguous().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            ki = ids[:, :w].to(torch.int64) & 0xFFFFFFFF
+            keys = torch.where(valid, (kd << 32) | ki, keys)
+        gk = torch.empty((self.world * nq, w), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(gk, keys.contiguous(), group=self.group)
+        gk = gk.view(self.world, nq, w).permute(1, 0, 2).reshape(nq, self.world * w)
+        gk = torch.where(gk < 0, torch.full_like(gk, torch.iinfo(torch.int64).max), gk)
+        gk, _ = torch.sort(gk, dim=1)
+        gcnt = torch.empty((self.world * nq,), dtype=cnt.dtype, device=dev)
+        dist.all_gather_into_tensor(gcnt, cnt.contiguous(), group=self.group)
+        tot = gcnt.view(self.world, nq).sum(0).to(torch.int64)
+        offs = torch.zeros(nq + 1, dtype=torch.int64, device=dev)
+        offs[1:] = torch.cumsum(tot, 0)
+        sel = torch.arange(self.world * w, device=dev).unsqueeze(0) < tot.unsqueeze(1)
+        flat = gk[sel]
+        out_ids = (flat & 0xFFFFFFFF).to(torch.int64)
+        out_d = ((flat >> 32) & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
+        c = cts[:, :5].sum(0)
+        dist.all_reduce(c, group=self.group)
+        return offs, out_ids, out_d, c
+
     def search_knn(self, queries, k: int, nprobe: int, gamma: float):
         """Global top-k over all shards + summed counters {dc, edc, pruned,
         evaluated, hops, coarse_dc (one rank's)}."""

@@ -164,3 +164,53 @@ def test_replicas_equal_single_run():
         np.testing.assert_array_equal(ids.view(np.uint32), want_ids)
         np.testing.assert_array_equal(d.view(np.uint32), want_d.view(np.uint32))
         np.testing.assert_array_equal(cts[:, :5], want_ct.astype(np.int64))
+
+
+def _range_worker(rank, port, results):
+    from oracle.oracle import COracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        ix, qs, _ = goldens.load("ivf_fixture")
+        full = IvfArrays.from_any(ix)
+        sh = shard_arrays(full, rank, WORLD)
+        hsh = host_index(sh)
+        hsh.vectors = np.ascontiguousarray(ix.vectors)  # global ids index the rows
+        co = COracle()
+
+        def rs(q, r, npb, g, cap):
+            offs, ids, d, ct, cdc = co.search_range(hsh, q.numpy(), r, npb, g)
+            nq = q.shape[0]
+            cnt = np.diff(offs.astype(np.int64))
+            I = np.zeros((nq, cap), np.int32)
+            D = np.zeros((nq, cap), np.float32)
+            for i in range(nq):
+                I[i, :cnt[i]] = ids[offs[i]:offs[i + 1]].view(np.int32)
+                D[i, :cnt[i]] = d[offs[i]:offs[i + 1]]
+            c6 = np.concatenate([ct.astype(np.int64), cdc.astype(np.int64)[:, None]], 1)
+            return (torch.from_numpy(cnt.astype(np.int32)), torch.from_numpy(I), torch.from_numpy(D),
+                    torch.from_numpy(c6))
+        shd = ShardedIvfIndex(sh, searcher=lambda *a: None, merge=np_merge)
+        offs, ids, d, c = shd.search_range(torch.from_numpy(qs), 3.0, 12, 0.35, range_searcher=rs, cap=512)
+        results[rank] = (offs.numpy().copy(), ids.numpy().copy(), d.numpy().copy(), c.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_range_equals_single_run():
+    """Range search is order-free: the merged shards equal the global run."""
+    from oracle.oracle import COracle
+    ix, qs, _ = goldens.load("ivf_fixture")
+    h = host_index(IvfArrays.from_any(ix))
+    offs, ids, d, ct, _ = COracle().search_range(h, qs, 3.0, 12, 0.35)
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_range_worker, args=(_free_port(), results), nprocs=WORLD, join=True)
+    for r in range(WORLD):
+        go, gi, gd, gc = results[r]
+        np.testing.assert_array_equal(go, offs.astype(np.int64))
+        np.testing.assert_array_equal(gi.astype(np.uint32), ids)
+        np.testing.assert_array_equal(gd.view(np.uint32), d.view(np.uint32))
+        # evaluated/dc/pruned sum over shards; edc = evaluated for range
+        np.testing.assert_array_equal(gc[[0, 2, 3]], ct.sum(0)[[0, 2, 3]].astype(np.int64))

@@ -1,6 +1,7 @@
 """GPU side of the multi-GPU path: the device merge kernel after the
 all-gather (trim_merge_topk_device) against a plain sort by (dist, id), and
-ShardedIvfIndex over a 1-rank NCCL group equal to the single-GPU search."""
+ShardedIvfIndex (kNN and range) over a 1-rank NCCL group equal to the
+single-GPU search."""
 import os
 import socket
 
@@ -52,5 +53,17 @@ def test_sharded_index_one_rank_nccl():
         np.testing.assert_array_equal(mi.cpu().numpy().view(np.uint32), ids)
         np.testing.assert_array_equal(md.cpu().numpy().view(np.uint32), d.view(np.uint32))
         np.testing.assert_array_equal(c.cpu().numpy(), ct[:, :5].sum(0).astype(np.int64))
+        # range through the padded all-gather + merge (device range API per rank)
+        ix2, qs2, _ = goldens.load("ivf_fixture")
+        full2 = G.IvfArrays.from_any(ix2)
+        sh2 = ShardedIvfIndex(shard_arrays(full2, 0, 1))
+        q2 = torch.from_numpy(np.ascontiguousarray(qs2)).cuda()
+        r = torch.full((q2.shape[0],), 3.0, dtype=torch.float32, device="cuda")
+        offs, rid, rd, rc = sh2.search_range(q2, r, 12, 0.35)
+        wo, wi, wd, wct = G.search_trim_ivf_range_batch(G.GpuIvfIndex(full2), G.PruningProfile.manual(0.35), qs2,
+                                                        3.0, 12)
+        np.testing.assert_array_equal(offs.cpu().numpy(), wo.astype(np.int64))
+        np.testing.assert_array_equal(rid.cpu().numpy().astype(np.uint32), wi)
+        np.testing.assert_array_equal(rd.cpu().numpy().view(np.uint32), wd.view(np.uint32))
     finally:
         dist.destroy_process_group()

@@ -846,7 +846,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--recall-q", type=int, default=200)
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=3,
                     help="streams that consecutive batches alternate between (1 = serial)")
     ap.add_argument("--parallel", default="shard", choices=["shard", "replicas"],
                     help="N>1 layout: id-sharded index (weak scaling, all-gather merge) or replicas "

@@ -47,6 +47,10 @@ CONFIGS = {
     "c4": dict(workload="flat_trim_knn_1M_d960_k100", n=1_000_000, dim=960, data="uniform_normalized",
                n_centers=0, sigma=0.0, nq=1000, batch=1000, m=120, nlist=1, nprobe=1, k=100,
                gammas=[0.5, 0.7, 0.9], gamma=0.9),
+    # BASELINE.json configs[4]: billion-scale sharded flat scan, 100M rows per GPU (weak
+    # scaling: --gpus 8 is the 800M configuration), batches of 2048
+    "c5": dict(workload="flat_trim_knn_100M_per_gpu_d96", n=100_000_000, dim=96, n_centers=4096, sigma=0.3,
+               nq=10_000, batch=2048, m=48, nlist=1, nprobe=1, k=10, gammas=[0.8], gamma=0.8),
     # BASELINE.json configs[0] (CPU-runnable reference case; parity + extra line)
     "c1": dict(workload="flat_trim_knn_100k_d128", n=100_000, dim=128, n_centers=64, sigma=0.3,
                nq=1000, batch=1000, m=16, nlist=1, nprobe=1, k=10, gammas=[0.0, 0.605, 1.0],
@@ -401,7 +405,7 @@ def run_ours(args, cfg):
     # code/lx: the kernel's algorithmic bytes count only the positions it scans
     skipped_all = skipped * (world if world > 1 else 1)
     scanned = evaluated - skipped_all
-    flat_bounds = cfg["nlist"] == 1 and os.environ.get("TRIM_FLAT_BOUNDS") != "0"
+    flat_bounds = cfg["nlist"] == 1 and cfg["n"] <= (16 << 20) and os.environ.get("TRIM_FLAT_BOUNDS") != "0"
     if flat_bounds:
         # flat scans read D~[q][row] (4 B) for evaluated candidates; exact rows only
         # for the few members that can enter the top-k (not counted)

@@ -511,8 +511,9 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     }
     // flat scans: tensor-core distance bounds for every (query, row), so only
     // members that can enter the top-k get the exact distance
-    const bool flat_bounds = ix->dev.nlist == 1 && np == 1 && ix->dev.n > 0 && flat_bounds_enabled() &&
-                             ensure_flat_tiles(const_cast<trim_index*>(ix));
+    // (up to 16M rows: D~ holds nq x rows floats and the pre-tiled rows another copy of the vectors)
+    const bool flat_bounds = ix->dev.nlist == 1 && np == 1 && ix->dev.n > 0 && ix->dev.n <= (16ull << 20) &&
+                             flat_bounds_enabled() && ensure_flat_tiles(const_cast<trim_index*>(ix));
     const uint64_t ld = flat_bounds ? (ix->dev.n + kMmaN - 1) / kMmaN * kMmaN : 0;
     // slices: grid.x <= 2^31-1; with bounds, D~ of a slice (nq x ld floats) within ~8 GB
     uint64_t slice = 1u << 30;

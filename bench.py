@@ -369,7 +369,7 @@ def run_ours(args, cfg):
                              qps=nq * max(1, min(2, args.steps)) / (ms / 1e3),
                              prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])))
         if rank == 0:
-            sweep[str(g)][f"recall@{k}"] = recall(arrays, queries, ids, k, args.recall_q, world)
+            sweep[str(g)][f"recall@{k}"] = recall(gix, queries, ids, k, args.recall_q, world)
     clk = ClockSampler(local)
     for _ in range(args.warmup):
         step(head)
@@ -429,7 +429,7 @@ def run_ours(args, cfg):
     out["clocks"] = clk.summary()
     out["sweep"] = sweep
     if rank == 0:
-        out[f"recall@{k}"] = recall(arrays, queries, ids, k, args.recall_q, world)
+        out[f"recall@{k}"] = recall(gix, queries, ids, k, args.recall_q, world)
     # e2e through the C-ABI host call with pinned host buffers
     out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
     if cfg.get("baseline_kprime") and rank == 0 and world == 1:
@@ -450,21 +450,18 @@ class _Null:
         return False
 
 
-def recall(arrays, queries, ids, k, nsample, world):
-    """recall@k (bench::recall_at_k, metrics.hpp:14-24) of the local shard's
-    results vs an fp32 brute force (torch) on `nsample` queries. Informational."""
+def recall(gix, queries, ids, k, nsample, world):
+    """bench::recall_at_k (bench/metrics.hpp:14-24), averaged over `nsample`
+    queries, against the exact ground truth computed on the GPU bit-identically
+    to core/ground_truth.hpp (trim_ground_truth_knn). Informational; the local
+    shard's results at N > 1 are not comparable (None)."""
     if world > 1 or nsample <= 0:
         return None
-    import torch
-    x = arrays.vectors
-    q = queries[:nsample]
-    best = []
-    for i in range(0, q.shape[0], 16):
-        d = torch.cdist(q[i:i + 16], x)
-        best.append(torch.topk(d, k, largest=False).indices)
-    gt = torch.cat(best).cpu().numpy()
+    from paper_2508_17828_b200 import ivf as G
+    q = queries[:nsample].cpu().numpy()
+    gt, _ = G.ground_truth_knn(gix, q, k)
     got = ids[:nsample].cpu().numpy().view(np.uint32)
-    hits = sum(len(set(gt[i].tolist()) & set(got[i].tolist())) for i in range(len(gt)))
+    hits = sum(len(set(gt[i].tolist()) & set(got[i, :k].tolist())) for i in range(len(gt)))
     return hits / (k * len(gt))
 
 
@@ -525,7 +522,7 @@ def baseline_line(gix, arrays, queries, cfg, args):
     ev = sum(pool.map(one, range(0, nq, B)))
     sec = time.perf_counter() - t0
     ids = np.concatenate([res[b] for b in range(0, nq, B)])
-    rec = recall(arrays, queries, torch.from_numpy(ids.view(np.int32)), k, args.recall_q, 1)
+    rec = recall(gix, queries, torch.from_numpy(ids.view(np.int32)), k, args.recall_q, 1)
     return dict(k_prime=kp, qps=nq / sec, cand_per_s=ev / sec, **{f"recall@{k}": rec},
                 api="trim_search_baseline_ivfpq (C ABI, host buffers)")
 

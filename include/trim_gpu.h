@@ -190,6 +190,13 @@ int trim_search_range_device(trim_index_t index, const float* d_queries, uint64_
                              uint32_t* d_counts, uint32_t* d_ids, float* d_dist,
                              trim_counters* d_counters, uint32_t* d_status, void* stream);
 
+/* core/ground_truth.hpp ground_truth_knn (:97-113, brute_force_knn :53-74): the
+ * exact k nearest rows of every query over the index's vectors, ascending by
+ * (dist_sq, id), bit-identical to the reference (fp32 4-accumulator distances).
+ * queries nq*dim (host); ids_out/dist_out nq*k (host). 1 <= k <= min(n, 4096). */
+int trim_ground_truth_knn(trim_index_t index, const float* queries, uint64_t nq, uint32_t k,
+                          uint32_t* ids_out, float* dist_out);
+
 /* pq::build_distance_table (pq/pq.hpp:158-172) for nq queries: lut_out is
  * nq*m*ksub floats (host), j-major like DistanceTable::entries. */
 int trim_build_lut(trim_index_t index, const float* queries, uint64_t nq, float* lut_out);

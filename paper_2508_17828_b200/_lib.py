@@ -74,6 +74,7 @@ SIGNATURES = {
     "trim_search_range_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
                                             C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p, C.c_void_p]),
+    "trim_ground_truth_knn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
     "trim_search_knn_preassigned_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                                      C.c_void_p, C.c_uint32, C.c_float, C.c_void_p,
                                                      C.c_void_p, C.c_void_p, C.c_void_p,

@@ -467,6 +467,18 @@ bool ensure_flat_tiles(trim_index* ix) {
     return true;
 }
 
+// D~ for nq queries (tiled) x every row, row tiles in launches of <= 65535 (grid.y).
+void launch_flat_dist(const float4* qtiles, const float* qn2, uint64_t nq, uint64_t nqt, const trim_index* ix,
+                      uint32_t K, float* dap, uint64_t ld, uint64_t nrt, cudaStream_t st) {
+    for (uint64_t r0 = 0; r0 < nrt; r0 += 65535) {
+        const uint64_t ny = std::min<uint64_t>(65535, nrt - r0);
+        trim_flat_dist_kernel<<<dim3(static_cast<unsigned>(nqt), static_cast<unsigned>(ny)), kMmaThreads,
+                                flat_mma_smem(), st>>>(qtiles, qn2, nq, ix->flat_tiles, ix->xn2, ix->dev.n, K, dap, ld,
+                                                       r0);
+        CK(cudaGetLastError());
+    }
+}
+
 // kNN filter launch over padded device queries and precomputed probe lists
 // (d_probe null => nlist == 1, the single list 0).
 int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t np,
@@ -538,10 +550,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
             dap = DevBuf(sizeof(float) * pb.nq * ld, st);
             CK(cudaFuncSetAttribute(trim_flat_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(flat_mma_smem())));
-            trim_flat_dist_kernel<<<dim3(static_cast<unsigned>(nqt), static_cast<unsigned>(nrt)), kMmaThreads,
-                                    flat_mma_smem(), st>>>(qtiles.as<float4>(), qn2.as<float>(), pb.nq,
-                                                           ix->flat_tiles, ix->xn2, v.n, K, dap.as<float>(), ld);
-            CK(cudaGetLastError());
+            launch_flat_dist(qtiles.as<float4>(), qn2.as<float>(), pb.nq, nqt, ix, K, dap.as<float>(), ld, nrt, st);
             pb.dap = dap.as<float>();
             pb.dap_ld = ld;
             pb.xnorm = ix->xn;
@@ -1159,6 +1168,53 @@ int trim_search_range_device(trim_index_t ix, const float* d_queries, uint64_t n
             d_eval.as<unsigned long long>(), nq, cap, ix->dev.nlist, d_counts, d_ids, d_dist,
             reinterpret_cast<unsigned long long*>(d_counters));
         CK(cudaGetLastError());
+        return TRIM_OK;
+    });
+}
+
+int trim_ground_truth_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t k, uint32_t* ids_out,
+                          float* dist_out) {
+    if (!ix || (nq && (!queries || !ids_out || !dist_out)))
+        return set_err(TRIM_EINVAL, "ground_truth_knn: null argument");
+    if (k == 0 || k > ix->dev.n)
+        return set_err(TRIM_EINVAL, "brute_force_knn: k out of range");
+    if (k > kGtCap)
+        return set_err(TRIM_EINVAL, "ground_truth_knn: k > 4096 is not supported by the GPU selection");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(ix->device);
+        cudaStream_t st = thread_stream(ix->device);
+        ensure_flat_tiles(ix);
+        const DevIndex& v = ix->dev;
+        DevBuf d_q = upload_queries(ix, queries, nq, cudaMemcpyHostToDevice, st);
+        const uint32_t K = flat_kpad(v.dim);
+        const uint64_t ld = (v.n + kMmaN - 1) / kMmaN * kMmaN, nrt = ld / kMmaN;
+        const uint64_t slice = std::max<uint64_t>(kMmaM, (4ull << 30) / (ld * 4) / kMmaM * kMmaM);
+        DevBuf d_ids(sizeof(uint32_t) * nq * k, st), d_dist(sizeof(float) * nq * k, st);
+        CK(cudaFuncSetAttribute(trim_flat_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(flat_mma_smem())));
+        CK(cudaFuncSetAttribute(trim_gt_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(gt_smem(v.dim_stride))));
+        for (uint64_t b = 0; b < nq; b += slice) {
+            const uint64_t nb = std::min<uint64_t>(slice, nq - b);
+            const uint64_t nqt = (nb + kMmaM - 1) / kMmaM;
+            const float* qb = d_q.as<float>() + b * v.dim_stride;
+            DevBuf qtiles(sizeof(float4) * nqt * (K / kFlatKB) * 8 * kMmaM, st), qn2(sizeof(float) * nb, st);
+            trim_flat_tile_kernel<<<static_cast<unsigned>(nqt), kThreads, 0, st>>>(qb, nb, v.dim_stride, v.dim, K,
+                                                                                   qtiles.as<float4>());
+            trim_query_norm_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(qb, nb, v.dim_stride,
+                                                                                            v.dim, qn2.as<float>());
+            DevBuf dap(sizeof(float) * nb * ld, st), scratch(sizeof(float) * nb * ld, st);
+            launch_flat_dist(qtiles.as<float4>(), qn2.as<float>(), nb, nqt, ix, K, dap.as<float>(), ld, nrt, st);
+            trim_gt_select_kernel<<<static_cast<unsigned>(nb), kGtThreads, gt_smem(v.dim_stride), st>>>(
+                v, qb, nb, k, dap.as<float>(), ld, ix->xn, ix->xn2, scratch.as<float>(), d_ids.as<uint32_t>() + b * k,
+                d_dist.as<float>() + b * k);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(uint32_t) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(dist_out, d_dist.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         return TRIM_OK;
     });
 }

@@ -77,10 +77,10 @@ __global__ void trim_row_norm_kernel(const float* __restrict__ rows, uint64_t nr
 __global__ void __launch_bounds__(kMmaThreads, 2)
 trim_flat_dist_kernel(const float4* __restrict__ qtiles, const float* __restrict__ qn2, uint64_t nq,
                       const float4* __restrict__ rtiles, const float* __restrict__ xn2, uint64_t nrows, uint32_t kpad,
-                      float* __restrict__ dap, uint64_t ld) {
+                      float* __restrict__ dap, uint64_t ld, uint64_t rt0) {
     extern __shared__ __align__(128) unsigned char fm_smem[];
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    const uint64_t qt = blockIdx.x, rt = blockIdx.y;
+    const uint64_t qt = blockIdx.x, rt = rt0 + blockIdx.y; // row tiles launched in groups of <= 65535
     const uint32_t nkb = kpad / kFlatKB;
     const size_t tile_f4 = static_cast<size_t>(nkb) * 8 * kMmaM;
     unsigned char* sA = fm_smem;                                   // [stages][16 KB]
@@ -183,6 +183,212 @@ __global__ void trim_query_norm_kernel(const float* __restrict__ q, uint64_t nq,
     for (uint32_t j = 0; j < dim; ++j)
         s += static_cast<double>(q[i * stride + j]) * q[i * stride + j];
     n2[i] = static_cast<float>(s);
+}
+
+} // namespace trimgpu
+
+namespace trimgpu {
+
+// --------------------------------------------------------------------------
+// Exact brute-force ground truth (core/ground_truth.hpp:53-74, 97-113): the k
+// smallest (euclidean_sq, id) over every row, in the reference's fp32
+// 4-accumulator arithmetic, from the tensor-core bounds D~ +- E: one CTA per
+// query takes tau >= the k-th smallest upper bound (two 11-bit radix passes
+// over the row keys in global memory), keeps the rows whose lower bound is <=
+// tau (the true k nearest are among them), computes their exact distances and
+// sorts by (d, id). More than kGtCap survivors (massive ties) fall back to
+// exact distances for every row.
+// --------------------------------------------------------------------------
+constexpr uint32_t kGtCap = 4096;
+constexpr uint32_t kGtThreads = 256;
+
+__host__ __device__ inline size_t gt_smem(uint32_t dim_stride) {
+    return sizeof(uint64_t) * kGtCap + sizeof(uint32_t) * 2048 + sizeof(float) * dim_stride + 64;
+}
+
+__device__ __forceinline__ float gt_err(float qn, float qn2, float xn, float xn2) {
+    return __fadd_ru(__fmul_ru(__fmul_ru(qn, xn), 1.0f / 128.0f), __fmul_ru(__fadd_ru(qn2, xn2), 1.0f / 16384.0f));
+}
+
+// Radix select over keys produced by key_of(row) for rows [0, n): the prefix
+// after `passes` 11/11/10-bit passes of the rank-th smallest key.
+template <typename KeyFn>
+__device__ uint32_t gt_radix(uint64_t n, uint32_t rank, uint32_t* hist, uint32_t* sc, int passes, KeyFn key_of) {
+    const uint32_t tid = threadIdx.x;
+    uint32_t prefix = 0, pmask = 0;
+    for (int p = 0; p < passes; ++p) {
+        const uint32_t shift = p == 0 ? 21u : (p == 1 ? 10u : 0u);
+        const uint32_t nb = p < 2 ? 2048u : 1024u;
+        for (uint32_t i = tid; i < nb; i += kGtThreads)
+            hist[i] = 0;
+        __syncthreads();
+        for (uint64_t r = tid; r < n; r += kGtThreads) {
+            const uint32_t kk = key_of(r);
+            if ((kk & pmask) == prefix)
+                atomicAdd(&hist[(kk >> shift) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        const uint32_t per = nb / kGtThreads;
+        uint32_t s = 0;
+        for (uint32_t i = 0; i < per; ++i)
+            s += hist[tid * per + i];
+        uint32_t tot;
+        const uint32_t excl = block_excl_scan(s, sc + 8, &tot);
+        if (excl < rank && rank <= excl + s) {
+            uint32_t cum = excl;
+            for (uint32_t i = 0; i < per; ++i) {
+                const uint32_t h = hist[tid * per + i];
+                if (cum + h >= rank) {
+                    sc[0] = tid * per + i;
+                    sc[1] = cum;
+                    break;
+                }
+                cum += h;
+            }
+        }
+        __syncthreads();
+        prefix |= sc[0] << shift;
+        pmask |= (nb - 1) << shift;
+        rank -= sc[1];
+        __syncthreads();
+    }
+    return prefix;
+}
+
+__global__ void __launch_bounds__(kGtThreads)
+trim_gt_select_kernel(DevIndex ix, const float* __restrict__ queries, uint64_t nq, uint32_t k,
+                      const float* __restrict__ dap, uint64_t ld, const float* __restrict__ xn,
+                      const float* __restrict__ xn2, float* __restrict__ scratch, uint32_t* __restrict__ ids_out,
+                      float* __restrict__ dist_out) {
+    extern __shared__ __align__(16) unsigned char gs_smem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    if (q >= nq)
+        return;
+    const uint64_t n = ix.n;
+    uint64_t* sq = reinterpret_cast<uint64_t*>(gs_smem);          // [kGtCap]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sq + kGtCap);     // [2048]
+    float* qv = reinterpret_cast<float*>(hist + 2048);             // [dim_stride]
+    uint32_t* sc = reinterpret_cast<uint32_t*>(qv + ix.dim_stride); // [16]
+    const float* qrow = queries + q * ix.dim_stride;
+    const float* arow = dap + q * ld;
+    float qp = 0.0f;
+    for (uint32_t i = tid; i < ix.dim_stride; i += kGtThreads) {
+        const float x = qrow[i];
+        qv[i] = x;
+        qp = __fadd_ru(qp, __fmul_ru(x, x));
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        qp = __fadd_ru(qp, __shfl_xor_sync(0xffffffffu, qp, o));
+    if (lane == 0)
+        hist[warp] = __float_as_uint(qp);
+    __syncthreads();
+    float qn2 = 0.0f;
+    for (uint32_t w = 0; w < kGtThreads / 32; ++w)
+        qn2 = __fadd_ru(qn2, __uint_as_float(hist[w]));
+    qn2 = __fmul_ru(qn2, 1.0f + 1.0f / 65536.0f);
+    const float qn = __fsqrt_ru(qn2);
+    __syncthreads();
+    auto ukey = [&](uint64_t r) { return f2key(__fadd_ru(arow[r], gt_err(qn, qn2, __ldg(xn + r), __ldg(xn2 + r)))); };
+    const float tau = key2f(gt_radix(n, k, hist, sc, 2, ukey) | 0x3FFu);
+    if (tid == 0)
+        sc[2] = 0;
+    __syncthreads();
+    for (uint64_t r = tid; r < n; r += kGtThreads)
+        if (__fsub_rd(arow[r], gt_err(qn, qn2, __ldg(xn + r), __ldg(xn2 + r))) <= tau) {
+            const uint32_t slot = atomicAdd(&sc[2], 1u);
+            if (slot < kGtCap)
+                sq[slot] = r;
+        }
+    __syncthreads();
+    const uint32_t ncand = sc[2];
+    uint32_t* io = ids_out + q * k;
+    float* dout = dist_out + q * k;
+    if (ncand <= kGtCap) {
+        uint32_t n2 = 1;
+        while (n2 < ncand)
+            n2 <<= 1;
+        for (uint32_t i = tid; i < n2; i += kGtThreads) {
+            uint64_t kk = ~0ull;
+            if (i < ncand) {
+                const uint64_t r = sq[i];
+                const float d = euclid_sq_vec4(qv, ix.vectors + r * ix.dim_stride, ix.dim);
+                kk = (static_cast<uint64_t>(__float_as_uint(d)) << 32) | static_cast<uint32_t>(ix.id_base + r);
+            }
+            sq[i] = kk;
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= n2; size <<= 1)
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = tid; i < n2 / 2; i += kGtThreads) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint64_t a = sq[lo], b = sq[hi];
+                    if ((a > b) == up) {
+                        sq[lo] = b;
+                        sq[hi] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        for (uint32_t i = tid; i < k; i += kGtThreads) {
+            io[i] = static_cast<uint32_t>(sq[i] & 0xffffffffu);
+            dout[i] = __uint_as_float(static_cast<uint32_t>(sq[i] >> 32));
+        }
+        return;
+    }
+    // massive ties: exact distances of every row (into scratch), exact selection
+    float* ex = scratch + q * ld;
+    for (uint64_t r = tid; r < n; r += kGtThreads)
+        ex[r] = euclid_sq_vec4(qv, ix.vectors + r * ix.dim_stride, ix.dim);
+    __syncthreads();
+    auto ekey = [&](uint64_t r) { return __float_as_uint(ex[r]); };
+    const uint32_t kth = gt_radix(n, k, hist, sc, 3, ekey);
+    if (tid == 0)
+        sc[2] = 0;
+    __syncthreads();
+    for (uint64_t r = tid; r < n; r += kGtThreads) // rows below the k-th distance: fewer than k
+        if (__float_as_uint(ex[r]) < kth)
+            sq[atomicAdd(&sc[2], 1u)] = (static_cast<uint64_t>(__float_as_uint(ex[r])) << 32) |
+                                        static_cast<uint32_t>(ix.id_base + r);
+    __syncthreads();
+    const uint32_t n_lt = sc[2];
+    if (warp == 0) { // ties at the k-th distance: the lowest ids, in order
+        uint32_t n_eq = 0;
+        const uint32_t need = k - n_lt;
+        for (uint64_t r0 = 0; r0 < n && n_eq < need; r0 += 32) {
+            const uint64_t r = r0 + lane;
+            const bool eq = r < n && __float_as_uint(ex[r]) == kth;
+            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+            const uint32_t rr = n_eq + __popc(beq & ((1u << lane) - 1u));
+            if (eq && rr < need)
+                sq[n_lt + rr] = (static_cast<uint64_t>(kth) << 32) | static_cast<uint32_t>(ix.id_base + r);
+            n_eq += __popc(beq);
+        }
+    }
+    uint32_t n2 = 1;
+    while (n2 < k)
+        n2 <<= 1;
+    for (uint32_t i = k + tid; i < n2; i += kGtThreads)
+        sq[i] = ~0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= n2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < n2 / 2; i += kGtThreads) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = sq[lo], b = sq[hi];
+                if ((a > b) == up) {
+                    sq[lo] = b;
+                    sq[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = tid; i < k; i += kGtThreads) {
+        io[i] = static_cast<uint32_t>(sq[i] & 0xffffffffu);
+        dout[i] = __uint_as_float(static_cast<uint32_t>(sq[i] >> 32));
+    }
 }
 
 } // namespace trimgpu

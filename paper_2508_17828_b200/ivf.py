@@ -356,3 +356,16 @@ def search_trim_ivf_range_device(ix: GpuIvfIndex, profile: PruningProfile, d_que
         C.c_void_p(d_status.data_ptr()) if d_status is not None else None, C.c_void_p(sh))
     _lib.check(rc, "search_trim_ivf_range")
     return counts, ids, dist
+
+
+def ground_truth_knn(ix: GpuIvfIndex, queries, k: int):
+    """core/ground_truth.hpp ground_truth_knn: exact k nearest rows of every
+    query, ascending by (dist_sq, id), bit-identical to the reference
+    (trim_ground_truth_knn). Returns (ids[nq, k] u32, dist_sq[nq, k] f32)."""
+    q = _queries(ix, queries)
+    nq = q.shape[0]
+    ids = np.zeros((nq, k), np.uint32)
+    dist = np.zeros((nq, k), np.float32)
+    _lib.check(_lib.load().trim_ground_truth_knn(ix.handle, _addr(q), nq, k, _addr(ids), _addr(dist)),
+               "ground_truth_knn")
+    return ids, dist

@@ -726,7 +726,11 @@ def run_ours_range(args, cfg):
                              prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])),
                              mean_result_size=float(counts.double().mean()))
     clk = ClockSampler(local)
-    ms, busy, nl, ct, launches = timed(head, args.steps, args.warmup, clk)
+    for _ in range(args.warmup):
+        step(head)
+    gix.skipped_positions(reset=True)  # (synchronises; outside the timed region)
+    ms, busy, nl, ct, launches = timed(head, args.steps, 0, clk)
+    skipped = gix.skipped_positions() / args.steps  # rows pruned as whole blocks, per step
     assert int(status.item()) & 1 == 0, "range result larger than cap"
     evaluated, dc = float(ct[3]), float(ct[0])
     value = evaluated * args.steps / (ms / 1e3)
@@ -745,12 +749,17 @@ def run_ours_range(args, cfg):
     qt = gix.info()["range_query_tile"]
     peak, peak_src = measured_peaks()
     m, D = cfg["m"], cfg["dim"]
-    # the flat scan streams codes + lx once per query tile; survivors read their row
-    alg = (nq + qt - 1) // qt * cfg["n"] * (m + 4) + dc * (4 * D + 4)
+    if skipped > 0:  # block partition: only the kept blocks' rows are scanned (codes + lx)
+        qt = 1
+        alg = (evaluated - skipped) * (m + 4) + dc * (4 * D + 4)
+    else:  # the query-tiled flat scan streams codes + lx once per query tile
+        alg = (nq + qt - 1) // qt * cfg["n"] * (m + 4) + dc * (4 * D + 4)
     achieved = alg / (busy / args.steps / 1e3) / 1e9
     out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                           traffic=ncu_traffic(cfg["workload"]), kernel="trim_range_flat_kernel",
+                           traffic=ncu_traffic(cfg["workload"]),
+                           kernel="trim_range_kernel (block partition)" if skipped > 0 else "trim_range_flat_kernel",
                            bytes_per_step=alg, query_tile=qt, peak_source=peak_src,
+                           block_skip_fraction=skipped / max(1.0, evaluated),
                            pair_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4)) / (busy / args.steps / 1e3) / 1e9)
     out["gpu_launches"] = launches
     out["clocks"] = clk.summary()

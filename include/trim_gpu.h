@@ -114,7 +114,8 @@ int trim_index_create(const trim_index_desc* desc, trim_index_t* out);
 int trim_index_destroy(trim_index_t index);
 int trim_index_get_info(trim_index_t index, trim_index_info* info);
 /* Diagnostic (no reference equivalent): stream positions the kNN kernel pruned
- * as whole lists by the list-level bound since creation or the last reset
+ * as whole lists by the list-level bound (and, for flat range search, rows
+ * pruned as whole blocks of the block partition) since creation or the last reset
  * (they are counted as pruned in trim_counters, exactly as the reference
  * prunes them one by one). Synchronises the index's device. */
 int trim_index_skip_stats(trim_index_t index, uint64_t* skipped_positions, int reset);

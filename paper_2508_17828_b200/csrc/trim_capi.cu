@@ -132,6 +132,14 @@ struct trim_index {
     float4* flat_tiles = nullptr;
     float* xn = nullptr;
     float* xn2 = nullptr;
+    // flat range search: a block partition of the rows (build_flat_partition), built on first use
+    std::mutex part_mu;
+    bool part_tried = false;
+    uint32_t part_nb = 0;
+    DevIndex part{};
+    float4* part_tiles = nullptr;
+    float* part_cn2 = nullptr;
+    float* part_cn = nullptr;
     uint64_t bytes = 0;
     std::vector<void*> allocs;
 
@@ -364,6 +372,114 @@ DevBuf upload_queries(const trim_index* ix, const float* q, uint64_t nq, cudaMem
     return d;
 }
 
+// TRIM_FLAT_PARTITION=0 keeps flat range scans in row order (A/B; results and
+// counters are identical either way).
+bool flat_partition_enabled() {
+    const char* e = std::getenv("TRIM_FLAT_PARTITION");
+    return !(e && e[0] == '0');
+}
+
+// Block partition for flat range search: k-means centroids of a row sample,
+// every row assigned to its (tf32-bound) nearest block, the entries regrouped
+// by block (ascending ids inside a block), per-block R / lx range for the
+// list-level bound, tcgen05 probe tiles of the block centroids. Any partition is
+// valid (the bounds use the actual members); the range filter is order-free,
+// so the members and counters are the reference's. Built once, on first use.
+bool ensure_flat_partition(trim_index* ix) {
+    std::lock_guard<std::mutex> lk(ix->part_mu);
+    if (ix->part_tried)
+        return ix->part_nb > 0;
+    ix->part_tried = true;
+    const DevIndex& v = ix->dev;
+    const uint64_t n = ix->total;
+    uint64_t min_rows = 1u << 18; // TRIM_FLAT_PARTITION_MIN_ROWS: tests partition small indexes
+    if (const char* e = std::getenv("TRIM_FLAT_PARTITION_MIN_ROWS"))
+        min_rows = std::strtoull(e, nullptr, 10);
+    if (!flat_partition_enabled() || v.nlist != 1 || v.dim_stride != v.dim || mma_k(v.dim) > kMmaMaxK ||
+        n < std::max<uint64_t>(min_rows, 1024) || n != v.n)
+        return false;
+    cudaStream_t st = nullptr;
+    {
+        DevBuf bad(sizeof(uint32_t), st);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(uint32_t), st));
+        trim_identity_check_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(v.list_ids, n, v.id_base,
+                                                                                         bad.as<uint32_t>());
+        uint32_t hb = 0;
+        CK(cudaMemcpyAsync(&hb, bad.p, sizeof hb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hb)
+            return false;
+    }
+    uint32_t nb = 256;
+    while (nb < 4096 && uint64_t(nb) * 2 * 2048 <= n)
+        nb *= 2;
+    // k-means on a row sample (the reference's Fisher-Yates sampler)
+    const uint64_t ns = std::min<uint64_t>(n, uint64_t(nb) * 40);
+    std::vector<uint64_t> rows(ns);
+    if (int rc = trim_sample_rows(n, ns, 0x5EED5EEDull, rows.data()))
+        throw std::runtime_error(trim_last_error());
+    DevBuf d_rows(sizeof(uint64_t) * ns, st), d_sample(sizeof(float) * ns * v.dim, st);
+    CK(cudaMemcpyAsync(d_rows.p, rows.data(), sizeof(uint64_t) * ns, cudaMemcpyHostToDevice, st));
+    trim_gather_rows_kernel<<<static_cast<unsigned>(ns), 128, 0, st>>>(v.vectors, v.dim_stride, d_rows.as<uint64_t>(),
+                                                                       ns, v.dim, d_sample.as<float>());
+    CK(cudaStreamSynchronize(st));
+    float* cent = ix->alloc<float>(static_cast<size_t>(nb) * v.dim);
+    if (int rc = trim_kmeans_device(d_sample.as<float>(), ns, v.dim, nb, 6, 0x5EEDull, cent, ix->device))
+        throw std::runtime_error(trim_last_error());
+    DevIndex a = v;
+    a.nlist = nb;
+    a.coarse = cent; // dim_stride == dim
+    const uint32_t K = mma_k(v.dim);
+    const uint32_t ntiles = (nb + kMmaN - 1) / kMmaN;
+    ix->part_tiles = ix->alloc<float4>(static_cast<size_t>(ntiles) * (K / 4) * kMmaN);
+    ix->part_cn2 = ix->alloc<float>(nb);
+    ix->part_cn = ix->alloc<float>(nb);
+    trim_coarse_tile_kernel<<<ntiles, kThreads, 0, st>>>(a, K, ix->part_tiles);
+    trim_coarse_norm_kernel<<<(nb + kThreads - 1) / kThreads, kThreads, 0, st>>>(a, ix->part_cn2, ix->part_cn);
+    CK(cudaGetLastError());
+    // assignment: argmin of the tf32 distance bounds, row chunks of 1M
+    DevBuf assign(sizeof(uint32_t) * n, st);
+    const uint64_t ch = 1u << 20, ld = mma_ld(nb);
+    DevBuf approx(sizeof(float) * ch * ld, st);
+    CK(cudaFuncSetAttribute(trim_probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(probe_mma_smem(K))));
+    for (uint64_t c0 = 0; c0 < n; c0 += ch) {
+        const uint64_t nc = std::min<uint64_t>(ch, n - c0);
+        const dim3 grid(static_cast<unsigned>((nc + kMmaM - 1) / kMmaM), (ntiles + kMmaTilesPerCta - 1) / kMmaTilesPerCta);
+        trim_probe_mma_kernel<<<grid, kMmaThreads, probe_mma_smem(K), st>>>(
+            v.vectors + c0 * v.dim_stride, nc, v.dim_stride, K, ix->part_tiles, ix->part_cn2, nb, approx.as<float>());
+        trim_argmin_kernel<<<static_cast<unsigned>((nc + 7) / 8), 256, 0, st>>>(approx.as<float>(), nc, nb, ld,
+                                                                                assign.as<uint32_t>() + c0);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    uint64_t* offs = ix->alloc<uint64_t>(nb + 1);
+    DevBuf order(sizeof(uint32_t) * n, st);
+    if (int rc = trim_ivf_lists_device(assign.as<uint32_t>(), n, nb, offs, order.as<uint32_t>(), ix->device, st))
+        throw std::runtime_error(trim_last_error());
+    uint8_t* codes = ix->alloc<uint8_t>(n * v.code_stride);
+    float* lx = ix->alloc<float>(n);
+    uint32_t* ids = ix->alloc<uint32_t>(n);
+    trim_partition_gather_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        order.as<uint32_t>(), n, v.codes, v.code_stride, v.lx, v.list_ids, codes, lx, ids);
+    a.list_offsets = offs;
+    a.list_ids = ids;
+    a.codes = codes;
+    a.lx = lx;
+    float* R = ix->alloc<float>(nb);
+    float* xmin = ix->alloc<float>(nb);
+    float* xmax = ix->alloc<float>(nb);
+    trim_list_meta_kernel<<<nb, kThreads, 0, st>>>(a, R, xmin, xmax);
+    CK(cudaGetLastError());
+    a.list_R = R;
+    a.list_xmin = xmin;
+    a.list_xmax = xmax;
+    CK(cudaStreamSynchronize(st));
+    ix->part = a;
+    ix->part_nb = nb;
+    return true;
+}
+
 // Query-tile size of the flat range kernel: as many LUTs as fit while two
 // CTAs stay resident per SM (1 = no tiling).
 uint32_t range_flat_qt(const DevIndex& v) {
@@ -388,6 +504,51 @@ void range_launch(const trim_index* ix, const float* d_q, uint64_t nq, const flo
     p.adc_eps = filter_eps(v.m);
     p.omg_hi = omg_round_up(gamma);
     p.cap = cap;
+    if (!d_probe && ensure_flat_partition(const_cast<trim_index*>(ix))) {
+        // flat scan over the block partition: blocks whose bound proves est > r^2 are skipped
+        const DevIndex& a = ix->part;
+        const uint32_t nb = ix->part_nb, K = mma_k(v.dim);
+        const uint32_t ntiles = (nb + kMmaN - 1) / kMmaN;
+        DevBuf approx(sizeof(float) * nq * mma_ld(nb), st), kept(sizeof(uint32_t) * nq * nb, st),
+            nkept(sizeof(uint32_t) * nq, st);
+        CK(cudaFuncSetAttribute(trim_probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(probe_mma_smem(K))));
+        trim_probe_mma_kernel<<<dim3(static_cast<unsigned>((nq + kMmaM - 1) / kMmaM),
+                                     (ntiles + kMmaTilesPerCta - 1) / kMmaTilesPerCta),
+                                kMmaThreads, probe_mma_smem(K), st>>>(d_q, nq, v.dim_stride, K, ix->part_tiles,
+                                                                      ix->part_cn2, nb, approx.as<float>());
+        const double u = std::ldexp(1.0, -24);
+        const float kq1 = std::nextafter(static_cast<float>(1.0 - 2.0 * (v.dim + 16) * u), 0.0f);
+        const float kq2 = std::nextafter(static_cast<float>(1.0 - 2.0 * (ix->max_sub_dim + v.m + 10) * u), 0.0f);
+        const float kest = std::nextafter(static_cast<float>(1.0 - 16.0 * u), 0.0f);
+        trim_block_select_kernel<<<static_cast<unsigned>(nq), kThreads, 0, st>>>(
+            a, d_q, nq, d_r2, approx.as<float>(), ix->part_cn2, ix->part_cn, omg_round_down(gamma), p.omg_hi, kq1, kq2,
+            kest, kept.as<uint32_t>(), nkept.as<uint32_t>(), ix->d_skipped);
+        CK(cudaGetLastError());
+        const size_t smem = range_smem_bytes(dispatch_m(a), a.m, a.dim_stride, nb);
+        if (smem > kSmemLimit)
+            throw std::runtime_error("flat range partition: per-query state exceeds shared memory");
+        p.np = nb;
+        p.np_q = nkept.as<uint32_t>();
+        p.eval_override = ix->total;
+        p.slice = 0;
+        constexpr uint32_t kSlices = 4;
+        for (uint64_t b = 0; b < nq; b += 65535) {
+            RangeParams pb = p;
+            const uint64_t nb2 = std::min<uint64_t>(65535, nq - b);
+            pb.queries = d_q + b * v.dim_stride;
+            pb.nq = nb2;
+            pb.radius_sq = d_r2 + b;
+            pb.probe = kept.as<uint32_t>() + b * nb;
+            pb.np_q = nkept.as<uint32_t>() + b;
+            pb.keys = d_keys + b * cap;
+            pb.count = d_cnt + b;
+            pb.dc = d_dc + b;
+            pb.evaluated = d_eval + b;
+            launch_range(a, pb, dim3(kSlices, static_cast<unsigned>(nb2)), smem, st);
+        }
+        return;
+    }
     const uint64_t bound = ix->stream_bound(np);
     const uint32_t qt = d_probe ? 1u : range_flat_qt(v);
     if (qt > 1) { // flat scan, query-tiled; at most 65535 slices (grid.y)

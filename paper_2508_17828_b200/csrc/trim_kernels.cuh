@@ -762,6 +762,11 @@ struct RangeParams {
     unsigned int* count;       // nq (members)
     unsigned long long* dc;    // nq (exact evaluations)
     unsigned long long* evaluated; // nq (stream length), written by slice 0
+    // flat indexes with a block partition: per-query kept block count (probe
+    // stride np), the stream split evenly over gridDim.x slices, and the
+    // reference's stream length (every row) reported as evaluated
+    const uint32_t* np_q;
+    uint64_t eval_override;
 };
 
 __host__ __device__ inline size_t range_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
@@ -798,14 +803,19 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = tid; i < ix.dim_stride; i += kThreads)
         qv[i] = qg[i];
+    const uint32_t npq = p.np_q ? p.np_q[q] : p.np;
     const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
-                                       p.np, st);
-    const uint32_t begin = blockIdx.x * p.slice;
+                                       npq, st);
+    uint32_t slice = p.slice;
+    if (p.np_q) // the kept blocks' positions, split evenly over the CTAs of this query
+        slice = max(static_cast<uint32_t>(kRangeChunk),
+                    ((total + gridDim.x - 1) / gridDim.x + kRangeChunk - 1) / kRangeChunk * kRangeChunk);
+    const uint32_t begin = blockIdx.x * slice;
     if (blockIdx.x == 0 && tid == 0)
-        p.evaluated[q] = total;
+        p.evaluated[q] = p.eval_override ? p.eval_override : total;
     if (begin >= total)
         return;
-    const uint32_t end = min(total, begin + p.slice);
+    const uint32_t end = min(total, begin + slice);
     build_lut_blocked(ix, qv, lut);
     const float r2 = p.radius_sq[q];
     LaneAdc la;
@@ -813,7 +823,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     const float r2_excl = __int_as_float(__float_as_int(r2) + 1); // smallest float > r2 (r2 >= 0)
 
     // first list whose range contains `begin`
-    uint32_t lo = 0, hi = p.np;
+    uint32_t lo = 0, hi = npq;
     while (lo + 1 < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (st.cum[mid] <= begin)
@@ -1420,6 +1430,166 @@ trim_list_meta_kernel(DevIndex ix, float* list_R, float* list_xmin, float* list_
         list_xmin[l] = lo;
         list_xmax[l] = hi;
     }
+}
+
+// --------------------------------------------------------------------------
+// Flat range search over a block partition of the rows (trim_capi.cu
+// build_flat_partition): the range filter is order-free (ivf.hpp:323-340), so
+// scanning the blocks instead of the rows in id order gives the reference's
+// members and counters exactly, and a block whose list-level bound proves
+// est > r^2 for all its rows is pruned whole. One CTA per query; D~ to the
+// block centroids comes from trim_probe_mma_kernel. Output: the kept blocks in
+// ascending order (probe stride nb) and their count.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ float block_lower_bound(float dq, float R, float xmin, float xmax, float omg_lo, float omg_hi,
+                                                   float kq1, float kq2, float kest) {
+    KnnParams p{};
+    p.omg_lo = omg_lo;
+    p.omg_hi = omg_hi;
+    p.kq1 = kq1;
+    p.kq2 = kq2;
+    p.kest = kest;
+    return list_lower_bound(dq, R, xmin, xmax, p);
+}
+
+__global__ void __launch_bounds__(kThreads)
+trim_block_select_kernel(DevIndex aux, const float* __restrict__ queries, uint64_t nq, const float* __restrict__ r2,
+                         const float* __restrict__ approx, const float* __restrict__ cn2, const float* __restrict__ cn,
+                         float omg_lo, float omg_hi, float kq1, float kq2, float kest, uint32_t* __restrict__ kept,
+                         uint32_t* __restrict__ nkept, unsigned long long* skipped) {
+    __shared__ uint32_t ws[16];
+    __shared__ unsigned long long s_len;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    if (q >= nq)
+        return;
+    const uint32_t nb = aux.nlist;
+    const float* qrow = queries + q * aux.dim_stride;
+    float qp = 0.0f;
+    for (uint32_t i = tid; i < aux.dim; i += kThreads)
+        qp = __fadd_ru(qp, __fmul_ru(qrow[i], qrow[i]));
+    for (int o = 16; o > 0; o >>= 1)
+        qp = __fadd_ru(qp, __shfl_xor_sync(0xffffffffu, qp, o));
+    if (lane == 0)
+        ws[warp] = __float_as_uint(qp);
+    __syncthreads();
+    float qn2 = 0.0f;
+    for (uint32_t w = 0; w < kWarps; ++w)
+        qn2 = __fadd_ru(qn2, __uint_as_float(ws[w]));
+    qn2 = __fmul_ru(qn2, 1.0f + 1.0f / 65536.0f);
+    const float qn = __fsqrt_ru(qn2);
+    const float rr = r2[q];
+    const float T = __int_as_float(__float_as_int(rr) + 1); // pruned iff est >= the float after r^2
+    const float* arow = approx + q * mma_ld(nb);
+    if (tid == 0)
+        s_len = 0;
+    __syncthreads();
+    uint32_t carry = 0;
+    unsigned long long my_len = 0;
+    for (uint32_t b0 = 0; b0 < nb; b0 += kThreads) {
+        const uint32_t b = b0 + tid;
+        bool keep = false;
+        if (b < nb && aux.list_offsets[b + 1] > aux.list_offsets[b]) {
+            keep = true;
+            if (rr >= 0.0f) {
+                const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(cn + b)), 1.0f / 64.0f),
+                                          __fmul_ru(__fadd_ru(qn2, __ldg(cn2 + b)), 1.0f / 16384.0f));
+                const float dq = fmaxf(__fsub_rd(arow[b], e), 0.0f); // <= |q - c_b|^2
+                keep = !(block_lower_bound(dq, __ldg(aux.list_R + b), __ldg(aux.list_xmin + b),
+                                           __ldg(aux.list_xmax + b), omg_lo, omg_hi, kq1, kq2, kest) >= T);
+            } else {
+                keep = false; // negative radius: nothing (status reported by the caller)
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0)
+            ws[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = carry, tot = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            before += w < warp ? ws[w] : 0u;
+            tot += ws[w];
+        }
+        if (keep) {
+            kept[q * nb + before + __popc(bal & ((1u << lane) - 1u))] = b;
+            my_len += aux.list_offsets[b + 1] - aux.list_offsets[b];
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (my_len)
+        atomicAdd(&s_len, my_len);
+    __syncthreads();
+    if (tid == 0) {
+        nkept[q] = carry;
+        const unsigned long long all = aux.list_offsets[nb];
+        if (skipped && all > s_len)
+            atomicAdd(skipped, all - s_len); // rows pruned as whole blocks (diagnostic)
+    }
+}
+
+// entry rows -> block order: codes, lx and ids gathered by the sorted rows.
+__global__ void trim_partition_gather_kernel(const uint32_t* __restrict__ rows, uint64_t n, const uint8_t* __restrict__ codes,
+                                             uint32_t cs, const float* __restrict__ lx, const uint32_t* __restrict__ ids,
+                                             uint8_t* __restrict__ codes_o, float* __restrict__ lx_o,
+                                             uint32_t* __restrict__ ids_o) {
+    const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n)
+        return;
+    const uint32_t r = rows[e];
+    const uint4* src = reinterpret_cast<const uint4*>(codes + static_cast<size_t>(r) * cs);
+    uint4* dst = reinterpret_cast<uint4*>(codes_o + e * cs);
+    for (uint32_t i = 0; i < cs / 16; ++i)
+        dst[i] = src[i];
+    lx_o[e] = lx[r];
+    ids_o[e] = ids[r];
+}
+
+// argmin over D~ rows (block assignment of a row chunk; any partition is valid,
+// the per-block bounds are computed from the actual members).
+__global__ void trim_argmin_kernel(const float* __restrict__ approx, uint64_t n, uint32_t nb, uint64_t ld,
+                                   uint32_t* __restrict__ out) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (r >= n)
+        return;
+    float best = __int_as_float(0x7f800000);
+    uint32_t bi = 0;
+    for (uint32_t b = lane; b < nb; b += 32) {
+        const float d = approx[r * ld + b];
+        if (d < best) {
+            best = d;
+            bi = b;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float od = __shfl_xor_sync(0xffffffffu, best, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (od < best || (od == best && oi < bi)) {
+            best = od;
+            bi = oi;
+        }
+    }
+    if (lane == 0)
+        out[r] = bi;
+}
+
+// rows (stride floats apart, given by index) -> a contiguous [ns x dim] sample
+__global__ void trim_gather_rows_kernel(const float* __restrict__ src, uint32_t stride, const uint64_t* __restrict__ rows,
+                                        uint64_t ns, uint32_t dim, float* __restrict__ dst) {
+    const uint64_t i = blockIdx.x;
+    if (i >= ns)
+        return;
+    for (uint32_t j = threadIdx.x; j < dim; j += blockDim.x)
+        dst[i * dim + j] = src[rows[i] * stride + j];
+}
+
+// 1 if list entry e holds row e (id_base + e) for every e (flat lists in row order).
+__global__ void trim_identity_check_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint64_t id_base,
+                                           uint32_t* __restrict__ bad) {
+    const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < n && ids[e] != id_base + e)
+        atomicOr(bad, 1u);
 }
 
 #endif // TRIM_M

@@ -97,3 +97,21 @@ def test_range_device_api(flat):
     torch.cuda.synchronize()
     assert int(st.item()) & 2
     assert int(c3[0].item()) == 0
+
+
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 0.8, 1.0])
+def test_flat_range_block_partition(flat, gamma, monkeypatch):
+    """Flat range over the block partition (built when the index is first
+    searched; forced here for a small index): identical members and counters."""
+    hix, qs, rad, _ = flat
+    monkeypatch.setenv("TRIM_FLAT_PARTITION_MIN_ROWS", "1000")
+    gix = G.GpuIvfIndex(G.IvfArrays.from_any(hix))  # fresh index: the partition is built on this call
+    want = co.search_range(hix, qs, rad, 1, gamma)
+    got = G.search_trim_ivf_range_batch(gix, G.PruningProfile.manual(gamma), qs, rad, 1)
+    check(got, want)
+    # the device API over the same partition
+    import torch
+    cnt, di, dd = G.search_trim_ivf_range_device(gix, G.PruningProfile.manual(gamma), torch.from_numpy(qs).cuda(),
+                                                 torch.from_numpy(rad).cuda(), 1, cap=4096)
+    cnt = cnt.cpu().numpy()
+    np.testing.assert_array_equal(cnt, np.diff(want[0].astype(np.int64)))

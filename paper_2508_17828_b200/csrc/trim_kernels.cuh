@@ -238,7 +238,7 @@ __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t di
     b += sizeof(uint32_t) * kRing * kChunkW * 4; // superset bins: id, est_lo, est_hi, d
     b += sizeof(uint32_t) * kRing * kWorkers * 2; // bin counts, bin lane masks
     b = (b + 15) & ~size_t(15);
-    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers, plan barrier (+pad)
+    b += sizeof(uint64_t) * (2 * kRing + 2);     // full/empty mbarriers (+2 spare)
     b += 16;                                     // published threshold, plan length
     return b;
 }
@@ -266,20 +266,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             break;
     }
 }
-// For the long once-per-query waits (plan, chunk 0's replay): back off so the
-// waiting warps do not burn the issue slots the SM's other queries need.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (;;) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done)
-                     : "r"(saddr(bar)), "r"(parity)
-                     : "memory");
-        if (done)
-            break;
-        __nanosleep(256u);
-    }
+// Named hardware barriers between the replay warp and the workers (a warp
+// blocked in bar.sync issues nothing, unlike an mbarrier poll).
+constexpr uint32_t kBarWorkers = 1;   // workers only: LUT complete
+constexpr uint32_t kBarPlan = 2;      // replay arrives: seeds + plan published
+constexpr uint32_t kBarChunk0 = 3;    // replay arrives: chunk 0 replayed
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ float ld_volatile(const float* p) {
     return *reinterpret_cast<const volatile float*>(p);
@@ -404,7 +400,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             mbar_init(full + s, kWorkers * kWarp);
             mbar_init(empty + s, kWarp);
         }
-        mbar_init(plan, kWarp);
         *s_T = kInf;
     }
     __syncthreads();
@@ -494,7 +489,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         const uint32_t ncum = nk;
         TRIM_TL(if (tl && lane == 0) tl[3] = gtime();)
         __syncwarp();
-        mbar_arrive(plan);
+        named_arrive(kBarPlan, kThreads);
 
         uint64_t dc = nseed;
         TRIM_TL(uint32_t members = 0;)
@@ -568,6 +563,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 *reinterpret_cast<volatile float*>(s_T) = topk.wd;
             __syncwarp();
             mbar_arrive(empty + s);
+            if (c == 0 && nchunks > 1) // the workers filter chunk 1 on against this threshold
+                named_arrive(kBarChunk0, kThreads);
             TRIM_TL(if (tl) {
                 cyc_wait += k1 - k0;
                 cyc_busy += clock64() - k1;
@@ -617,7 +614,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
             unsigned long long wk = wtl ? clock64() : 0;)
     build_lut_blocked(ix, qv, lut, tid - kWarp, kThreads - kWarp);
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - kWarp) : "memory"); // workers only
+    named_sync(kBarWorkers, kThreads - kWarp); // workers only
     const uint32_t w = warp - 1;
     LaneAdc la;
     la.init(lane, LutShape::of(m));
@@ -626,7 +623,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         wc[0] = t - wk;
         wk = t;
     })
-    mbar_wait_backoff(plan, 0); // seeds done, compacted stream ready
+    named_sync(kBarPlan, kThreads); // seeds done, compacted stream ready
     TRIM_TL(if (wtl) {
         const unsigned long long t = clock64();
         wc[1] = t - wk;
@@ -671,7 +668,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         if (c >= kRing)
             mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
         if (c == 1) // filter the rest against the threshold after chunk 0, not the seeds'
-            mbar_wait_backoff(empty, 0);
+            named_sync(kBarChunk0, kThreads);
         const float T = ld_volatile(s_T);
         TRIM_TL(const unsigned long long k1 = wtl ? clock64() : 0;)
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
@@ -703,8 +700,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     exact = false;
                 }
             }
-            if (exact)
-                d = euclid_sq_vec4(qv, ix.vectors + rw * ix.dim_stride, ix.dim);
+            if (exact) // the whole row in flight at once (one DRAM round trip)
+                d = euclid_sq_vec4(qv, ix.vectors + rw * ix.dim_stride, ix.dim, true);
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (keep) {

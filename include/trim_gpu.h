@@ -261,6 +261,71 @@ int trim_pq_encode_device(const float* d_x, uint64_t n, uint32_t dim, uint32_t m
 int trim_ivf_lists_device(const uint32_t* d_assign, uint64_t n, uint32_t nlist,
                           uint64_t* d_offsets, uint32_t* d_ids, int device, void* stream);
 
+/* ------------------------------------------------------------------------
+ * TRIM filter over an HNSW graph: the per-hop
+ * neighbour filter of graph::search_trim_knn / search_trim_range
+ * (graph/search.hpp:188-347), batched over queries (one warp per query).
+ * ------------------------------------------------------------------------ */
+
+/*
+ * graph::GraphIndex (graph/hnsw.hpp:22-35) as per-level CSR, with the
+ * trim::LandmarkStore (trim/landmarks.hpp:18-28) and VectorDataset it is
+ * searched with. trim_graph_create copies everything (host or device arrays
+ * per `memory`); the caller keeps ownership.
+ *   offsets   levels x (n+1): node i's level-l list is
+ *             nbrs[nbr_base[l] + offsets[l*(n+1)+i] .. + offsets[l*(n+1)+i+1])
+ *   codes     n x code_stride landmark codes (LandmarkStore::codes, by node id)
+ *   lx        n plain Γ(l,x) (LandmarkStore::lx_dist)
+ *   centroids the codebook, trim_index_desc layout
+ * lm.count != ds.count (search.hpp:198-199) cannot arise: both are n.
+ */
+typedef struct {
+    uint64_t n;
+    uint32_t dim;
+    uint32_t m;
+    uint32_t ksub;
+    const uint32_t* sub_dims;
+    const float* centroids;
+    const uint8_t* codes;
+    uint32_t code_stride;
+    const float* lx;
+    const float* vectors;
+    uint32_t levels; /* GraphIndex::max_level + 1 */
+    uint32_t entry;  /* GraphIndex::entry */
+    const uint64_t* offsets;
+    const uint64_t* nbr_base;
+    const uint32_t* nbrs;
+    uint64_t total_nbrs;
+    int device;
+    trim_memory memory;
+} trim_graph_desc;
+
+typedef struct trim_graph* trim_graph_t;
+
+int trim_graph_create(const trim_graph_desc* desc, trim_graph_t* out);
+int trim_graph_destroy(trim_graph_t graph);
+
+/*
+ * graph::search_trim_knn (graph/search.hpp:188-264) for nq queries (host
+ * arrays). ids_out/dist_out: nq*k, each row ascending by (dist_sq, id); a
+ * query with fewer than k results pads with id 0xFFFFFFFF / +inf.
+ * counters_out: nq (hops = expanded nodes, coarse_dc = 0), may be NULL.
+ * k == 0 or k > ef -> TRIM_EINVAL (search.hpp:193-194); gamma < 0 ->
+ * TRIM_EINVAL (uncalibrated profile, search.hpp:195-196); ef <= 256.
+ */
+int trim_graph_search_knn(trim_graph_t graph, const float* queries, uint64_t nq, uint32_t k,
+                          uint32_t ef, float gamma, uint32_t* ids_out, float* dist_out,
+                          trim_counters* counters_out);
+/*
+ * graph::search_trim_range (graph/search.hpp:267-347). radius: nq plain radii
+ * (negative -> TRIM_EINVAL). Results as trim_search_range: offsets_out nq+1,
+ * library-allocated *ids_out / *dist_out (trim_free), ascending (dist_sq, id).
+ * 1 <= ef <= 256.
+ */
+int trim_graph_search_range(trim_graph_t graph, const float* queries, uint64_t nq,
+                            const float* radius, uint32_t ef, float gamma, uint64_t* offsets_out,
+                            uint32_t** ids_out, float** dist_out, trim_counters* counters_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -284,6 +284,48 @@ class _FlatIndex(C.Structure):
     ]
 
 
+class _FlatGraph(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64), ("M", C.c_uint32), ("levels", C.c_uint32), ("entry", C.c_uint32),
+        ("efc", C.c_uint32), ("offsets", _u64p), ("nbr_base", _u64p), ("nbrs", _u32p),
+    ]
+
+
+@dataclass
+class HostGraph:
+    """HNSW GraphIndex (graph/hnsw.hpp:22-35) as per-level CSR arrays, plus the
+    LandmarkStore (trim/landmarks.hpp:18-28) and VectorDataset it searches."""
+
+    n: int
+    M: int
+    efc: int
+    entry: int
+    offsets: list  # per level: u64[n+1]
+    nbrs: list  # per level: u32[offsets[-1]]
+    dim: int = 0
+    m: int = 0
+    ksub: int = 256
+    sub_dims: np.ndarray = None  # u32[m]
+    centroids: np.ndarray = None  # f32[ksub*dim]
+    codes: np.ndarray = None  # u8[n, m]
+    lx: np.ndarray = None  # f32[n]
+    vectors: np.ndarray = None  # f32[n, dim]
+
+    @property
+    def levels(self) -> int:
+        return len(self.offsets)
+
+    def flat(self):
+        """(_FlatGraph, keep-alive arrays) for the harness."""
+        offs = np.ascontiguousarray(np.concatenate([np.asarray(o, np.uint64) for o in self.offsets]))
+        sizes = [int(np.asarray(o)[-1]) for o in self.offsets]
+        base = np.ascontiguousarray(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64))
+        nb = np.ascontiguousarray(np.concatenate([np.asarray(x, np.uint32) for x in self.nbrs]))
+        fg = _FlatGraph(self.n, self.M, self.levels, self.entry, self.efc, _ptr(offs, _u64p),
+                        _ptr(base, _u64p), _ptr(nb, _u32p))
+        return fg, (offs, base, nb)
+
+
 def ref_available(path: str = REF_SO) -> bool:
     return os.path.exists(path)
 
@@ -350,6 +392,16 @@ class RefOracle:
                                       _f32p]
         L.ref_adc_lookup.restype = C.c_float
         L.ref_adc_lookup.argtypes = [_f32p, C.c_uint32, C.c_uint32, _u8p]
+        L.ref_graph_build.restype = C.c_void_p
+        L.ref_graph_build.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
+        L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_graph_info.argtypes = [C.c_void_p, _u32p, _u32p, _u64p]
+        L.ref_graph_export.argtypes = [C.c_void_p, C.c_uint32, _u64p, _u32p]
+        L.ref_graph_save.argtypes = [C.POINTER(_FlatGraph), C.c_char_p]
+        L.ref_graph_search_batch.argtypes = [C.POINTER(_FlatGraph), C.c_uint32, C.c_uint32, C.c_uint32,
+                                             _u32p, _f32p, _u8p, _f32p, _f32p, _f32p, C.c_uint64,
+                                             C.c_int, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
+                                             C.c_uint64, _u32p, _f32p, _u64p, _u64p]
         self._keep = []
 
     def _err(self, rc: int, what: str):
@@ -361,6 +413,60 @@ class RefOracle:
 
     def set_threads(self, t: int):
         self.lib.ref_set_threads(t)
+
+    # -- HNSW graph (graph/hnsw.hpp:165-268) and graph searches (graph/search.hpp) --
+    def build_graph(self, data, M, efc, seed) -> HostGraph:
+        data = np.ascontiguousarray(data, np.float32)
+        n, dim = data.shape
+        h = self.lib.ref_graph_build(_ptr(data, _f32p), n, dim, M, efc, seed)
+        if not h:
+            raise ValueError(f"build_graph: {self.lib.ref_last_error().decode()}")
+        try:
+            lv, en = C.c_uint32(0), C.c_uint32(0)
+            self.lib.ref_graph_info(h, C.byref(lv), C.byref(en), None)
+            sizes = np.zeros(lv.value, np.uint64)
+            self.lib.ref_graph_info(h, C.byref(lv), C.byref(en), _ptr(sizes, _u64p))
+            offs, nbrs = [], []
+            for lvl in range(lv.value):
+                o = np.zeros(n + 1, np.uint64)
+                nb = np.zeros(max(int(sizes[lvl]), 1), np.uint32)
+                self.lib.ref_graph_export(h, lvl, _ptr(o, _u64p), _ptr(nb, _u32p))
+                offs.append(o)
+                nbrs.append(nb[:int(sizes[lvl])])
+        finally:
+            self.lib.ref_graph_free(h)
+        return HostGraph(n=n, M=M, efc=efc, entry=en.value, offsets=offs, nbrs=nbrs, dim=dim,
+                         vectors=data)
+
+    def graph_save(self, g: HostGraph, path: str):
+        fg, keep = g.flat()
+        self._err(self.lib.ref_graph_save(C.byref(fg), path.encode()), "graph_save")
+
+    def graph_search(self, g: HostGraph, qs, kind: str, *, k=0, ef=0, gamma=0.0, radius=0.0, cap=0):
+        """kind: "trim_knn" (graph/search.hpp:188-264), "trim_range" (:267-347,
+        results truncated at cap per query) or "baseline_knn" (:85-124).
+        Returns ids, dist_sq ([nq, k] or [nq, cap]), counts[nq], counters[nq, 6]."""
+        qs = np.ascontiguousarray(qs, np.float32)
+        nq = qs.shape[0]
+        kid = {"trim_knn": 0, "trim_range": 1, "baseline_knn": 2}[kind]
+        w = cap if kid == 1 else k
+        ids = np.full((nq, max(w, 1)), 0xFFFFFFFF, np.uint32)
+        dist = np.full((nq, max(w, 1)), np.inf, np.float32)
+        counts = np.zeros(nq, np.uint64)
+        ct = np.zeros((nq, 6), np.uint64)
+        fg, keep = g.flat()
+        sub = np.ascontiguousarray(g.sub_dims, np.uint32)
+        cent = np.ascontiguousarray(g.centroids, np.float32).ravel()
+        codes = np.ascontiguousarray(g.codes, np.uint8)
+        lx = np.ascontiguousarray(g.lx, np.float32)
+        vec = np.ascontiguousarray(g.vectors, np.float32)
+        rc = self.lib.ref_graph_search_batch(C.byref(fg), g.dim, g.m, g.ksub, _ptr(sub, _u32p),
+                                             _ptr(cent, _f32p), _ptr(codes, _u8p), _ptr(lx, _f32p),
+                                             _ptr(vec, _f32p), _ptr(qs, _f32p), nq, kid, k, ef, gamma,
+                                             radius, cap, _ptr(ids, _u32p), _ptr(dist, _f32p),
+                                             _ptr(counts, _u64p), _ptr(ct, _u64p))
+        self._err(rc, f"graph {kind}")
+        return ids[:, :w], dist[:, :w], counts, ct
 
     # -- generators (core/synthetic.hpp) --
     def make_normal(self, n, dim, seed) -> np.ndarray:
@@ -629,6 +735,16 @@ class RefOracle:
         code = np.ascontiguousarray(code, np.uint8)
         return self.lib.ref_adc_lookup(_ptr(table, _f32p), table.shape[0], table.shape[1],
                                        _ptr(code, _u8p))
+
+
+def make_reference_graph(ref: RefOracle, data, *, M=8, efc=64, graph_seed=5, m, c=256, iters=25,
+                         pq_seed=1) -> HostGraph:
+    """The reference's graph pipeline: build_graph + pq::train + build_landmarks."""
+    g = ref.build_graph(data, M, efc, graph_seed)
+    sub, cent = ref.pq_train(data, m, c, iters, pq_seed, 0)
+    codes, lx = ref.build_landmarks(data, m, c, sub, cent)
+    g.m, g.ksub, g.sub_dims, g.centroids, g.codes, g.lx = m, c, sub, cent, codes, lx
+    return g
 
 
 def make_reference_index(ref: RefOracle, data, *, m, c=256, iters=25, pq_seed=1, nlist=1,

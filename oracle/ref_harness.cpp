@@ -23,6 +23,8 @@
 #include "trimsearch/core/parallel.hpp"
 #include "trimsearch/core/synthetic.hpp"
 #include "trimsearch/core/vecs_io.hpp"
+#include "trimsearch/graph/hnsw.hpp"
+#include "trimsearch/graph/search.hpp"
 #include "trimsearch/ivf/ivf.hpp"
 #include "trimsearch/pq/pq.hpp"
 #include "trimsearch/trim/calibration.hpp"
@@ -124,6 +126,50 @@ void put_counters(std::uint64_t* out, const SearchCounters& c, std::uint64_t coa
     out[4] = c.hops;
     out[5] = coarse_dc;
 }
+
+// Flat CSR view of an HNSW GraphIndex (graph/hnsw.hpp:22-35): level l's
+// adjacency is offsets[l*(n+1) + i .. + i+1) into nbrs + nbr_base[l].
+struct FlatGraph {
+    std::uint64_t n;
+    std::uint32_t M, levels, entry, efc;
+    const std::uint64_t* offsets;
+    const std::uint64_t* nbr_base;
+    const std::uint32_t* nbrs;
+};
+
+graph::GraphIndex make_graph(const FlatGraph& f) {
+    graph::GraphIndex g;
+    g.count = f.n;
+    g.M = f.M;
+    g.ef_construction = f.efc;
+    g.entry = f.entry;
+    g.max_level = f.levels - 1;
+    g.layers.resize(f.levels);
+    for (std::uint32_t l = 0; l < f.levels; ++l) {
+        const std::uint64_t* o = f.offsets + static_cast<std::size_t>(l) * (f.n + 1);
+        const std::uint32_t* nb = f.nbrs + f.nbr_base[l];
+        g.layers[l].resize(f.n);
+        for (std::uint64_t i = 0; i < f.n; ++i)
+            g.layers[l][i].assign(nb + o[i], nb + o[i + 1]);
+    }
+    return g;
+}
+
+// LandmarkStore (trim/landmarks.hpp:18-28) from flat arrays: codes n*m, lx n.
+trim::LandmarkStore make_lm(std::uint32_t dim, std::uint32_t m, std::uint32_t c,
+                            const std::uint32_t* sub_dims, const float* centroids,
+                            const std::uint8_t* codes, const float* lx, std::uint64_t n) {
+    trim::LandmarkStore lm;
+    lm.codebook = make_cb(dim, m, c, sub_dims, centroids);
+    lm.count = n;
+    lm.codes.assign(codes, codes + n * m);
+    lm.lx_dist.assign(lx, lx + n);
+    return lm;
+}
+
+struct GraphSession {
+    graph::GraphIndex g;
+};
 
 } // namespace
 
@@ -559,6 +605,91 @@ int ref_calibrate_empirical(const float* data, std::uint64_t n, std::uint32_t di
         ep.seed = seed;
         *gamma_out =
             trim::calibrate_gamma(trim::sample_one_minus_z_empirical(ds, lm, q, ep), p).gamma;
+    });
+}
+
+// ---- HNSW graph (graph/hnsw.hpp:165-268) and the TRIM graph searches
+// (graph/search.hpp:188-347): test infrastructure for the graph filter path.
+void* ref_graph_build(const float* data, std::uint64_t n, std::uint32_t dim, std::uint32_t M,
+                      std::uint32_t efc, std::uint64_t seed) {
+    auto* s = new GraphSession;
+    const int rc = guarded([&] { s->g = graph::build_graph(make_ds(data, n, dim), M, efc, seed); });
+    if (rc != REF_OK) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+void ref_graph_free(void* p) { delete static_cast<GraphSession*>(p); }
+// levels, entry, and per level the total adjacency size (sizes_out: levels).
+int ref_graph_info(void* p, std::uint32_t* levels, std::uint32_t* entry, std::uint64_t* sizes_out) {
+    auto* s = static_cast<GraphSession*>(p);
+    *levels = static_cast<std::uint32_t>(s->g.max_level + 1);
+    *entry = s->g.entry;
+    if (sizes_out)
+        for (std::size_t l = 0; l <= s->g.max_level; ++l) {
+            std::uint64_t t = 0;
+            for (const auto& a : s->g.layers[l])
+                t += a.size();
+            sizes_out[l] = t;
+        }
+    return REF_OK;
+}
+int ref_graph_export(void* p, std::uint32_t level, std::uint64_t* offsets_out, std::uint32_t* nbrs_out) {
+    auto* s = static_cast<GraphSession*>(p);
+    std::uint64_t off = 0;
+    for (std::size_t i = 0; i < s->g.count; ++i) {
+        offsets_out[i] = off;
+        for (std::uint32_t v : s->g.layers[level][i])
+            nbrs_out[off++] = v;
+    }
+    offsets_out[s->g.count] = off;
+    return REF_OK;
+}
+int ref_graph_save(const FlatGraph* f, const char* path) {
+    return guarded([&] { make_graph(*f).save(path); });
+}
+
+// graph::search_trim_knn (kind 0, k results) / search_trim_range (kind 1,
+// arg = radius; results at ids_out + qi*cap, counts_out[qi] = true count) /
+// search_baseline_knn (kind 2) over a batch, parallel_for over queries.
+int ref_graph_search_batch(const FlatGraph* fg, std::uint32_t dim, std::uint32_t m, std::uint32_t c,
+                           const std::uint32_t* sub_dims, const float* centroids,
+                           const std::uint8_t* codes, const float* lx, const float* data,
+                           const float* qs, std::uint64_t nq, int kind, std::uint32_t k,
+                           std::uint32_t ef, double gamma, double arg, std::uint64_t cap,
+                           std::uint32_t* ids_out, float* dist_out, std::uint64_t* counts_out,
+                           std::uint64_t* counters_out) {
+    return guarded([&] {
+        const auto g = make_graph(*fg);
+        const auto lm = make_lm(dim, m, c, sub_dims, centroids, codes, lx, fg->n);
+        const auto ds = make_ds(data, fg->n, dim);
+        std::vector<std::string> errs(nq);
+        parallel_for(nq, [&](std::size_t qi) {
+            try {
+                const VectorView q(qs + qi * dim, dim);
+                graph::SearchResult r;
+                if (kind == 0)
+                    r = graph::search_trim_knn(g, ds, lm, trim::PruningProfile::manual(gamma), q, k, ef);
+                else if (kind == 1)
+                    r = graph::search_trim_range(g, ds, lm, trim::PruningProfile::manual(gamma), q,
+                                                 static_cast<float>(arg), ef);
+                else
+                    r = graph::search_baseline_knn(g, ds, q, k, ef);
+                const std::size_t w = kind == 1 ? cap : k;
+                for (std::size_t i = 0; i < r.ids.size() && i < w; ++i) {
+                    ids_out[qi * w + i] = r.ids[i];
+                    dist_out[qi * w + i] = r.dist_sq[i];
+                }
+                counts_out[qi] = r.ids.size();
+                put_counters(counters_out + qi * 6, r.counters, 0);
+            } catch (const std::exception& e) {
+                errs[qi] = e.what();
+            }
+        });
+        for (const auto& e : errs)
+            if (!e.empty())
+                throw std::invalid_argument(e);
     });
 }
 

@@ -49,6 +49,17 @@ class TrimIndexInfo(C.Structure):
                 ("device_bytes", C.c_uint64), ("device", C.c_int), ("range_query_tile", C.c_uint32)]
 
 
+class TrimGraphDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_uint64), ("dim", C.c_uint32), ("m", C.c_uint32), ("ksub", C.c_uint32),
+        ("sub_dims", C.c_void_p), ("centroids", C.c_void_p), ("codes", C.c_void_p),
+        ("code_stride", C.c_uint32), ("lx", C.c_void_p), ("vectors", C.c_void_p),
+        ("levels", C.c_uint32), ("entry", C.c_uint32), ("offsets", C.c_void_p),
+        ("nbr_base", C.c_void_p), ("nbrs", C.c_void_p), ("total_nbrs", C.c_uint64),
+        ("device", C.c_int), ("memory", C.c_int),
+    ]
+
+
 # name -> (restype, argtypes); must cover every function include/trim_gpu.h declares
 SIGNATURES = {
     "trim_last_error": (C.c_char_p, []),
@@ -85,6 +96,14 @@ SIGNATURES = {
                                          C.c_uint32, C.c_void_p, C.c_void_p, C.c_int,
                                          C.c_void_p]),
     "trim_free": (None, [C.c_void_p]),
+    # TRIM filter over an HNSW graph
+    "trim_graph_create": (C.c_int, [C.POINTER(TrimGraphDesc), C.POINTER(C.c_void_p)]),
+    "trim_graph_destroy": (C.c_int, [C.c_void_p]),
+    "trim_graph_search_knn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                        C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "trim_graph_search_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
+                                          C.c_float, C.c_void_p, C.POINTER(_u32p), C.POINTER(_f32p),
+                                          C.c_void_p]),
     # device-side index build
     "trim_synth_normal_device": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int,
                                            C.c_void_p]),

@@ -19,6 +19,7 @@
 
 #include "../../include/trim_gpu.h"
 #include "trim_baseline.cuh"
+#include "trim_graph.cuh"
 #include "trim_kernels.cuh"
 #include "trim_launch.h"
 
@@ -808,9 +809,131 @@ int baseline_device(const trim_index* ix, const float* d_q, uint64_t nq, uint32_
     return TRIM_OK;
 }
 
+// ------------------------------------------------------------ graph search
 } // namespace
 
-// ======================================================================= API
+struct trim_graph {
+    int device = 0;
+    GraphDev dev{};
+    std::vector<void*> allocs;
+    ~trim_graph() {
+        if (!allocs.empty()) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            for (void* p : allocs)
+                cudaFree(p);
+            cudaSetDevice(prev);
+        }
+    }
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(sizeof(T) * count, 16)));
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+
+namespace {
+
+// Candidate-queue register sets: 32*S >= max(ef, k) slots.
+uint32_t graph_slots(uint32_t need) {
+    uint32_t S = 1;
+    while (32u * S < need)
+        S <<= 1;
+    return S;
+}
+
+// One graph search over nq device-resident queries (rows padded to
+// dim_stride). Workspace: a visited bitmap and a search-queue heap per query;
+// queries run in groups that fit `budget` bytes, and a query whose search
+// queue outgrew the first capacity is re-run with capacity n + 1 (exact).
+// kNN writes d_ids/d_dist (nq x k); range writes the pool (nq x cap keys) and
+// counts. d_ct: nq x 6 counters.
+void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32_t ef, float gamma,
+               bool range, const float* d_r2, uint32_t* d_ids, float* d_dist, unsigned long long* d_pool,
+               uint64_t cap, unsigned long long* d_counts, unsigned long long* d_ct, cudaStream_t st) {
+    const GraphDev& g = gr->dev;
+    const uint64_t n = g.ix.n, vwords = (n + 31) / 32;
+    const uint32_t S = graph_slots(std::max(ef, range ? 1u : k));
+    const size_t smem = graph_smem_bytes(g.ix.m, g.ix.dim_stride);
+    const size_t budget = size_t(1) << 30;
+    GraphParams p{};
+    p.k = k;
+    p.ef = ef;
+    p.two_gamma = 2.0f * gamma;
+    p.range = range ? 1u : 0u;
+    p.cap = cap;
+    p.vwords = vwords;
+    auto run = [&](uint64_t q0, uint64_t nb, uint64_t heap_cap, uint32_t* d_status) {
+        const size_t per_q = vwords * 4 + heap_cap * 8;
+        const uint64_t group = std::max<uint64_t>(1, std::min<uint64_t>(nb, budget / per_q));
+        DevBuf vis(vwords * 4 * group, st), heap(heap_cap * 8 * group, st);
+        for (uint64_t g0 = 0; g0 < nb; g0 += group) {
+            const uint64_t gn = std::min(group, nb - g0), qi = q0 + g0;
+            CK(cudaMemsetAsync(vis.p, 0, vwords * 4 * gn, st));
+            GraphParams pp = p;
+            pp.nq = gn;
+            pp.queries = d_q + qi * g.ix.dim_stride;
+            pp.r2 = range ? d_r2 + qi : nullptr;
+            pp.ids_out = range ? nullptr : d_ids + qi * k;
+            pp.dist_out = range ? nullptr : d_dist + qi * k;
+            pp.pool = range ? d_pool + qi * cap : nullptr;
+            pp.counts = range ? d_counts + qi : nullptr;
+            pp.counters = d_ct + qi * 6;
+            pp.visited = vis.as<uint32_t>();
+            pp.heap = heap.as<unsigned long long>();
+            pp.heap_cap = heap_cap;
+            pp.status = d_status + g0;
+            CK(launch_graph(g, pp, S, smem, st));
+        }
+    };
+    DevBuf d_status(sizeof(uint32_t) * std::max<uint64_t>(nq, 1), st);
+    CK(cudaMemsetAsync(d_status.p, 0, sizeof(uint32_t) * nq, st));
+    // TRIM_GRAPH_HEAP_CAP (tests): a smaller first search-queue capacity, so
+    // the overflow re-run path runs on small graphs too
+    uint64_t cap0 = 1u << 16;
+    if (const char* e = std::getenv("TRIM_GRAPH_HEAP_CAP"))
+        cap0 = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    run(0, nq, std::min<uint64_t>(n + 1, cap0), d_status.as<uint32_t>());
+    if (n + 1 <= cap0)
+        return;
+    std::vector<uint32_t> status(nq);
+    CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(uint32_t) * nq, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    DevBuf d_st1(sizeof(uint32_t), st);
+    for (uint64_t i = 0; i < nq; ++i)
+        if (status[i] & 1u) {
+            CK(cudaMemsetAsync(d_st1.p, 0, sizeof(uint32_t), st));
+            run(i, 1, n + 1, d_st1.as<uint32_t>());
+        }
+}
+
+DevBuf graph_upload_queries(const trim_graph* gr, const float* q, uint64_t nq, cudaStream_t st) {
+    const uint32_t dim = gr->dev.ix.dim, ds = gr->dev.ix.dim_stride;
+    DevBuf d(sizeof(float) * std::max<uint64_t>(nq, 1) * ds, st);
+    if (nq == 0)
+        return d;
+    CK(cudaMemsetAsync(d.p, 0, sizeof(float) * nq * ds, st));
+    CK(cudaMemcpy2DAsync(d.p, sizeof(float) * ds, q, sizeof(float) * dim, sizeof(float) * dim, nq,
+                         cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+void put_counters_host(trim_counters* out, const std::vector<unsigned long long>& ct, uint64_t nq) {
+    for (uint64_t i = 0; i < nq; ++i) {
+        out[i].dc = ct[i * 6 + 0];
+        out[i].edc = ct[i * 6 + 1];
+        out[i].pruned = ct[i * 6 + 2];
+        out[i].evaluated = ct[i * 6 + 3];
+        out[i].hops = ct[i * 6 + 4];
+        out[i].coarse_dc = ct[i * 6 + 5];
+    }
+}
+
+} // namespace
+
 extern "C" {
 
 const char* trim_last_error(void) { return g_err.c_str(); }
@@ -1467,6 +1590,254 @@ int trim_merge_topk_device(const float* d_dist, const uint32_t* d_ids, uint32_t 
         trim_merge_kernel<<<static_cast<unsigned>(nq), kThreads, smem, st>>>(
             d_dist, d_ids, nshards, nq, k, n2, d_dist_out, d_ids_out);
         CK(cudaGetLastError());
+        return TRIM_OK;
+    });
+}
+
+// ------------------------------------------------------------ graph search
+// (include/trim_gpu.h: trim_graph_*; graph/search.hpp:188-347)
+int trim_graph_create(const trim_graph_desc* d, trim_graph_t* out) {
+    if (!d || !out)
+        return set_err(TRIM_EINVAL, "trim_graph_create: null argument");
+    *out = nullptr;
+    if (d->n == 0)
+        return set_err(TRIM_EINVAL, "trim_graph_create: empty graph");
+    if (d->n >= 0xFFFFFFFFull)
+        return set_err(TRIM_EINVAL, "trim_graph_create: more than 2^32-2 nodes");
+    if (d->dim == 0 || d->m == 0 || d->ksub == 0 || d->ksub > 256 || d->levels == 0)
+        return set_err(TRIM_EINVAL, "trim_graph_create: need dim, m, levels >= 1 and 1 <= ksub <= 256");
+    if (!d->sub_dims || !d->centroids || !d->codes || !d->lx || !d->vectors || !d->offsets ||
+        !d->nbr_base || (d->total_nbrs && !d->nbrs))
+        return set_err(TRIM_EINVAL, "trim_graph_create: null array in descriptor");
+    if (d->code_stride < d->m)
+        return set_err(TRIM_EINVAL, "trim_graph_create: code_stride < m");
+    if (d->entry >= d->n)
+        return set_err(TRIM_EDATA, "graph entry %u outside [0, %llu)", d->entry, (unsigned long long)d->n);
+    if (int rc = check_device_present())
+        return rc;
+    const bool host = d->memory == TRIM_MEM_HOST;
+    const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    return guarded([&]() -> int {
+        DeviceGuard dg(d->device);
+        const uint64_t n = d->n, L = d->levels;
+        std::vector<uint32_t> sub(d->m);
+        CK(cudaMemcpy(sub.data(), d->sub_dims, sizeof(uint32_t) * d->m,
+                      host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> suboff(d->m);
+        uint64_t sdsum = 0;
+        for (uint32_t j = 0; j < d->m; ++j) {
+            suboff[j] = static_cast<uint32_t>(sdsum);
+            sdsum += sub[j];
+        }
+        if (sdsum != d->dim)
+            return set_err(TRIM_EDATA, "codebook sub_dims do not sum to dim");
+        if (host) { // graph/hnsw.hpp:58-83 invariants: monotone CSR, ids < count
+            for (uint64_t l = 0; l < L; ++l) {
+                const uint64_t* o = d->offsets + l * (n + 1);
+                if (o[0] != 0)
+                    return set_err(TRIM_EDATA, "graph level %llu offsets must start at 0", (unsigned long long)l);
+                for (uint64_t i = 0; i < n; ++i)
+                    if (o[i + 1] < o[i])
+                        return set_err(TRIM_EDATA, "graph level %llu offsets are not monotone", (unsigned long long)l);
+                if (d->nbr_base[l] + o[n] > d->total_nbrs)
+                    return set_err(TRIM_EDATA, "graph level %llu adjacency exceeds total_nbrs", (unsigned long long)l);
+                for (uint64_t e = 0; e < o[n]; ++e)
+                    if (d->nbrs[d->nbr_base[l] + e] >= n)
+                        return set_err(TRIM_EDATA, "graph neighbour id %u outside [0, %llu)",
+                                       d->nbrs[d->nbr_base[l] + e], (unsigned long long)n);
+            }
+        }
+        auto* gr = new trim_graph;
+        gr->device = d->device;
+        try {
+            DevIndex& v = gr->dev.ix;
+            v.dim = d->dim;
+            v.dim_stride = round_up(d->dim, 4);
+            v.m = d->m;
+            v.ksub = d->ksub;
+            v.code_stride = round_up(d->m, 16);
+            v.nlist = 0;
+            v.sd_uniform = sub[0];
+            for (uint32_t j = 1; j < d->m; ++j)
+                if (sub[j] != sub[0])
+                    v.sd_uniform = 0;
+            v.n = n;
+            v.id_base = 0;
+            uint32_t* dsub = gr->alloc<uint32_t>(d->m);
+            uint32_t* doff = gr->alloc<uint32_t>(d->m);
+            CK(cudaMemcpy(dsub, sub.data(), sizeof(uint32_t) * d->m, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(doff, suboff.data(), sizeof(uint32_t) * d->m, cudaMemcpyHostToDevice));
+            v.sub_dims = dsub;
+            v.sub_offsets = doff;
+            float* cent = gr->alloc<float>(static_cast<size_t>(d->ksub) * d->dim);
+            CK(cudaMemcpy(cent, d->centroids, sizeof(float) * d->ksub * d->dim, kind));
+            v.centroids = cent;
+            uint8_t* codes = gr->alloc<uint8_t>(n * v.code_stride);
+            CK(cudaMemset(codes, 0, n * v.code_stride));
+            CK(cudaMemcpy2D(codes, v.code_stride, d->codes, d->code_stride, d->m, n, kind));
+            v.codes = codes;
+            float* lx = gr->alloc<float>(n);
+            CK(cudaMemcpy(lx, d->lx, sizeof(float) * n, kind));
+            v.lx = lx;
+            float* vec = gr->alloc<float>(n * v.dim_stride);
+            CK(cudaMemset(vec, 0, sizeof(float) * n * v.dim_stride));
+            CK(cudaMemcpy2D(vec, sizeof(float) * v.dim_stride, d->vectors, sizeof(float) * d->dim,
+                            sizeof(float) * d->dim, n, kind));
+            v.vectors = vec;
+            uint64_t* offs = gr->alloc<uint64_t>(L * (n + 1));
+            CK(cudaMemcpy(offs, d->offsets, sizeof(uint64_t) * L * (n + 1), kind));
+            uint64_t* base = gr->alloc<uint64_t>(L);
+            CK(cudaMemcpy(base, d->nbr_base, sizeof(uint64_t) * L, kind));
+            uint32_t* nb = gr->alloc<uint32_t>(std::max<uint64_t>(d->total_nbrs, 1));
+            if (d->total_nbrs)
+                CK(cudaMemcpy(nb, d->nbrs, sizeof(uint32_t) * d->total_nbrs, kind));
+            gr->dev.levels = d->levels;
+            gr->dev.entry = d->entry;
+            gr->dev.offsets = offs;
+            gr->dev.nbr_base = base;
+            gr->dev.nbrs = nb;
+            CK(cudaDeviceSynchronize());
+        } catch (...) {
+            delete gr;
+            throw;
+        }
+        *out = gr;
+        return TRIM_OK;
+    });
+}
+
+int trim_graph_destroy(trim_graph_t graph) {
+    delete graph;
+    return TRIM_OK;
+}
+
+int trim_graph_search_knn(trim_graph_t gr, const float* queries, uint64_t nq, uint32_t k, uint32_t ef,
+                          float gamma, uint32_t* ids_out, float* dist_out, trim_counters* counters_out) {
+    if (!gr || (nq && (!queries || !ids_out || !dist_out)))
+        return set_err(TRIM_EINVAL, "search_trim_knn: null argument");
+    if (k == 0 || k > ef)
+        return set_err(TRIM_EINVAL, "search_trim_knn: need 1 <= k <= ef");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_knn: uncalibrated pruning profile");
+    if (ef > 256)
+        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 256 is not supported on the GPU path");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(gr->device);
+        cudaStream_t st = thread_stream(gr->device);
+        DevBuf d_q = graph_upload_queries(gr, queries, nq, st);
+        DevBuf d_ids(sizeof(uint32_t) * nq * k, st), d_dist(sizeof(float) * nq * k, st),
+            d_ct(sizeof(unsigned long long) * nq * 6, st);
+        graph_run(gr, d_q.as<float>(), nq, k, ef, gamma, false, nullptr, d_ids.as<uint32_t>(),
+                  d_dist.as<float>(), nullptr, 0, nullptr, d_ct.as<unsigned long long>(), st);
+        std::vector<unsigned long long> ct(nq * 6);
+        CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(uint32_t) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(dist_out, d_dist.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ct.data(), d_ct.p, sizeof(unsigned long long) * nq * 6, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (counters_out)
+            put_counters_host(counters_out, ct, nq);
+        return TRIM_OK;
+    });
+}
+
+int trim_graph_search_range(trim_graph_t gr, const float* queries, uint64_t nq, const float* radius,
+                            uint32_t ef, float gamma, uint64_t* offsets_out, uint32_t** ids_out,
+                            float** dist_out, trim_counters* counters_out) {
+    if (!gr || !offsets_out || !ids_out || !dist_out || (nq && (!queries || !radius)))
+        return set_err(TRIM_EINVAL, "search_trim_range: null argument");
+    *ids_out = nullptr;
+    *dist_out = nullptr;
+    for (uint64_t i = 0; i < nq; ++i)
+        if (radius[i] < 0.0f)
+            return set_err(TRIM_EINVAL, "search_trim_range: negative radius");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_range: uncalibrated pruning profile");
+    if (ef == 0 || ef > 256)
+        return set_err(TRIM_EINVAL, "search_trim_range: the GPU path needs 1 <= ef <= 256");
+    offsets_out[0] = 0;
+    if (nq == 0) {
+        *ids_out = static_cast<uint32_t*>(std::malloc(4));
+        *dist_out = static_cast<float*>(std::malloc(4));
+        return TRIM_OK;
+    }
+    return guarded([&]() -> int {
+        DeviceGuard g(gr->device);
+        cudaStream_t st = thread_stream(gr->device);
+        DevBuf d_q = graph_upload_queries(gr, queries, nq, st);
+        std::vector<float> r2(nq); // search.hpp:278: radius * radius in fp32
+        for (uint64_t i = 0; i < nq; ++i)
+            r2[i] = radius[i] * radius[i];
+        DevBuf d_r2(sizeof(float) * nq, st), d_counts(sizeof(unsigned long long) * nq, st),
+            d_ct(sizeof(unsigned long long) * nq * 6, st);
+        CK(cudaMemcpyAsync(d_r2.p, r2.data(), sizeof(float) * nq, cudaMemcpyHostToDevice, st));
+        uint64_t cap = std::min<uint64_t>(gr->dev.ix.n, 1024);
+        std::vector<unsigned long long> cnt(nq);
+        DevBuf d_pool;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            d_pool = DevBuf(sizeof(unsigned long long) * nq * cap, st);
+            graph_run(gr, d_q.as<float>(), nq, 0, ef, gamma, true, d_r2.as<float>(), nullptr, nullptr,
+                      d_pool.as<unsigned long long>(), cap, d_counts.as<unsigned long long>(),
+                      d_ct.as<unsigned long long>(), st);
+            CK(cudaMemcpyAsync(cnt.data(), d_counts.p, sizeof(unsigned long long) * nq, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const unsigned long long mx = *std::max_element(cnt.begin(), cnt.end());
+            if (mx <= cap)
+                break;
+            cap = mx; // the exact size: the second run cannot overflow
+        }
+        // per-query sort by (dist, id) — search.hpp:336
+        std::vector<uint64_t> beg(nq), endv(nq);
+        uint64_t tot = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            beg[i] = i * cap;
+            endv[i] = i * cap + cnt[i];
+            offsets_out[i] = tot;
+            tot += cnt[i];
+        }
+        offsets_out[nq] = tot;
+        DevBuf d_beg(sizeof(uint64_t) * nq, st), d_end(sizeof(uint64_t) * nq, st),
+            d_sorted(sizeof(unsigned long long) * std::max<uint64_t>(nq * cap, 1), st);
+        CK(cudaMemcpyAsync(d_beg.p, beg.data(), sizeof(uint64_t) * nq, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_end.p, endv.data(), sizeof(uint64_t) * nq, cudaMemcpyHostToDevice, st));
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, d_pool.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(), static_cast<int64_t>(nq * cap),
+                                              static_cast<int64_t>(nq), d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        DevBuf d_tmp(tmp_bytes, st);
+        CK(cub::DeviceSegmentedSort::SortKeys(d_tmp.p, tmp_bytes, d_pool.as<unsigned long long>(),
+                                              d_sorted.as<unsigned long long>(), static_cast<int64_t>(nq * cap),
+                                              static_cast<int64_t>(nq), d_beg.as<uint64_t>(), d_end.as<uint64_t>(), st));
+        DevBuf d_offs(sizeof(uint64_t) * (nq + 1), st);
+        CK(cudaMemcpyAsync(d_offs.p, offsets_out, sizeof(uint64_t) * (nq + 1), cudaMemcpyHostToDevice, st));
+        DevBuf d_ids(sizeof(uint32_t) * std::max<uint64_t>(tot, 1), st),
+            d_dist(sizeof(float) * std::max<uint64_t>(tot, 1), st);
+        trim_unpack_keys_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(
+            d_sorted.as<unsigned long long>(), static_cast<uint32_t>(cap), d_offs.as<uint64_t>(), nq,
+            d_ids.as<uint32_t>(), d_dist.as<float>());
+        CK(cudaGetLastError());
+        auto* hid = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<uint64_t>(tot, 1)));
+        auto* hd = static_cast<float*>(std::malloc(sizeof(float) * std::max<uint64_t>(tot, 1)));
+        if (!hid || !hd) {
+            std::free(hid);
+            std::free(hd);
+            return set_err(TRIM_ENOMEM, "search_trim_range: result allocation failed");
+        }
+        std::vector<unsigned long long> ct(nq * 6);
+        CK(cudaMemcpyAsync(hid, d_ids.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hd, d_dist.p, sizeof(float) * tot, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ct.data(), d_ct.p, sizeof(unsigned long long) * nq * 6, cudaMemcpyDeviceToHost, st));
+        cudaError_t se = cudaStreamSynchronize(st);
+        if (se != cudaSuccess) {
+            std::free(hid);
+            std::free(hd);
+            CK(se);
+        }
+        if (counters_out)
+            put_counters_host(counters_out, ct, nq);
+        *ids_out = hid;
+        *dist_out = hd;
         return TRIM_OK;
     });
 }

@@ -12,6 +12,12 @@ namespace trimgpu {
 struct KnnParams;
 struct RangeParams;
 struct BlParams;
+struct GraphDev;
+struct GraphParams;
+
+// trim_graph.cu: trim_graph_kernel<S> (candidate queue capacity 32*S).
+cudaError_t launch_graph(const GraphDev& g, const GraphParams& p, uint32_t S, size_t smem,
+                         cudaStream_t st);
 
 #define TRIM_DECLARE_LAUNCHERS(MV)                                                                \
     cudaError_t launch_knn_##MV(const DevIndex& ix, const KnnParams& p, size_t smem,             \

@@ -12,7 +12,42 @@ FIELDS = ("dim", "m", "ksub", "sub_dims", "centroids", "coarse", "list_offsets",
 
 
 def names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """IVF / flat fixtures (graph fixtures: graph_names())."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("graph_"))
+
+
+def graph_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "graph_*.npz")))
+
+
+GRAPH_FIELDS = ("entry", "M", "efc", "ksub", "sub_dims", "centroids", "codes", "lx", "vectors")
+
+
+def load_graph(name):
+    """(graph namespace with per-level offsets/nbrs + landmark store, queries, cases)."""
+    z = np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
+    g = SimpleNamespace(**{f: (z[f].item() if z[f].ndim == 0 else z[f]) for f in GRAPH_FIELDS})
+    lv = int(z["levels"])
+    g.offsets = [z[f"offsets_{i}"] for i in range(lv)]
+    g.nbrs = [z[f"nbrs_{i}"] for i in range(lv)]
+    g.n, g.dim = g.vectors.shape
+    g.m = g.codes.shape[1]
+    cases = {}
+    for c in z["cases"]:
+        c = str(c)
+        d = {key[len(c) + 2:]: (z[key].item() if z[key].ndim == 0 else z[key])
+             for key in z.files if key.startswith(c + "__")}
+        d["kind"] = str(d["kind"])
+        cases[c] = d
+    return g, z["queries"], cases
+
+
+def host_graph(g):
+    from oracle.oracle import HostGraph
+    return HostGraph(n=g.n, M=g.M, efc=g.efc, entry=g.entry, offsets=list(g.offsets), nbrs=list(g.nbrs),
+                     dim=g.dim, m=g.m, ksub=g.ksub, sub_dims=g.sub_dims, centroids=g.centroids,
+                     codes=g.codes, lx=g.lx, vectors=g.vectors)
 
 
 def load(name):

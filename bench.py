@@ -51,6 +51,11 @@ CONFIGS = {
     # scaling: --gpus 8 is the 800M configuration), batches of 2048
     "c5": dict(workload="flat_trim_knn_100M_per_gpu_d96", n=100_000_000, dim=96, n_centers=4096, sigma=0.3,
                nq=10_000, batch=2048, m=48, nlist=1, nprobe=1, k=10, gammas=[0.8], gamma=0.8),
+    # the TRIM filter over a search graph (graph/search.hpp:188-264) on
+    # config-1 data; level 0 = 32 exact nearest rows + 8 random long-range links per node
+    "g1": dict(kind="graph", workload="graph_trim_knn_100k_d128_deg40", n=100_000, dim=128, n_centers=64,
+               sigma=0.3, nq=10_000, batch=2048, m=16, nlist=1, nprobe=1, k=10, ef=64, M=32, n_random=8,
+               gammas=[0.0, 1.0], gamma=0.8),
     # BASELINE.json configs[0] (CPU-runnable reference case; parity + extra line)
     "c1": dict(workload="flat_trim_knn_100k_d128", n=100_000, dim=128, n_centers=64, sigma=0.3,
                nq=1000, batch=1000, m=16, nlist=1, nprobe=1, k=10, gammas=[0.0, 0.605, 1.0],
@@ -794,6 +799,249 @@ def run_ours_range(args, cfg):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------ graph filter (g1)
+def build_graph_workload(cfg, device):
+    """Config-1 data on the device, a flat index (landmarks: pq::train +
+    encode), and the kNN + random-link graph over it (builder.build_knn_graph)."""
+    import torch
+
+    from paper_2508_17828_b200 import builder as B
+    from paper_2508_17828_b200.ivf import GpuIvfIndex
+    t0 = time.time()
+    centers = B.synth_normal(cfg["n_centers"], cfg["dim"], seed=0, device=device)
+    base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1)
+    queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
+    arrays = B.build_ivf(base, B.BuildParams(m=cfg["m"], nlist=1, pq_seed=3))
+    gix = GpuIvfIndex(arrays, device=device)
+    ga = B.knn_graph_from_flat(arrays, gix, cfg["M"], cfg["n_random"], seed=5)
+    torch.cuda.synchronize()
+    log(f"built {cfg['workload']} in {time.time() - t0:.1f}s")
+    return arrays, gix, ga, queries
+
+
+def _host_graph(ga):
+    from oracle.oracle import HostGraph
+    n, dim = ga.vectors.shape
+    return HostGraph(n=n, M=ga.M, efc=0, entry=ga.entry, offsets=ga.offsets, nbrs=ga.nbrs, dim=dim,
+                     m=ga.codes.shape[1], ksub=ga.ksub, sub_dims=ga.sub_dims, centroids=ga.centroids,
+                     codes=ga.codes, lx=ga.lx, vectors=ga.vectors)
+
+
+def graph_cpu_timer(ga, cfg, gamma, qs, budget_s, threads):
+    """The reference's graph::search_trim_knn (oracle/_ref, unmodified headers)
+    over a bounded query sample with all host threads, timed like run_queries
+    (sweep.hpp:121-152). -> (seconds, queries, counters[6])."""
+    from oracle import oracle as O
+    ref = O.RefOracle()
+    ref.set_threads(threads)
+    sess = ref.graph_session(_host_graph(ga))
+    try:
+        n0 = min(len(qs), max(4 * threads, 64))
+        sec, _ = ref.graph_session_run(sess, "trim_knn", qs[:n0], k=cfg["k"], ef=cfg["ef"], gamma=gamma)
+        n = int(min(len(qs), max(4 * threads, budget_s * n0 / max(sec, 1e-9))))
+        sec, ct = ref.graph_session_run(sess, "trim_knn", qs[:n], k=cfg["k"], ef=cfg["ef"], gamma=gamma)
+    finally:
+        ref.graph_session_destroy(sess)
+    return sec, n, ct
+
+
+def run_ours_graph(args, cfg):
+    import torch
+
+    from paper_2508_17828_b200 import graph as GG
+    from paper_2508_17828_b200.graph import GpuGraph
+    from paper_2508_17828_b200.ivf import PruningProfile
+
+    world, rank, local = dist_env()
+    if world > 1:  # replicas: the graph is small; every rank searches a slice of the queries
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch.distributed as dist
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    arrays, gix, ga, queries = build_graph_workload(cfg, local)
+    gg = GpuGraph(ga, device=local)
+    nq, B, k, ef = cfg["nq"], cfg["batch"], cfg["k"], cfg["ef"]
+    q_lo, q_hi = 0, nq
+    if world > 1:
+        from paper_2508_17828_b200.distributed import shard_bounds
+        q_lo, q_hi = shard_bounds(nq, rank, world)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    cts = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(max(1, args.streams) - 1)]
+    batches = [(b, min(B, q_hi - b)) for b in range(q_lo, q_hi, B)]
+
+    def step(gamma, ev=None):
+        prof = PruningProfile.manual(gamma)
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for x in streams[1:]:
+            x.wait_event(fork)
+        for i, (b0, nb) in enumerate(batches):
+            st_ = streams[i % len(streams)]
+            if ev is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(st_)
+            GG.search_trim_knn_device(gg, prof, queries[b0:b0 + nb], k, ef, ids[b0:b0 + nb], dists[b0:b0 + nb],
+                                      cts[b0:b0 + nb], stream=st_)
+            if ev is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(st_)
+                ev.append((e0, e1))
+        for x in streams[1:]:
+            j = torch.cuda.Event()
+            j.record(x)
+            stream.wait_event(j)
+        return len(batches)
+
+    def timed(gamma, steps, warmup, clocks=None):
+        for _ in range(warmup):
+            step(gamma)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev = []
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches = 0
+        with (clocks if clocks is not None else _Null()):
+            s0.record(stream)
+            for _ in range(steps):
+                launches += step(gamma, ev)
+            s1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = s0.elapsed_time(s1)
+        iv = sorted((s0.elapsed_time(a), s0.elapsed_time(b)) for a, b in ev)
+        busy, cur = 0.0, None
+        for a, b in iv:
+            if cur is None or a > cur[1]:
+                if cur is not None:
+                    busy += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        if cur is not None:
+            busy += cur[1] - cur[0]
+        ct = cts[q_lo:q_hi].sum(0).cpu().numpy()
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            ctt = torch.from_numpy(ct.astype(np.int64)).to(dev)
+            dist.all_reduce(ctt)
+            ct = ctt.cpu().numpy()
+        return ms, busy, len(ev), ct, launches
+
+    def rec(nsample):
+        if world > 1 or nsample <= 0:
+            return None
+        from paper_2508_17828_b200 import ivf as G
+        gt, _ = G.ground_truth_knn(gix, queries[:nsample].cpu().numpy(), k)
+        got = ids[:nsample].cpu().numpy().view(np.uint32)
+        return sum(len(set(gt[i].tolist()) & set(got[i].tolist())) for i in range(len(gt))) / (k * len(gt))
+
+    head = args.gamma if args.gamma else cfg["gamma"]
+    sweep = {}
+    for g in ([] if args.gamma else cfg["gammas"]):
+        ms, _, _, ct, _ = timed(g, 1, 1)
+        sweep[str(g)] = dict(ms_per_step=ms, cand_per_s=float(ct[3]) / (ms / 1e3), qps=(q_hi - q_lo) * world / (ms / 1e3),
+                             prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])), hops_per_query=float(ct[4]) / nq,
+                             **{f"recall@{k}": rec(args.recall_q)})
+    clk = ClockSampler(local)
+    ms, busy, nl, ct, launches = timed(head, args.steps, args.warmup, clk)
+    evaluated, dc = float(ct[3]), float(ct[0])
+    value = evaluated * args.steps / (ms / 1e3)
+    m, D = cfg["m"], cfg["dim"]
+    s_frac = dc / max(1.0, evaluated)
+    bpc = m + 4 + 4 + s_frac * 4 * D  # code + Γ(l,x) + neighbour id + exact rows
+    per_launch = evaluated * bpc / max(1, nl // args.steps) / world
+    achieved = per_launch / (busy / max(1, nl) / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    out = dict(metric="candidates filtered/sec (TRIM graph filter, graph/search.hpp:188-264; QPS, prune ratio alongside)",
+               value=value, unit="candidates/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+               ms_per_step=ms / args.steps, higher_is_better=True, scaling="strong" if world > 1 else "weak",
+               vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic",
+               config=dict(workload=cfg["workload"], n=cfg["n"], dim=D, queries=nq, batch=B, m=m, k=k, ef=ef,
+                           degree=cfg["M"] + cfg["n_random"], levels=1, gamma=head,
+                           parallelism=f"replicas x{world}" if world > 1 else "single",
+                           l2="graph + vectors + codes (~60 MB) fit L2; reported as-is",
+                           data_gen="device Philox blobs (config-1 shape), seeds centers=0 base=1 queries=2; "
+                                    "graph = 32 exact NN (trim_ground_truth_knn) + 8 seeded random links"),
+               qps=(q_hi - q_lo) * world * args.steps / (ms / 1e3),
+               prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])), hops_per_query=float(ct[4]) / nq,
+               candidates_per_query=evaluated / nq)
+    out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                           traffic=ncu_traffic(cfg["workload"]), kernel="trim_graph_kernel",
+                           bytes_per_candidate=bpc, peak_source=peak_src, filter_share_of_step=busy / ms,
+                           note="one warp per query walks the graph: latency-bound (dependent hops), not "
+                                "bandwidth-bound")
+    out["gpu_launches"] = launches
+    out["clocks"] = clk.summary()
+    out["sweep"] = sweep
+    out[f"recall@{k}"] = rec(args.recall_q)
+    if rank == 0:
+        # e2e: the C-ABI host call (pinned host queries in, results + counters out)
+        hq = queries[q_lo:q_hi].cpu().pin_memory().numpy()
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(max(1, args.streams))
+        prof = PruningProfile.manual(head)
+
+        def one(b):
+            _, _, c = GG.search_trim_knn_batch(gg, prof, hq[b:b + B], k, ef)
+            return int(c[:, 3].sum())
+        sum(pool.map(one, range(0, len(hq), B)))
+        t0 = time.perf_counter()
+        cand = sum(pool.map(one, range(0, len(hq), B)))
+        sec = time.perf_counter() - t0
+        out["e2e"] = dict(value=cand / sec, unit="candidates/s", qps=len(hq) / sec,
+                          h2d_bytes_per_step=len(hq) * D * 4, d2h_bytes_per_step=len(hq) * (k * 8 + 48),
+                          api=f"trim_graph_search_knn (C ABI, host buffers; {max(1, args.streams)} client threads)")
+        if world == 1 and not args.skip_cpu:
+            threads = os.cpu_count() or 1
+            sec, n, cct = graph_cpu_timer(ga, cfg, head, queries.cpu().numpy(), args.cpu_seconds, threads)
+            out["cpu_baseline"] = dict(value=float(cct[3]) / sec, unit="candidates/s", cores=threads, kind="reference",
+                                       sample=f"first {n} of {nq} queries of {cfg['workload']} at gamma={head}, "
+                                              f"{threads} threads, {sec:.1f}s",
+                                       qps=n / sec, prune_ratio=float(cct[2] / max(1, cct[2] + cct[0])))
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference_graph(args, cfg):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    torch.cuda.set_device(local)
+    arrays, gix, ga, queries = build_graph_workload(cfg, local)
+    head = args.gamma if args.gamma else cfg["gamma"]
+    threads = os.cpu_count() or 1
+    qs = queries.cpu().numpy()
+    per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    secs, evs, nqs = 0.0, 0, 0
+    for i in range(args.warmup + args.steps):
+        sec, n, ct = graph_cpu_timer(ga, cfg, head, np.roll(qs, -i * 97, 0), per, threads)
+        if i >= args.warmup:
+            secs, evs, nqs = secs + sec, evs + int(ct[3]), nqs + n
+    value = evs / secs
+    out = dict(metric="candidates filtered/sec (TRIM graph filter, graph/search.hpp:188-264; QPS, prune ratio alongside)",
+               value=value, unit="candidates/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+               ms_per_step=secs * 1e3 / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+               dtype="f32 (u8 PQ codes)", data="synthetic", impl="reference",
+               config=dict(workload=cfg["workload"], n=cfg["n"], dim=cfg["dim"], queries=cfg["nq"], m=cfg["m"],
+                           k=cfg["k"], ef=cfg["ef"], gamma=head),
+               qps=nqs / secs,
+               cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind="reference",
+                                 sample=f"~{nqs // max(1, args.steps)} queries per step of {cfg['workload']}, "
+                                        f"{threads} threads"),
+               e2e=dict(value=value, unit="candidates/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(out), flush=True)
+
+
 # ------------------------------------------------------ reference CPU arm
 def run_reference(args, cfg):
     world, rank, local = dist_env()
@@ -872,7 +1120,9 @@ def main():
     if args.warmup < 3 and args.impl == "ours" and os.environ.get("BENCH_ALLOW_SHORT") != "1":
         log("note: the contract asks for >= 3 warm-up steps")
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference_graph(args, cfg) if cfg.get("kind") == "graph" else run_reference(args, cfg)
+    elif cfg.get("kind") == "graph":
+        run_ours_graph(args, cfg)
     elif cfg.get("kind") == "range":
         run_ours_range(args, cfg)
     else:

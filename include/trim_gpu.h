@@ -316,6 +316,12 @@ int trim_graph_destroy(trim_graph_t graph);
 int trim_graph_search_knn(trim_graph_t graph, const float* queries, uint64_t nq, uint32_t k,
                           uint32_t ef, float gamma, uint32_t* ids_out, float* dist_out,
                           trim_counters* counters_out);
+/* Device-resident trim_graph_search_knn: device pointers on the graph's device
+ * (queries nq*dim, ids/dist nq*k, counters nq*6 u64 in trim_counters order),
+ * asynchronous on `stream` (cudaStream_t). */
+int trim_graph_search_knn_device(trim_graph_t graph, const float* d_queries, uint64_t nq, uint32_t k,
+                                 uint32_t ef, float gamma, uint32_t* d_ids, float* d_dist,
+                                 unsigned long long* d_counters, void* stream);
 /*
  * graph::search_trim_range (graph/search.hpp:267-347). radius: nq plain radii
  * (negative -> TRIM_EINVAL). Results as trim_search_range: offsets_out nq+1,

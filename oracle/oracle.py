@@ -395,6 +395,11 @@ class RefOracle:
         L.ref_graph_build.restype = C.c_void_p
         L.ref_graph_build.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
         L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_graph_session_create.restype = C.c_void_p
+        L.ref_graph_session_create.argtypes = [C.POINTER(_FlatGraph), C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
+                                               _f32p, _u8p, _f32p, _f32p]
+        L.ref_graph_session_run.argtypes = [C.c_void_p, C.c_int, _f32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                            C.c_double, C.c_double, _f64p, _u64p]
         L.ref_graph_info.argtypes = [C.c_void_p, _u32p, _u32p, _u64p]
         L.ref_graph_export.argtypes = [C.c_void_p, C.c_uint32, _u64p, _u32p]
         L.ref_graph_save.argtypes = [C.POINTER(_FlatGraph), C.c_char_p]
@@ -437,6 +442,32 @@ class RefOracle:
             self.lib.ref_graph_free(h)
         return HostGraph(n=n, M=M, efc=efc, entry=en.value, offsets=offs, nbrs=nbrs, dim=dim,
                          vectors=data)
+
+    def graph_session(self, g: HostGraph):
+        """Resident reference graph + landmarks + vectors (for timing)."""
+        fg, keep = g.flat()
+        arrs = [np.ascontiguousarray(g.sub_dims, np.uint32), np.ascontiguousarray(g.centroids, np.float32).ravel(),
+                np.ascontiguousarray(g.codes, np.uint8), np.ascontiguousarray(g.lx, np.float32),
+                np.ascontiguousarray(g.vectors, np.float32)]
+        h = self.lib.ref_graph_session_create(C.byref(fg), g.dim, g.m, g.ksub, _ptr(arrs[0], _u32p),
+                                              _ptr(arrs[1], _f32p), _ptr(arrs[2], _u8p), _ptr(arrs[3], _f32p),
+                                              _ptr(arrs[4], _f32p))
+        if not h:
+            raise ValueError(f"graph_session: {self.lib.ref_last_error().decode()}")
+        return h
+
+    def graph_session_run(self, sess, kind: str, qs, *, k=0, ef=0, gamma=0.0, radius=0.0):
+        """-> (seconds, counters summed over the queries [6])."""
+        qs = np.ascontiguousarray(qs, np.float32)
+        sec = C.c_double(0)
+        ct = np.zeros(6, np.uint64)
+        self._err(self.lib.ref_graph_session_run(sess, {"trim_knn": 0, "trim_range": 1}[kind], _ptr(qs, _f32p),
+                                                 qs.shape[0], k, ef, gamma, radius, C.byref(sec), _ptr(ct, _u64p)),
+                  "graph_session_run")
+        return sec.value, ct
+
+    def graph_session_destroy(self, sess):
+        self.lib.ref_graph_free(sess)
 
     def graph_save(self, g: HostGraph, path: str):
         fg, keep = g.flat()

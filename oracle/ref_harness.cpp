@@ -169,6 +169,8 @@ trim::LandmarkStore make_lm(std::uint32_t dim, std::uint32_t m, std::uint32_t c,
 
 struct GraphSession {
     graph::GraphIndex g;
+    trim::LandmarkStore lm;
+    VectorDataset ds;
 };
 
 } // namespace
@@ -690,6 +692,46 @@ int ref_graph_search_batch(const FlatGraph* fg, std::uint32_t dim, std::uint32_t
         for (const auto& e : errs)
             if (!e.empty())
                 throw std::invalid_argument(e);
+    });
+}
+
+// A resident graph + landmarks + dataset for timing the reference's graph
+// searches like bench::detail_sweep::run_queries (sweep.hpp:121-152).
+void* ref_graph_session_create(const FlatGraph* fg, std::uint32_t dim, std::uint32_t m, std::uint32_t c,
+                               const std::uint32_t* sub_dims, const float* centroids, const std::uint8_t* codes,
+                               const float* lx, const float* data) {
+    auto* s = new GraphSession;
+    const int rc = guarded([&] {
+        s->g = make_graph(*fg);
+        s->lm = make_lm(dim, m, c, sub_dims, centroids, codes, lx, fg->n);
+        s->ds = make_ds(data, fg->n, dim);
+    });
+    if (rc != REF_OK) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+// kind 0: search_trim_knn (k, ef), 1: search_trim_range (arg = radius, ef).
+int ref_graph_session_run(void* p, int kind, const float* qs, std::uint64_t nq, std::uint32_t k,
+                          std::uint32_t ef, double gamma, double arg, double* seconds_out,
+                          std::uint64_t* counters_sum_out) {
+    auto* s = static_cast<GraphSession*>(p);
+    return guarded([&] {
+        const auto prof = trim::PruningProfile::manual(gamma);
+        std::vector<SearchCounters> cs(nq);
+        const auto t0 = std::chrono::steady_clock::now();
+        parallel_for(nq, [&](std::size_t qi) {
+            const VectorView q(qs + qi * s->ds.dim, s->ds.dim);
+            cs[qi] = kind == 0 ? graph::search_trim_knn(s->g, s->ds, s->lm, prof, q, k, ef).counters
+                               : graph::search_trim_range(s->g, s->ds, s->lm, prof, q, static_cast<float>(arg), ef)
+                                     .counters;
+        });
+        *seconds_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        SearchCounters tot;
+        for (const auto& c : cs)
+            tot += c;
+        put_counters(counters_sum_out, tot, 0);
     });
 }
 

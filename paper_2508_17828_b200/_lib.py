@@ -101,6 +101,8 @@ SIGNATURES = {
     "trim_graph_destroy": (C.c_int, [C.c_void_p]),
     "trim_graph_search_knn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
                                         C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "trim_graph_search_knn_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                               C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "trim_graph_search_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
                                           C.c_float, C.c_void_p, C.POINTER(_u32p), C.POINTER(_f32p),
                                           C.c_void_p]),

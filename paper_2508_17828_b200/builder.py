@@ -163,3 +163,63 @@ def to_host(a: IvfArrays) -> IvfArrays:
                      list_offsets=h(a.list_offsets, np.uint64), list_ids=h(a.list_ids, np.uint32),
                      list_codes=h(a.list_codes, np.uint8), list_lx=h(a.list_lx, np.float32),
                      vectors=h(a.vectors, np.float32), id_base=a.id_base)
+
+
+def build_knn_graph(x: torch.Tensor, M: int, n_random: int, m: int, ksub: int = 256, pq_iters: int = 25,
+                    pq_seed: int = 1, seed: int = 0):
+    """A single-level search graph for the graph filter benchmark (the HNSW
+    builder, graph/hnsw.hpp:165-268, is a sequential host loop and not on the
+    hot path): node i's list = its M exact nearest rows (trim_ground_truth_knn,
+    itself excluded) followed by n_random seeded random rows (long-range links);
+    entry 0. Landmarks: pq::train + encode on the device. Returns GraphArrays
+    (host numpy)."""
+    from .ivf import GpuIvfIndex
+
+    arrays = build_ivf(x, BuildParams(m=m, ksub=ksub, pq_iters=pq_iters, pq_seed=pq_seed, nlist=1))
+    gix = GpuIvfIndex(arrays, device=x.device.index or 0)
+    return knn_graph_from_flat(arrays, gix, M, n_random, seed)
+
+
+def knn_graph_from_flat(arrays: IvfArrays, gix, M: int, n_random: int, seed: int = 0):
+    """build_knn_graph over a flat index already on the device (list entry e =
+    row e): the landmark store is the index's codes / Γ(l,x)."""
+    from .graph import GraphArrays
+    from .ivf import ground_truth_knn
+
+    x = arrays.vectors
+    n, dim = x.shape
+    m = arrays.m
+    xh = x.cpu().numpy()
+    nbr = np.empty((n, M + 1), np.uint32)
+    for b0 in range(0, n, 65536):
+        nbr[b0:b0 + 65536] = ground_truth_knn(gix, xh[b0:b0 + 65536], M + 1)[0]
+    self_ = nbr == np.arange(n, dtype=np.uint32)[:, None]
+    # drop the row itself (or, with exact duplicates ahead of it, the last entry)
+    drop = np.where(self_.any(1), self_.argmax(1), M)
+    keep = np.ones_like(nbr, dtype=bool)
+    keep[np.arange(n), drop] = False
+    knn = nbr[keep].reshape(n, M)
+    rng = np.random.default_rng(seed)
+    rnd = rng.integers(0, n - 1, size=(n, n_random), dtype=np.uint32)
+    rnd = rnd + (rnd >= np.arange(n, dtype=np.uint32)[:, None])  # never the row itself
+    lists = np.concatenate([knn, rnd.astype(np.uint32)], 1)
+    # dedupe each list, first occurrence kept
+    srt = np.sort(lists, 1)
+    dup_any = (srt[:, 1:] == srt[:, :-1]).any(1)
+    sizes = np.full(n, lists.shape[1], np.uint64)
+    flat = lists.reshape(-1)
+    if dup_any.any():
+        parts = []
+        for i in range(n):
+            li = lists[i]
+            if dup_any[i]:
+                _, first = np.unique(li, return_index=True)
+                li = li[np.sort(first)]
+                sizes[i] = li.size
+            parts.append(li)
+        flat = np.concatenate(parts)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64)
+    h = to_host(arrays)
+    return GraphArrays(entry=0, offsets=[offs], nbrs=[flat.astype(np.uint32)], sub_dims=h.sub_dims,
+                       centroids=h.centroids, codes=np.ascontiguousarray(h.list_codes[:, :m]), lx=h.list_lx,
+                       vectors=xh, ksub=h.ksub, M=M)

@@ -893,7 +893,7 @@ void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32
     CK(cudaMemsetAsync(d_status.p, 0, sizeof(uint32_t) * nq, st));
     // TRIM_GRAPH_HEAP_CAP (tests): a smaller first search-queue capacity, so
     // the overflow re-run path runs on small graphs too
-    uint64_t cap0 = 1u << 16;
+    uint64_t cap0 = 1u << 14;
     if (const char* e = std::getenv("TRIM_GRAPH_HEAP_CAP"))
         cap0 = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     run(0, nq, std::min<uint64_t>(n + 1, cap0), d_status.as<uint32_t>());
@@ -1738,6 +1738,37 @@ int trim_graph_search_knn(trim_graph_t gr, const float* queries, uint64_t nq, ui
         CK(cudaStreamSynchronize(st));
         if (counters_out)
             put_counters_host(counters_out, ct, nq);
+        return TRIM_OK;
+    });
+}
+
+int trim_graph_search_knn_device(trim_graph_t gr, const float* d_queries, uint64_t nq, uint32_t k,
+                                 uint32_t ef, float gamma, uint32_t* d_ids, float* d_dist,
+                                 unsigned long long* d_counters, void* stream) {
+    if (!gr || (nq && (!d_queries || !d_ids || !d_dist || !d_counters)))
+        return set_err(TRIM_EINVAL, "search_trim_knn: null argument");
+    if (k == 0 || k > ef)
+        return set_err(TRIM_EINVAL, "search_trim_knn: need 1 <= k <= ef");
+    if (!(gamma >= 0.0f))
+        return set_err(TRIM_EINVAL, "search_trim_knn: uncalibrated pruning profile");
+    if (ef > 256)
+        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 256 is not supported on the GPU path");
+    if (nq == 0)
+        return TRIM_OK;
+    return guarded([&]() -> int {
+        DeviceGuard g(gr->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const uint32_t dim = gr->dev.ix.dim, ds = gr->dev.ix.dim_stride;
+        DevBuf d_pad;
+        const float* q = d_queries;
+        if (ds != dim) {
+            d_pad = DevBuf(sizeof(float) * nq * ds, st);
+            CK(cudaMemsetAsync(d_pad.p, 0, sizeof(float) * nq * ds, st));
+            CK(cudaMemcpy2DAsync(d_pad.p, sizeof(float) * ds, d_queries, sizeof(float) * dim, sizeof(float) * dim,
+                                 nq, cudaMemcpyDeviceToDevice, st));
+            q = d_pad.as<float>();
+        }
+        graph_run(gr, q, nq, k, ef, gamma, false, nullptr, d_ids, d_dist, nullptr, 0, nullptr, d_counters, st);
         return TRIM_OK;
     });
 }

@@ -108,6 +108,26 @@ def search_trim_knn_batch(g: GpuGraph, profile: PruningProfile, queries, k: int,
     return ids, dist, ct
 
 
+def search_trim_knn_device(g: GpuGraph, profile: PruningProfile, d_queries, k: int, ef: int, d_ids=None,
+                           d_dist=None, d_counters=None, stream=None):
+    """torch.cuda tensors in and out, async on `stream` (default: torch's current)."""
+    import torch
+
+    nq = d_queries.shape[0]
+    dev = d_queries.device
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev) if d_ids is None else d_ids
+    d_dist = torch.empty((nq, k), dtype=torch.float32, device=dev) if d_dist is None else d_dist
+    d_counters = torch.zeros((nq, 6), dtype=torch.int64, device=dev) if d_counters is None else d_counters
+    stream = torch.cuda.current_stream(dev) if stream is None else stream
+    sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    rc = _lib.load().trim_graph_search_knn_device(g.handle, C.c_void_p(d_queries.data_ptr()), nq, k, ef,
+                                                  profile.gamma_f32(), C.c_void_p(d_ids.data_ptr()),
+                                                  C.c_void_p(d_dist.data_ptr()), C.c_void_p(d_counters.data_ptr()),
+                                                  C.c_void_p(sh))
+    _lib.check(rc, "search_trim_knn")
+    return d_ids, d_dist, d_counters
+
+
 def search_trim_range_batch(g: GpuGraph, profile: PruningProfile, queries, radius, ef: int):
     """Batch graph::search_trim_range. Returns (offsets[nq+1], ids, dist_sq, counters[nq, 6])."""
     q = _queries(g, queries)

@@ -64,6 +64,8 @@ int guarded(Fn&& fn) {
         return e.code;
     } catch (const std::bad_alloc&) {
         return set_err(TRIM_ENOMEM, "host allocation failed");
+    } catch (const std::runtime_error& e) { // a nested trim_* call failed (message kept)
+        return set_err(TRIM_ECUDA, "%s", e.what());
     }
 }
 
@@ -857,7 +859,13 @@ void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32
     const GraphDev& g = gr->dev;
     const uint64_t n = g.ix.n, vwords = (n + 31) / 32;
     const uint32_t S = graph_slots(std::max(ef, range ? 1u : k));
-    const size_t smem = graph_smem_bytes(g.ix.m, g.ix.dim_stride);
+    // first run: the search queue in shared memory (TRIM_GRAPH_HEAP_CAP entries,
+    // default 1024; tests force overflows with a tiny one); overflowed queries
+    // are re-run with a global-memory queue of capacity n + 1 (exact)
+    uint64_t hs = 1024;
+    if (const char* e = std::getenv("TRIM_GRAPH_HEAP_CAP"))
+        hs = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    hs = std::min<uint64_t>(hs, n + 1);
     const size_t budget = size_t(1) << 30;
     GraphParams p{};
     p.k = k;
@@ -866,15 +874,23 @@ void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32
     p.range = range ? 1u : 0u;
     p.cap = cap;
     p.vwords = vwords;
-    auto run = [&](uint64_t q0, uint64_t nb, uint64_t heap_cap, uint32_t* d_status) {
-        const size_t per_q = vwords * 4 + heap_cap * 8;
+    // run queries [q0, q0 + nb), or the nb queries listed in d_map
+    auto run = [&](uint64_t q0, uint64_t nb, bool global_heap, const uint32_t* d_map, uint32_t* d_status) {
+        const uint64_t heap_cap = global_heap ? n + 1 : hs;
+        const size_t smem = graph_smem_bytes(g.ix.m, g.ix.dim_stride, global_heap ? 0 : hs);
+        if (smem > kSmemLimit) {
+            set_err(TRIM_EINVAL, "graph search: per-query shared memory (%zu B) exceeds 227 KB", smem);
+            throw CudaError{TRIM_EINVAL};
+        }
+        const size_t per_q = vwords * 4 + (global_heap ? heap_cap * 8 : 0);
         const uint64_t group = std::max<uint64_t>(1, std::min<uint64_t>(nb, budget / per_q));
-        DevBuf vis(vwords * 4 * group, st), heap(heap_cap * 8 * group, st);
+        DevBuf vis(vwords * 4 * group, st), heap(global_heap ? heap_cap * 8 * group : 8, st);
         for (uint64_t g0 = 0; g0 < nb; g0 += group) {
-            const uint64_t gn = std::min(group, nb - g0), qi = q0 + g0;
+            const uint64_t gn = std::min(group, nb - g0), qi = d_map ? 0 : q0 + g0;
             CK(cudaMemsetAsync(vis.p, 0, vwords * 4 * gn, st));
             GraphParams pp = p;
             pp.nq = gn;
+            pp.qmap = d_map ? d_map + g0 : nullptr;
             pp.queries = d_q + qi * g.ix.dim_stride;
             pp.r2 = range ? d_r2 + qi : nullptr;
             pp.ids_out = range ? nullptr : d_ids + qi * k;
@@ -883,31 +899,30 @@ void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32
             pp.counts = range ? d_counts + qi : nullptr;
             pp.counters = d_ct + qi * 6;
             pp.visited = vis.as<uint32_t>();
-            pp.heap = heap.as<unsigned long long>();
+            pp.heap = global_heap ? heap.as<unsigned long long>() : nullptr;
             pp.heap_cap = heap_cap;
-            pp.status = d_status + g0;
+            pp.status = d_status + qi;
             CK(launch_graph(g, pp, S, smem, st));
         }
     };
     DevBuf d_status(sizeof(uint32_t) * std::max<uint64_t>(nq, 1), st);
     CK(cudaMemsetAsync(d_status.p, 0, sizeof(uint32_t) * nq, st));
-    // TRIM_GRAPH_HEAP_CAP (tests): a smaller first search-queue capacity, so
-    // the overflow re-run path runs on small graphs too
-    uint64_t cap0 = 1u << 14;
-    if (const char* e = std::getenv("TRIM_GRAPH_HEAP_CAP"))
-        cap0 = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
-    run(0, nq, std::min<uint64_t>(n + 1, cap0), d_status.as<uint32_t>());
-    if (n + 1 <= cap0)
+    run(0, nq, false, nullptr, d_status.as<uint32_t>());
+    if (hs >= n + 1)
         return;
     std::vector<uint32_t> status(nq);
     CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(uint32_t) * nq, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    DevBuf d_st1(sizeof(uint32_t), st);
+    std::vector<uint32_t> redo;
     for (uint64_t i = 0; i < nq; ++i)
-        if (status[i] & 1u) {
-            CK(cudaMemsetAsync(d_st1.p, 0, sizeof(uint32_t), st));
-            run(i, 1, n + 1, d_st1.as<uint32_t>());
-        }
+        if (status[i] & 1u)
+            redo.push_back(static_cast<uint32_t>(i));
+    if (redo.empty())
+        return;
+    DevBuf d_map(sizeof(uint32_t) * redo.size(), st);
+    CK(cudaMemcpyAsync(d_map.p, redo.data(), sizeof(uint32_t) * redo.size(), cudaMemcpyHostToDevice, st));
+    run(0, redo.size(), true, d_map.as<uint32_t>(), d_status.as<uint32_t>());
+    CK(cudaStreamSynchronize(st)); // d_map / redo stay alive until the re-run is done
 }
 
 DevBuf graph_upload_queries(const trim_graph* gr, const float* q, uint64_t nq, cudaStream_t st) {

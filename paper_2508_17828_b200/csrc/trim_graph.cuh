@@ -19,10 +19,15 @@
 //     the keys are unique (every node is pushed at most once), so the kept set
 //     and the heap top are those of the reference whatever the heap layout;
 //   * the search queue S (unbounded min-heap by bound) is a binary heap of
-//     (key bits << 32 | id) words in global memory (L1-resident near the top),
-//     owned by lane 0; u64 order = ScoredId order for non-negative keys.
-// Queries whose S outgrows its capacity set status bit 0 and are re-run by the
-// host with a capacity of n + 1 (trim_capi.cu).
+//     (key bits << 32 | id) words owned by lane 0, in shared memory; u64
+//     order = ScoredId order for non-negative keys. Once C is full its top
+//     max_can_dis only falls, so an entry keyed above it can never be popped
+//     before the search stops (the reference breaks on the first such pop,
+//     search.hpp:222-223, and stops identically on an empty queue): such
+//     entries are not pushed, and are purged when the heap fills.
+// Queries whose S still outgrows the shared-memory heap set status bit 0 and
+// are re-run by the host with a global-memory heap of capacity n + 1
+// (trim_capi.cu).
 #pragma once
 
 #include "trim_adc.cuh"
@@ -58,44 +63,29 @@ struct GraphParams {
     unsigned long long* counters; // nq x 6
     uint32_t* visited;   // nq x vwords bitmap, zeroed
     uint64_t vwords;
-    unsigned long long* heap; // nq x heap_cap
+    unsigned long long* heap; // nq x heap_cap in global memory, or null: heap_cap entries in shared memory
     uint64_t heap_cap;
     uint32_t* status;    // nq flags: bit 0 = search queue overflow (re-run)
+    const uint32_t* qmap; // null, or the query index of each CTA (re-runs of a subset)
 };
 
 constexpr uint32_t kGraphThreads = 32;
 
-__host__ __device__ inline size_t graph_smem_bytes(uint32_t m, uint32_t dim_stride) {
-    return lut_bytes(0, m) + sizeof(float) * dim_stride;
+__host__ __device__ inline size_t graph_smem_bytes(uint32_t m, uint32_t dim_stride, uint64_t smem_heap) {
+    const size_t b = (lut_bytes(0, m) + sizeof(float) * dim_stride + 7) & ~size_t(7);
+    return b + sizeof(unsigned long long) * smem_heap;
 }
 
 __device__ __forceinline__ unsigned long long skey(float d, uint32_t id) {
     return (static_cast<unsigned long long>(__float_as_uint(d)) << 32) | id;
 }
 
-// Lane 0's binary min-heap (std::priority_queue<ScoredId, ..., greater>).
-struct GlobalMinHeap {
+// Lane 0's binary min-heap (std::priority_queue<ScoredId, ..., greater>), in
+// shared or global memory (generic addressing).
+struct MinHeap {
     unsigned long long* h;
     uint64_t n, cap;
-    __device__ __forceinline__ bool push(unsigned long long x) {
-        if (n == cap)
-            return false;
-        uint64_t i = n++;
-        while (i > 0) {
-            const uint64_t p = (i - 1) >> 1;
-            const unsigned long long hp = h[p];
-            if (hp <= x)
-                break;
-            h[i] = hp;
-            i = p;
-        }
-        h[i] = x;
-        return true;
-    }
-    __device__ __forceinline__ unsigned long long pop() {
-        const unsigned long long top = h[0];
-        const unsigned long long x = h[--n];
-        uint64_t i = 0;
+    __device__ __forceinline__ void sift_down(uint64_t i, unsigned long long x) {
         for (;;) {
             uint64_t c = 2 * i + 1;
             if (c >= n)
@@ -113,11 +103,78 @@ struct GlobalMinHeap {
             h[i] = hc;
             i = c;
         }
+        h[i] = x;
+    }
+    // Drop the entries keyed above `bound` (never popped before the search
+    // stops) and re-heapify. Returns false if nothing could be dropped.
+    __device__ __forceinline__ bool purge(unsigned long long bound) {
+        uint64_t w = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (h[i] <= bound)
+                h[w++] = h[i];
+        if (w == n)
+            return false;
+        n = w;
+        for (uint64_t i = n / 2; i-- > 0;)
+            sift_down(i, h[i]);
+        return true;
+    }
+    // Push unless `x` is above `bound`; false when the heap is full.
+    __device__ __forceinline__ bool push(unsigned long long x, unsigned long long bound) {
+        if (x > bound)
+            return true;
+        if (n == cap && !purge(bound))
+            return false;
+        uint64_t i = n++;
+        while (i > 0) {
+            const uint64_t p = (i - 1) >> 1;
+            const unsigned long long hp = h[p];
+            if (hp <= x)
+                break;
+            h[i] = hp;
+            i = p;
+        }
+        h[i] = x;
+        return true;
+    }
+    __device__ __forceinline__ unsigned long long pop() {
+        const unsigned long long top = h[0];
+        const unsigned long long x = h[--n];
         if (n)
-            h[i] = x;
+            sift_down(0, x);
         return top;
     }
 };
+
+// pq::adc_lookup (pq.hpp:186-192) of one code row in the reference order
+// (sequential fp32 sum, j = 0..m-1) over the blocked LUT, as adc_serial, but
+// with the code bytes fetched 16 at a time (rows are 16-byte aligned and
+// zero-padded; a padded byte reads a zeroed LUT column, and acc + 0.0f == acc
+// for the non-negative running sum), the next 16 in flight while the current
+// ones are summed.
+__device__ __forceinline__ float adc_serial_row(const uint8_t* __restrict__ code, uint32_t m) {
+    const LutShape sh = LutShape::of(m);
+    const uint32_t base = lut_saddr();
+    const uint32_t hbase = base + sh.nfull * kFullBytes, hrow = sh.half_row_bytes();
+    const uint4* c4 = reinterpret_cast<const uint4*>(code);
+    float acc = 0.0f;
+    uint4 nxt = __ldg(c4);
+    for (uint32_t j0 = 0; j0 < m; j0 += 16) {
+        const uint4 w = nxt;
+        if (j0 + 16 < m)
+            nxt = __ldg(c4 + (j0 >> 4) + 1);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        const uint32_t bb = j0 >> 5, t0 = j0 & 31u;
+        const uint32_t rb = bb < sh.nfull ? base + bb * kFullBytes : hbase;
+        const uint32_t rs = bb < sh.nfull ? 128u : hrow;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xFFu;
+            acc = __fadd_rn(acc, lds_f32(rb + c * rs + 4u * (t0 + t)));
+        }
+    }
+    return acc;
+}
 
 // The (d, id) lexicographic minimum over the warp (lanes with valid == false
 // contribute nothing); result in every lane.
@@ -140,12 +197,15 @@ __device__ __forceinline__ void warp_argmin(float& d, uint32_t& id, bool valid) 
 template <int S>
 __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, GraphParams p) {
     const DevIndex& ix = g.ix;
-    const uint32_t q = blockIdx.x;
-    if (q >= p.nq)
+    if (blockIdx.x >= p.nq)
         return;
+    const uint32_t slot = blockIdx.x;                      // workspace slot
+    const uint32_t q = p.qmap ? p.qmap[slot] : slot;       // query (inputs, outputs)
     const uint32_t lane = threadIdx.x;
     float* lut = reinterpret_cast<float*>(trim_dyn_smem); // offset 0 (lut_saddr)
     float* qv = lut + lut_bytes(0, ix.m) / sizeof(float);
+    unsigned long long* sheap = reinterpret_cast<unsigned long long*>(
+        trim_dyn_smem + ((lut_bytes(0, ix.m) + sizeof(float) * ix.dim_stride + 7) & ~size_t(7)));
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = lane; i < ix.dim_stride; i += kWarp)
         qv[i] = qg[i];
@@ -198,12 +258,16 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
     }
 
     // ---- the TRIM walk on level 0 (search.hpp:206-262 / 284-333)
-    uint32_t* vis = p.visited + static_cast<size_t>(q) * p.vwords;
-    GlobalMinHeap sq{p.heap + static_cast<size_t>(q) * p.heap_cap, 0, p.heap_cap};
+    uint32_t* vis = p.visited + static_cast<size_t>(slot) * p.vwords;
+    MinHeap sq{p.heap ? p.heap + static_cast<size_t>(slot) * p.heap_cap : sheap, 0, p.heap_cap};
     WarpTopK<S> cand, res;
     cand.init(p.ef);
     res.init(p.range ? 1u : p.k);
     uint32_t cand_n = 0;
+    // entries above max_can_dis (C full) are dead: the bound for pushes
+    auto live_bound = [&]() -> unsigned long long {
+        return cand_n == p.ef ? skey(cand.wd, 0xFFFFFFFFu) : ~0ull;
+    };
     const float r2 = p.range ? p.r2[q] : 0.0f;
     unsigned long long nres = 0;
     unsigned long long* pool = p.range ? p.pool + static_cast<size_t>(q) * p.cap : nullptr;
@@ -212,11 +276,11 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
     if (lane == 0)
         atomicOr(vis + (cur >> 5), 1u << (cur & 31u));
     {
-        const float glq = __fsqrt_rn(adc_serial<0>(ix.codes + static_cast<size_t>(cur) * ix.code_stride, ix.m));
+        const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(cur) * ix.code_stride, ix.m));
         ++edc;
         const float plb = relaxed_lb(glq, __ldg(ix.lx + cur), p.two_gamma);
         if (lane == 0)
-            overflow = !sq.push(skey(plb, cur));
+            overflow = !sq.push(skey(plb, cur), ~0ull);
         cand.offer(cur_d, cur);
         cand_n = 1;
         if (!p.range) {
@@ -259,7 +323,7 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
             }
             float plb = 0.0f, d = 0.0f;
             if (fresh) { // pq::adc_lookup + sqrt + trim::relaxed_lb (search.hpp:229-231)
-                const float glq = __fsqrt_rn(adc_serial<0>(ix.codes + static_cast<size_t>(v) * ix.code_stride, ix.m));
+                const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(v) * ix.code_stride, ix.m));
                 plb = relaxed_lb(glq, __ldg(ix.lx + v), p.two_gamma);
                 // exact distance for every neighbour the replay may evaluate:
                 // cand only grows and max_dis only falls during the hop
@@ -284,7 +348,7 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
                         ++nres;
                     }
                     if (lane == 0 && !overflow)
-                        overflow = !sq.push(skey(pj, vj));
+                        overflow = !sq.push(skey(pj, vj), live_bound());
                     cand.offer(dj, vj);
                     cand_n = min(cand_n + 1, p.ef);
                     if (!p.range)
@@ -293,7 +357,7 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
                     ++pruned;
                     if (pj < cand.wd) { // plb < max_can_dis
                         if (lane == 0 && !overflow)
-                            overflow = !sq.push(skey(pj, vj));
+                            overflow = !sq.push(skey(pj, vj), live_bound());
                         cand.offer(pj, vj);
                         cand_n = min(cand_n + 1, p.ef);
                     }

@@ -395,6 +395,8 @@ class RefOracle:
         L.ref_graph_build.restype = C.c_void_p
         L.ref_graph_build.argtypes = [_f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64]
         L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_graph_load.restype = C.c_void_p
+        L.ref_graph_load.argtypes = [C.c_char_p]
         L.ref_graph_session_create.restype = C.c_void_p
         L.ref_graph_session_create.argtypes = [C.POINTER(_FlatGraph), C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
                                                _f32p, _u8p, _f32p, _f32p]
@@ -426,6 +428,19 @@ class RefOracle:
         h = self.lib.ref_graph_build(_ptr(data, _f32p), n, dim, M, efc, seed)
         if not h:
             raise ValueError(f"build_graph: {self.lib.ref_last_error().decode()}")
+        g = self._export_graph(h, n)
+        g.M, g.efc, g.dim, g.vectors = M, efc, dim, data
+        return g
+
+    def graph_load(self, path: str, n: int) -> HostGraph:
+        """graph::GraphIndex::load (graph/hnsw.hpp:58-83); graph fields only."""
+        h = self.lib.ref_graph_load(path.encode())
+        if not h:
+            msg = self.lib.ref_last_error().decode()
+            raise RuntimeError(f"graph_load: {msg}")
+        return self._export_graph(h, n)
+
+    def _export_graph(self, h, n) -> HostGraph:
         try:
             lv, en = C.c_uint32(0), C.c_uint32(0)
             self.lib.ref_graph_info(h, C.byref(lv), C.byref(en), None)
@@ -440,8 +455,7 @@ class RefOracle:
                 nbrs.append(nb[:int(sizes[lvl])])
         finally:
             self.lib.ref_graph_free(h)
-        return HostGraph(n=n, M=M, efc=efc, entry=en.value, offsets=offs, nbrs=nbrs, dim=dim,
-                         vectors=data)
+        return HostGraph(n=n, M=0, efc=0, entry=en.value, offsets=offs, nbrs=nbrs)
 
     def graph_session(self, g: HostGraph):
         """Resident reference graph + landmarks + vectors (for timing)."""

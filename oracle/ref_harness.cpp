@@ -648,6 +648,15 @@ int ref_graph_export(void* p, std::uint32_t level, std::uint64_t* offsets_out, s
     offsets_out[s->g.count] = off;
     return REF_OK;
 }
+void* ref_graph_load(const char* path) {
+    auto* s = new GraphSession;
+    const int rc = guarded([&] { s->g = graph::GraphIndex::load(path); });
+    if (rc != REF_OK) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
 int ref_graph_save(const FlatGraph* f, const char* path) {
     return guarded([&] { make_graph(*f).save(path); });
 }

@@ -26,5 +26,6 @@ from .ivf import (  # noqa: F401
     search_trim_ivf_range_device,
 )
 from . import formats  # noqa: F401  (reference on-disk formats)
+from . import graph  # noqa: F401  (TRIM filter over an HNSW graph)
 
 __version__ = "0.1.0"

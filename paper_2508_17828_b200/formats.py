@@ -255,3 +255,65 @@ def open_index(ivf_path: str, vectors_path: str, device: int = 0):
     from .ivf import GpuIvfIndex
     arr, _ = load_ivf(ivf_path, vectors=load_vecs(vectors_path))
     return GpuIvfIndex(arr, device=device)
+
+
+@dataclass
+class GraphFile:
+    """graph::GraphIndex as saved (graph/hnsw.hpp:37-56): per level, the CSR
+    offsets (count + 1, u64) and the concatenated neighbour ids (u32)."""
+
+    count: int
+    M: int
+    entry: int
+    ef_construction: int
+    offsets: list
+    nbrs: list
+
+
+def load_graph(path: str) -> GraphFile:
+    """graph::GraphIndex::load (graph/hnsw.hpp:58-83), the same checks."""
+    with open(path, "rb") as f:
+        n = int(_scalar(f, "<u8", "graph count"))
+        M = int(_scalar(f, "<u4", "graph M"))
+        levels = int(_scalar(f, "<u4", "graph levels"))
+        entry = int(_scalar(f, "<u4", "graph entry"))
+        efc = int(_scalar(f, "<u4", "graph efc"))
+        if levels == 0:
+            raise DataError(f"{path}: graph with zero levels")
+        offs, nbrs = [], []
+        for _ in range(levels):
+            o = _read(f, "<u8", n + 1, "graph offsets").astype(np.uint64)
+            sizes = np.diff(o.astype(np.int64))
+            if (sizes < 0).any():  # read_le_array of a negative degree fails in the reference
+                raise DataError(f"truncated graph ids: {path}")
+            nb = _read(f, "<u4", int(sizes.sum()), "graph ids").astype(np.uint32)
+            offs.append(np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint64))
+            nbrs.append(nb)
+    return GraphFile(n, M, entry, efc, offs, nbrs)
+
+
+def save_graph(path: str, g) -> None:
+    """graph::GraphIndex::save (graph/hnsw.hpp:37-56) of any object with count
+    (or n), M, entry, ef_construction (or efc), offsets and nbrs per level."""
+    n = int(getattr(g, "count", getattr(g, "n", 0)))
+    efc = int(getattr(g, "ef_construction", getattr(g, "efc", 0)))
+    with open(path, "wb") as f:
+        np.array([n], "<u8").tofile(f)
+        np.array([g.M, len(g.offsets), g.entry, efc], "<u4").tofile(f)
+        for o, nb in zip(g.offsets, g.nbrs):
+            np.asarray(o, "<u8").tofile(f)
+            np.asarray(nb, "<u4").tofile(f)
+
+
+def open_graph(graph_path: str, landmarks_path: str, vectors_path: str, device: int = 0):
+    """A device graph straight from the reference's artefacts: GraphIndex::save,
+    LandmarkStore::save and the base vectors (.fvecs/.bvecs)."""
+    from .graph import GpuGraph, GraphArrays
+    g = load_graph(graph_path)
+    cb, codes, lx = load_landmarks(landmarks_path)
+    vec = load_vecs(vectors_path)
+    if codes.shape[0] != g.count or vec.shape[0] != g.count:  # search.hpp:198-199
+        raise DataError("graph, landmark store and dataset sizes differ")
+    return GpuGraph(GraphArrays(entry=g.entry, offsets=g.offsets, nbrs=g.nbrs, sub_dims=cb.sub_dims,
+                                centroids=cb.centroids, codes=codes, lx=lx, vectors=vec, ksub=cb.c, M=g.M),
+                    device=device)

@@ -139,3 +139,35 @@ def test_reference_files_search_on_gpu(ref, tmp_path):
     np.testing.assert_array_equal(got[0], want[0])
     np.testing.assert_array_equal(np.asarray(got[1]).view(np.uint32), np.asarray(want[1]).view(np.uint32))
     np.testing.assert_array_equal(got[2][:, :5], want[2])
+
+
+@pytest.mark.parametrize("name", goldens.graph_names())
+def test_graph_file_both_ways(ref, name, tmp_path):
+    """GraphIndex::save (graph/hnsw.hpp:37-56) -> formats.load_graph, and
+    formats.save_graph -> GraphIndex::load, level for level."""
+    g, qs, cases = goldens.load_graph(name)
+    hg = goldens.host_graph(g)
+    p1 = str(tmp_path / "ref.graph")
+    ref.graph_save(hg, p1)
+    gf = F.load_graph(p1)
+    assert (gf.count, gf.M, gf.entry, gf.ef_construction) == (g.n, g.M, g.entry, g.efc)
+    for a, b in zip(gf.offsets, g.offsets):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(gf.nbrs, g.nbrs):
+        np.testing.assert_array_equal(a, b)
+    p2 = str(tmp_path / "ours.graph")
+    F.save_graph(p2, gf)
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+    back = ref.graph_load(p2, g.n)
+    assert back.entry == g.entry and len(back.offsets) == len(g.offsets)
+    for a, b in zip(back.nbrs, g.nbrs):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_graph_file_zero_levels(tmp_path):
+    p = str(tmp_path / "bad.graph")
+    with open(p, "wb") as f:
+        np.array([3], "<u8").tofile(f)
+        np.array([4, 0, 0, 8], "<u4").tofile(f)
+    with pytest.raises(DataError):
+        F.load_graph(p)

@@ -225,7 +225,10 @@ constexpr uint32_t kWorkers = kWarps - 1;          // 7
 constexpr uint32_t kLaneU = 1;                     // candidates per worker lane per chunk
 constexpr uint32_t kPerWorker = kWarp * kLaneU;    // 32 stream positions per worker per chunk
 constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per chunk
-constexpr uint32_t kRing = 6;                      // chunk buffers in flight
+#ifndef TRIM_KRING
+#define TRIM_KRING 6
+#endif
+constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
 static_assert(kLaneU == 1, "bin_mask records one ballot per worker chunk");
 
 __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,

@@ -521,25 +521,44 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             TRIM_TL(const unsigned long long k0 = tl ? clock64() : 0;)
             mbar_wait(full + s, (c / kRing) & 1u);
             TRIM_TL(const unsigned long long k1 = tl ? clock64() : 0;)
+            // the chunk's members of all kWorkers bins, in stream order (bin w
+            // before bin w+1, bin order inside), 32 at a time: lane i holds
+            // member base+i of bin w at rank r
             const uint32_t* cnts = bin_cnt + s * kWorkers;
-            uint32_t bins = __ballot_sync(0xffffffffu, lane < kWorkers && cnts[lane] != 0);
-            while (bins) {
-                const uint32_t w = __ffs(bins) - 1;
-                bins &= bins - 1;
-                const uint32_t cnt = cnts[w];
-                const uint32_t g0 = s * kChunkW + w * kPerWorker;
+            uint32_t inc = lane < kWorkers ? cnts[lane] : 0u;
+#pragma unroll
+            for (uint32_t o = 1; o < 8; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o)
+                    inc += t;
+            }
+            const uint32_t nmem = __shfl_sync(0xffffffffu, inc, kWorkers - 1);
+            for (uint32_t base = 0; base < nmem; base += kWarp) {
+                const uint32_t i = base + lane;
+                const uint32_t cnt = min(static_cast<uint32_t>(kWarp), nmem - base);
+                uint32_t w = 0, before = 0;
+#pragma unroll
+                for (uint32_t x = 0; x < kWorkers; ++x) {
+                    const uint32_t ix_ = __shfl_sync(0xffffffffu, inc, x);
+                    if (i >= ix_) {
+                        w = x + 1;
+                        before = ix_;
+                    }
+                }
+                const uint32_t r = i - before;
+                const uint32_t g = s * kChunkW + w * kPerWorker + r;
                 TRIM_TL(members += cnt;)
-                // Warp-parallel replay of the bin (members in stream order, lane i <->
-                // member i): with the live threshold T, a member is pruned iff
-                // lo >= T, evaluated iff hi < T (ivf.hpp:275) and replaces the top iff
-                // also (d, id) < top (ivf.hpp:277-282). Members up to the first one
-                // that replaces (or whose interval straddles T) are decided at once;
-                // that one is handled alone (it may lower T), then the rest again.
+                // Warp-parallel replay (lane i <-> member base+i): with the live
+                // threshold T, a member is pruned iff lo >= T, evaluated iff hi < T
+                // (ivf.hpp:275) and replaces the top iff also (d, id) < top
+                // (ivf.hpp:277-282). Members up to the first one that replaces (or
+                // whose interval straddles T) are decided at once; that one is
+                // handled alone (it may lower T), then the rest again.
                 const bool valid = lane < cnt;
-                const float lo = valid ? s_lo[g0 + lane] : kInf;
-                const float hi = valid ? s_hi[g0 + lane] : kInf;
-                const float dd = valid ? s_d[g0 + lane] : kInf;
-                const uint32_t did = valid ? s_e[g0 + lane] : kInvalidId;
+                const float lo = valid ? s_lo[g] : kInf;
+                const float hi = valid ? s_hi[g] : kInf;
+                const float dd = valid ? s_d[g] : kInf;
+                const uint32_t did = valid ? s_e[g] : kInvalidId;
                 uint32_t start = 0;
                 while (start < cnt) {
                     const bool mine = valid && lane >= start;
@@ -553,8 +572,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                         break;
                     const float hf = __shfl_sync(0xffffffffu, hi, f);
                     bool ev = true;
-                    if (!(hf < topk.wd))
-                        ev = exact_est(c, w, f, bin_mask[s * kWorkers + w]) < topk.wd;
+                    if (!(hf < topk.wd)) {
+                        const uint32_t wf = __shfl_sync(0xffffffffu, w, f);
+                        const uint32_t rf = __shfl_sync(0xffffffffu, r, f);
+                        ev = exact_est(c, wf, rf, bin_mask[s * kWorkers + wf]) < topk.wd;
+                    }
                     if (ev) {
                         ++dc;
                         topk.offer(__shfl_sync(0xffffffffu, dd, f), __shfl_sync(0xffffffffu, did, f));

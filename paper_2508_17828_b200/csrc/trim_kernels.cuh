@@ -206,7 +206,7 @@ struct KnnParams {
     const float* xnorm2;   // |x|^2 per row
 };
 
-constexpr uint32_t kTimeline = 16;
+constexpr uint32_t kTimeline = 32;
 // Phase instrumentation of trim_knn_kernel, compiled only into the perf-probe
 // build of the library (make timeline -> libtrim_b200_tl.so).
 #ifdef TRIM_TIMELINE
@@ -635,7 +635,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             qn2 = __fadd_ru(qn2, __fmul_ru(qv[i], qv[i]));
         qn = __fsqrt_ru(qn2);
     }
-    TRIM_TL(const bool wtl = tl && tid == kWarp; // worker 0, lane 0 records
+    TRIM_TL(const bool wtl = tl && lane == 0; // lane 0 of every worker records (worker 0: slots 10-15)
             unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
             unsigned long long wk = wtl ? clock64() : 0;)
     build_lut_blocked(ix, qv, lut, tid - kWarp, kThreads - kWarp);
@@ -758,8 +758,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     }
     TRIM_TL(if (wtl) {
         wc[5] = clock64() - wk;
-        for (int i = 0; i < 6; ++i)
-            tl[10 + i] = wc[i];
+        if (w == 0)
+            for (int i = 0; i < 6; ++i)
+                tl[10 + i] = wc[i];
+        tl[16 + w] = wc[2];          // per worker: ring / chunk-0 waits
+        tl[23 + w] = wc[3] + wc[4];  // per worker: ADC + exact L2
     })
 }
 

@@ -46,7 +46,7 @@ ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
 dist = torch.empty((nq, k), dtype=torch.float32, device="cuda")
 cts = torch.zeros((nq, 6), dtype=torch.int64, device="cuda")
 st = torch.zeros(1, dtype=torch.int32, device="cuda")
-tl = torch.zeros((nq, 16), dtype=torch.int64, device="cuda")
+tl = torch.zeros((nq, 32), dtype=torch.int64, device="cuda")
 sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 P = lambda t: C.c_void_p(t.data_ptr())
 _lib.check(lib.trim_probe_device(gix.handle, P(queries), nq, cfg["nprobe"], P(lists), sh), "probe")
@@ -92,6 +92,9 @@ for i, name in ((8, "replay_wait_full_us"), (9, "replay_busy_us"), (10, "w0_lut_
                 (12, "w0_ring_wait_us"), (13, "w0_adc_us"), (14, "w0_l2_us"), (15, "w0_pipeline_us")):
     v = t[:, i] / GHZ
     out[name] = {"mean": float(v.mean()), "p50": float(np.median(v))}
+# every worker: ring waits and busy (ADC + exact L2) time (imbalance across workers)
+out["worker_ring_wait_us"] = [float((t[:, 16 + w] / GHZ).mean()) for w in range(7)]
+out["worker_busy_us"] = [float((t[:, 23 + w] / GHZ).mean()) for w in range(7)]
 # per-chunk pipeline cost
 pc = ph["pipeline_us"] / np.maximum(1, t[:, 5])
 out["pipeline_us_per_chunk"] = {"mean": float(pc.mean()), "p50": float(np.median(pc))}

@@ -101,6 +101,11 @@ class _OrIndex(C.Structure):
     ]
 
 
+class _OrGraph(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("levels", C.c_uint32), ("entry", C.c_uint32), ("offsets", _u64p),
+                ("nbr_base", _u64p), ("nbrs", _u32p)]
+
+
 class OrCounters(C.Structure):
     _fields_ = [("dc", C.c_uint64), ("edc", C.c_uint64), ("pruned", C.c_uint64),
                 ("evaluated", C.c_uint64), ("hops", C.c_uint64)]
@@ -144,7 +149,61 @@ class COracle:
                                          C.c_uint32, _f32p, C.c_int]
         L.or_brute_force_knn_batch.argtypes = [_f32p, C.c_uint64, C.c_uint32, _f32p,
                                                C.c_uint64, C.c_uint32, _u32p, _f32p, C.c_int]
+        L.or_graph_search_trim_knn_batch.argtypes = [
+            C.POINTER(_OrGraph), C.POINTER(_OrIndex), _f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_float,
+            _u32p, _f32p, C.POINTER(OrCounters), C.c_int]
+        L.or_graph_search_trim_range_batch.argtypes = [
+            C.POINTER(_OrGraph), C.POINTER(_OrIndex), _f32p, C.c_uint64, _f32p, C.c_uint32, C.c_float,
+            _u64p, C.POINTER(_u32p), C.POINTER(_f32p), C.POINTER(OrCounters), C.c_int]
         L.or_free.argtypes = [C.c_void_p]
+
+    def _graph(self, g: "HostGraph"):
+        """(_OrGraph, _OrIndex landmark store, keep-alive arrays)."""
+        offs = np.ascontiguousarray(np.concatenate([np.asarray(o, np.uint64) for o in g.offsets]))
+        sizes = [int(np.asarray(o)[-1]) for o in g.offsets]
+        base = np.ascontiguousarray(np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64))
+        nb = np.ascontiguousarray(np.concatenate([np.asarray(x, np.uint32) for x in g.nbrs]))
+        sub = np.ascontiguousarray(g.sub_dims, np.uint32)
+        suboff = np.ascontiguousarray(np.concatenate([[0], np.cumsum(sub)[:-1]]).astype(np.uint32))
+        cent = np.ascontiguousarray(g.centroids, np.float32).ravel()
+        codes = np.ascontiguousarray(g.codes, np.uint8)
+        lx = np.ascontiguousarray(g.lx, np.float32)
+        vec = np.ascontiguousarray(g.vectors, np.float32)
+        og = _OrGraph(g.n, len(g.offsets), g.entry, _ptr(offs, _u64p), _ptr(base, _u64p), _ptr(nb, _u32p))
+        lm = _OrIndex(g.dim, g.m, g.ksub, _ptr(sub, _u32p), _ptr(suboff, _u32p), _ptr(cent, _f32p), 0, None,
+                      None, None, _ptr(codes, _u8p), codes.shape[1], _ptr(lx, _f32p), g.n, _ptr(vec, _f32p))
+        return og, lm, (offs, base, nb, sub, suboff, cent, codes, lx, vec)
+
+    def graph_search(self, g: "HostGraph", qs, kind: str, *, k=0, ef=0, gamma=0.0, radius=0.0, threads=0):
+        """C restatement of graph::search_trim_knn ("trim_knn": ids, dist [nq, k]
+        padded, counters [nq, 5]) / search_trim_range ("trim_range": offsets,
+        ids, dist, counters)."""
+        qs = np.ascontiguousarray(qs, np.float32).reshape(-1, g.dim)
+        nq = qs.shape[0]
+        og, lm, keep = self._graph(g)
+        cs = (OrCounters * max(nq, 1))()
+        th = threads or os.cpu_count()
+        if kind == "trim_knn":
+            ids = np.zeros((nq, k), np.uint32)
+            dist = np.zeros((nq, k), np.float32)
+            rc = self.lib.or_graph_search_trim_knn_batch(C.byref(og), C.byref(lm), _ptr(qs, _f32p), nq, k, ef,
+                                                         np.float32(gamma), _ptr(ids, _u32p), _ptr(dist, _f32p),
+                                                         cs, th)
+            self._err(rc, "graph search_trim_knn")
+            return ids, dist, counters_array(cs[:nq])
+        rad = np.ascontiguousarray(np.broadcast_to(np.float32(radius), (nq,)), np.float32)
+        offs = np.zeros(nq + 1, np.uint64)
+        pids, pd = _u32p(), _f32p()
+        rc = self.lib.or_graph_search_trim_range_batch(C.byref(og), C.byref(lm), _ptr(qs, _f32p), nq,
+                                                       _ptr(rad, _f32p), ef, np.float32(gamma), _ptr(offs, _u64p),
+                                                       C.byref(pids), C.byref(pd), cs, th)
+        self._err(rc, "graph search_trim_range")
+        tot = int(offs[-1])
+        ids = np.ctypeslib.as_array(pids, shape=(max(tot, 1),))[:tot].copy()
+        dist = np.ctypeslib.as_array(pd, shape=(max(tot, 1),))[:tot].copy()
+        self.lib.or_free(C.cast(pids, C.c_void_p))
+        self.lib.or_free(C.cast(pd, C.c_void_p))
+        return offs, ids, dist, counters_array(cs[:nq])
 
     def _err(self, rc: int, what: str):
         if rc != 0:

@@ -393,6 +393,237 @@ int or_search_baseline_ivfpq(const or_index* ix, const float* q, uint32_t k, uin
     return rc;
 }
 
+
+/* ======================= HNSW graph search (graph/search.hpp) ============= */
+/* A growable binary heap of ScoredId; max-heap when `maxh`, else min-heap
+ * (std::priority_queue<ScoredId> / <..., std::greater<ScoredId>>). */
+typedef struct {
+    scored* h;
+    uint64_t n, cap;
+    int maxh;
+} gheap;
+
+static int gh_above(const gheap* q, scored a, scored b) { /* a belongs above b */
+    return q->maxh ? scored_less(b, a) : scored_less(a, b);
+}
+static int gh_push(gheap* q, scored v) {
+    if (q->n == q->cap) {
+        uint64_t nc = q->cap ? 2 * q->cap : 64;
+        scored* nh = (scored*)realloc(q->h, sizeof(scored) * nc);
+        if (!nh)
+            return fail(OR_ENOMEM, "graph search: heap allocation failed");
+        q->h = nh;
+        q->cap = nc;
+    }
+    uint64_t i = q->n++;
+    q->h[i] = v;
+    while (i > 0) {
+        const uint64_t p = (i - 1) / 2;
+        if (!gh_above(q, q->h[i], q->h[p]))
+            break;
+        scored t = q->h[p];
+        q->h[p] = q->h[i];
+        q->h[i] = t;
+        i = p;
+    }
+    return OR_OK;
+}
+static scored gh_pop(gheap* q) {
+    const scored top = q->h[0];
+    q->h[0] = q->h[--q->n];
+    uint64_t i = 0;
+    for (;;) {
+        const uint64_t l = 2 * i + 1, r = l + 1;
+        uint64_t b = i;
+        if (l < q->n && gh_above(q, q->h[l], q->h[b]))
+            b = l;
+        if (r < q->n && gh_above(q, q->h[r], q->h[b]))
+            b = r;
+        if (b == i)
+            break;
+        scored t = q->h[b];
+        q->h[b] = q->h[i];
+        q->h[i] = t;
+        i = b;
+    }
+    return top;
+}
+
+static uint32_t g_adj(const or_graph* g, uint32_t lvl, uint32_t v, const uint32_t** nb) {
+    const uint64_t* o = g->offsets + (size_t)lvl * (g->n + 1);
+    *nb = g->nbrs + g->nbr_base[lvl] + o[v];
+    return (uint32_t)(o[v + 1] - o[v]);
+}
+
+/* detail_search::descend_to_level0 (search.hpp:37-58). */
+static scored g_descend(const or_graph* g, const or_index* lm, const float* q, or_counters* c) {
+    uint32_t cur = g->entry;
+    float cur_d = or_euclidean_sq(q, row_of(lm, cur), lm->dim);
+    ++c->dc;
+    ++c->evaluated;
+    for (uint32_t lvl = g->levels - 1; lvl > 0; --lvl) {
+        int changed = 1;
+        while (changed) {
+            changed = 0;
+            const uint32_t* nb;
+            const uint32_t deg = g_adj(g, lvl, cur, &nb);
+            for (uint32_t i = 0; i < deg; ++i) {
+                const uint32_t v = nb[i];
+                const float d = or_euclidean_sq(q, row_of(lm, v), lm->dim);
+                ++c->dc;
+                ++c->evaluated;
+                if (d < cur_d || (d == cur_d && v < cur)) {
+                    cur_d = d;
+                    cur = v;
+                    changed = 1;
+                }
+            }
+        }
+    }
+    scored r = {cur_d, cur};
+    return r;
+}
+
+static float g_plb(const or_index* lm, const float* table, uint32_t v, float gamma) {
+    const float glq = sqrtf(or_adc_lookup(table, lm->m, lm->ksub, lm->list_codes + (size_t)v * lm->code_stride));
+    return or_relaxed_lb(glq, lm->list_lx[v], gamma);
+}
+
+/* The shared walk of search_trim_knn (range = 0, search.hpp:188-264) and
+ * search_trim_range (range = 1, :267-347). kNN results in `res` (max-heap,
+ * capacity k); range results appended to *rout. */
+static int g_walk(const or_graph* g, const or_index* lm, const float* q, uint32_t k, uint32_t ef, float gamma,
+                  int range, float radius_sq, gheap* res, gheap* rout, or_counters* ct) {
+    const float kInf = INFINITY;
+    float* table = (float*)malloc(sizeof(float) * lm->m * lm->ksub);
+    char* visited = (char*)calloc(g->n, 1);
+    gheap sq = {NULL, 0, 0, 0}, cand = {NULL, 0, 0, 1};
+    int rc = OR_OK;
+    if (!table || !visited) {
+        rc = fail(OR_ENOMEM, "graph search: allocation failed");
+        goto out;
+    }
+    or_build_distance_table(lm, q, table);
+    const scored entry = g_descend(g, lm, q, ct);
+    visited[entry.id] = 1;
+    const float eplb = g_plb(lm, table, entry.id, gamma);
+    ++ct->edc;
+    scored se = {eplb, entry.id};
+    if ((rc = gh_push(&sq, se)) || (rc = gh_push(&cand, entry)))
+        goto out;
+    if (!range) {
+        if ((rc = gh_push(res, entry)))
+            goto out;
+    } else if (entry.d <= radius_sq) {
+        if ((rc = gh_push(rout, entry)))
+            goto out;
+    }
+    float max_dis = (!range && res->n == k) ? res->h[0].d : kInf;
+    float max_can_dis = cand.n == ef ? cand.h[0].d : kInf;
+    while (sq.n > 0) {
+        const scored cur = gh_pop(&sq);
+        if (cand.n == ef && cur.d > max_can_dis)
+            break;
+        ++ct->hops;
+        const uint32_t* nb;
+        const uint32_t deg = g_adj(g, 0, cur.id, &nb);
+        for (uint32_t i = 0; i < deg; ++i) {
+            const uint32_t v = nb[i];
+            if (visited[v])
+                continue;
+            visited[v] = 1;
+            ++ct->evaluated;
+            const float plb = g_plb(lm, table, v, gamma);
+            ++ct->edc;
+            if (cand.n < ef || (range ? plb <= radius_sq : plb < max_dis)) {
+                const float d = or_euclidean_sq(q, row_of(lm, v), lm->dim);
+                ++ct->dc;
+                scored sd = {d, v}, sp = {plb, v};
+                if (range && d <= radius_sq && (rc = gh_push(rout, sd)))
+                    goto out;
+                if ((rc = gh_push(&sq, sp)) || (rc = gh_push(&cand, sd)))
+                    goto out;
+                if (cand.n > ef)
+                    gh_pop(&cand);
+                if (cand.n == ef)
+                    max_can_dis = cand.h[0].d;
+                if (!range) {
+                    if ((rc = gh_push(res, sd)))
+                        goto out;
+                    if (res->n > k)
+                        gh_pop(res);
+                    if (res->n == k)
+                        max_dis = res->h[0].d;
+                }
+            } else {
+                ++ct->pruned;
+                if (plb < max_can_dis) {
+                    scored sp = {plb, v};
+                    if ((rc = gh_push(&sq, sp)) || (rc = gh_push(&cand, sp)))
+                        goto out;
+                    if (cand.n > ef)
+                        gh_pop(&cand);
+                    if (cand.n == ef)
+                        max_can_dis = cand.h[0].d;
+                }
+            }
+        }
+    }
+out:
+    free(table);
+    free(visited);
+    free(sq.h);
+    free(cand.h);
+    return rc;
+}
+
+int or_graph_search_trim_knn(const or_graph* g, const or_index* lm, const float* q, uint32_t k, uint32_t ef,
+                             float gamma, uint32_t* ids, float* dist, uint64_t* nres, or_counters* ct) {
+    if (k == 0 || k > ef)
+        return fail(OR_EINVAL, "search_trim_knn: need 1 <= k <= ef");
+    if (gamma < 0.0f)
+        return fail(OR_EINVAL, "search_trim_knn: uncalibrated pruning profile");
+    memset(ct, 0, sizeof *ct);
+    gheap res = {NULL, 0, 0, 1};
+    int rc = g_walk(g, lm, q, k, ef, gamma, 0, 0.0f, &res, NULL, ct);
+    if (rc == OR_OK) { /* collect_sorted (search.hpp:62-80) */
+        qsort(res.h, res.n, sizeof(scored), scored_cmp);
+        for (uint64_t i = 0; i < res.n; ++i) {
+            ids[i] = res.h[i].id;
+            dist[i] = res.h[i].d;
+        }
+        *nres = res.n;
+    }
+    free(res.h);
+    return rc;
+}
+
+int or_graph_search_trim_range(const or_graph* g, const or_index* lm, const float* q, float radius, uint32_t ef,
+                               float gamma, uint32_t** ids, float** dist, uint64_t* count, or_counters* ct) {
+    if (radius < 0.0f)
+        return fail(OR_EINVAL, "search_trim_range: negative radius");
+    if (gamma < 0.0f)
+        return fail(OR_EINVAL, "search_trim_range: uncalibrated pruning profile");
+    memset(ct, 0, sizeof *ct);
+    gheap out = {NULL, 0, 0, 1};
+    int rc = g_walk(g, lm, q, 0, ef, gamma, 1, radius * radius, NULL, &out, ct);
+    *ids = NULL;
+    *dist = NULL;
+    *count = 0;
+    if (rc == OR_OK) { /* std::sort(results) (search.hpp:336) */
+        qsort(out.h, out.n, sizeof(scored), scored_cmp);
+        *ids = (uint32_t*)malloc(sizeof(uint32_t) * (out.n ? out.n : 1));
+        *dist = (float*)malloc(sizeof(float) * (out.n ? out.n : 1));
+        for (uint64_t i = 0; i < out.n; ++i) {
+            (*ids)[i] = out.h[i].id;
+            (*dist)[i] = out.h[i].d;
+        }
+        *count = out.n;
+    }
+    free(out.h);
+    return rc;
+}
+
 /* ---- query batches: static contiguous chunks per worker (parallel.hpp:31-56) ---- */
 typedef struct {
     int kind;
@@ -418,11 +649,14 @@ typedef struct {
     uint8_t* codes;
     uint32_t code_stride;
     float* lx;
+    /* graph */
+    const or_graph* g;
+    uint32_t ef;
     int rc;
     char err[512];
 } job;
 
-enum { J_KNN, J_RANGE, J_BASE, J_BF, J_LM };
+enum { J_KNN, J_RANGE, J_BASE, J_BF, J_LM, J_GKNN, J_GRANGE };
 
 static int bf_knn(const float* data, uint64_t n, uint32_t dim, const float* q, uint32_t k,
                   uint32_t* ids, float* dist) {
@@ -470,6 +704,20 @@ static void* run_job(void* arg) {
         }
         case J_BF:
             j->rc = bf_knn(j->data, j->n, j->dim, q, j->k, j->ids + i * j->k, j->dist + i * j->k);
+            break;
+        case J_GKNN: {
+            uint64_t nres = 0;
+            j->rc = or_graph_search_trim_knn(j->g, j->ix, q, j->k, j->ef, j->gamma, j->ids + i * j->k,
+                                             j->dist + i * j->k, &nres, j->ct + i);
+            for (uint64_t r = nres; r < j->k; ++r) {
+                j->ids[i * j->k + r] = 0xFFFFFFFFu;
+                j->dist[i * j->k + r] = INFINITY;
+            }
+            break;
+        }
+        case J_GRANGE:
+            j->rc = or_graph_search_trim_range(j->g, j->ix, q, j->radius[i], j->ef, j->gamma, j->rids + i,
+                                               j->rdist + i, j->rcount + i, j->ct + i);
             break;
         case J_LM:
             or_pq_encode(j->ix, j->data + i * j->ix->dim, j->codes + i * j->code_stride);
@@ -633,4 +881,64 @@ int or_brute_force_knn_batch(const float* data, uint64_t n, uint32_t dim, const 
     p.ids = ids_out;
     p.dist = dist_out;
     return run_parallel(&p, nq, threads);
+}
+
+int or_graph_search_trim_knn_batch(const or_graph* g, const or_index* lm, const float* qs, uint64_t nq,
+                                   uint32_t k, uint32_t ef, float gamma, uint32_t* ids_out, float* dist_out,
+                                   or_counters* counters, int threads) {
+    job p;
+    memset(&p, 0, sizeof p);
+    p.kind = J_GKNN;
+    p.g = g;
+    p.ix = lm;
+    p.qs = qs;
+    p.k = k;
+    p.ef = ef;
+    p.gamma = gamma;
+    p.ids = ids_out;
+    p.dist = dist_out;
+    p.ct = counters;
+    return run_parallel(&p, nq, threads);
+}
+
+int or_graph_search_trim_range_batch(const or_graph* g, const or_index* lm, const float* qs, uint64_t nq,
+                                     const float* radius, uint32_t ef, float gamma, uint64_t* offsets_out,
+                                     uint32_t** ids_out, float** dist_out, or_counters* counters, int threads) {
+    uint32_t** rids = (uint32_t**)calloc(nq ? nq : 1, sizeof(uint32_t*));
+    float** rdist = (float**)calloc(nq ? nq : 1, sizeof(float*));
+    uint64_t* rcount = (uint64_t*)calloc(nq ? nq : 1, sizeof(uint64_t));
+    job p;
+    memset(&p, 0, sizeof p);
+    p.kind = J_GRANGE;
+    p.g = g;
+    p.ix = lm;
+    p.qs = qs;
+    p.ef = ef;
+    p.gamma = gamma;
+    p.radius = radius;
+    p.ct = counters;
+    p.rids = rids;
+    p.rdist = rdist;
+    p.rcount = rcount;
+    int rc = run_parallel(&p, nq, threads);
+    uint64_t tot = 0;
+    offsets_out[0] = 0;
+    for (uint64_t i = 0; i < nq; ++i) {
+        tot += rcount[i];
+        offsets_out[i + 1] = tot;
+    }
+    *ids_out = (uint32_t*)malloc(sizeof(uint32_t) * (tot ? tot : 1));
+    *dist_out = (float*)malloc(sizeof(float) * (tot ? tot : 1));
+    for (uint64_t i = 0; i < nq; ++i) {
+        if (rcount[i]) {
+            memcpy(*ids_out + offsets_out[i], rids[i], sizeof(uint32_t) * rcount[i]);
+            memcpy(*dist_out + offsets_out[i], rdist[i], sizeof(float) * rcount[i]);
+        }
+        free(rids[i]);
+        free(rdist[i]);
+    }
+    free(rids);
+    free(rdist);
+    free(rcount);
+    return rc;
 }

@@ -70,3 +70,23 @@ def test_graph_search_argument_errors_without_gpu():
         with pytest.raises(_lib.InvalidArgument):
             _lib.check(lib.trim_graph_search_knn(C.c_void_p(1), q.ctypes.data, 1, k, ef, gam, ids.ctypes.data,
                                                  d.ctypes.data, None))
+
+
+@pytest.mark.parametrize("name", goldens.graph_names())
+def test_graph_c_restatement_matches_goldens(name):
+    """The plain-C restatement (oracle/trim_oracle.c, or_graph_search_trim_*)
+    reproduces the reference's fixtures bit for bit, counters included."""
+    from oracle.oracle import COracle
+    co = COracle()
+    g, qs, cases = goldens.load_graph(name)
+    hg = goldens.host_graph(g)
+    for cname, c in cases.items():
+        if c["kind"] == "knn":
+            ids, dist, ct = co.graph_search(hg, qs, "trim_knn", k=c["k"], ef=c["ef"], gamma=c["gamma"])
+            assert (ids == c["ids"]).all() and (dist.view(np.uint32) == c["dist"].view(np.uint32)).all(), cname
+        else:
+            offs, ids, dist, ct = co.graph_search(hg, qs, "trim_range", ef=c["ef"], gamma=c["gamma"],
+                                                  radius=float(c["radius"]))
+            assert (offs == c["offsets"]).all() and (ids == c["ids"]).all(), cname
+            assert (dist.view(np.uint32) == c["dist"].view(np.uint32)).all(), cname
+        assert (ct == c["counters"][:, :5]).all(), cname

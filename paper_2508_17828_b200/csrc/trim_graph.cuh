@@ -334,6 +334,15 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
             uint32_t fm = __ballot_sync(0xffffffffu, fresh);
             evaluated += __popc(fm);
             edc += __popc(fm);
+            // Neighbours the replay would only count as pruned: C is full (it
+            // stays full) and the bound is at or above both max_dis (or beyond
+            // the radius) and max_can_dis now — both only fall during the
+            // replay, so at their turn they take the pruned branch without a
+            // push (search.hpp:249-259).
+            const bool idle = fresh && cand_n == p.ef && (p.range ? plb > r2 : plb >= res.wd) && !(plb < cand.wd);
+            const uint32_t im = __ballot_sync(0xffffffffu, idle);
+            pruned += __popc(im);
+            fm &= ~im;
             while (fm) { // the reference's per-neighbour decisions, in list order
                 const uint32_t j = __ffs(fm) - 1;
                 fm &= fm - 1;

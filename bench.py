@@ -300,7 +300,8 @@ def run_ours(args, cfg):
                 gix.handle, p(queries, qoff), nb, k, p(lists, b0 * np_eff * 4), np_eff,
                 float(np.float32(gamma)), p(ids, b0 * k * 4), p(dists, b0 * k * 4),
                 p(cts, b0 * 48), p(status), sh_), "knn")
-            launches += 1
+            # the filter kernel, plus trim_knn_setup_kernel (seeds + plan) on IVF indexes
+            launches += 1 + (1 if cfg["nlist"] > 1 and os.environ.get("TRIM_KNN_SETUP") != "0" else 0)
             if filt_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(st_)

@@ -260,6 +260,11 @@ float omg_round_down(float gamma) {
 //   TRIM_LIST_SKIP=0     disables the kNN list-level bound (A/B timing);
 //   TRIM_EPS_SCALE=x>=1  widens the any-order ADC error interval x-fold, so the
 //                        exact (reference-order) resolution paths run often.
+//   TRIM_KNN_SETUP=0     seeds + plan inside trim_knn_kernel instead of trim_knn_setup_kernel.
+bool knn_setup_enabled() {
+    const char* e = std::getenv("TRIM_KNN_SETUP");
+    return !(e && e[0] == '0');
+}
 bool list_skip_enabled() {
     const char* e = std::getenv("TRIM_LIST_SKIP");
     return !(e && e[0] == '0');
@@ -726,6 +731,18 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         pb.dist_out = d_dist + b * k;
         pb.counters = d_ct ? d_ct + b * 6 : nullptr;
         pb.timeline = p.timeline ? p.timeline + b * kTimeline : nullptr;
+        DevBuf recs;
+        if (pb.probe && knn_setup_enabled()) { // seeds + plan ahead of the filter kernel
+            const KnnPlanLayout lo = KnnPlanLayout::of(np, k);
+            recs = DevBuf(sizeof(uint32_t) * lo.words * pb.nq, st);
+            const size_t ssm = sizeof(uint64_t) * np + sizeof(uint32_t) * (np + 1);
+            if (ssm > 48 * 1024)
+                CK(cudaFuncSetAttribute(trim_knn_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssm)));
+            trim_knn_setup_kernel<<<static_cast<unsigned>(pb.nq), kWarp, ssm, st>>>(ix->dev, pb, recs.as<uint32_t>());
+            CK(cudaGetLastError());
+            pb.plan = recs.as<uint32_t>();
+        }
         launch_knn(ix->dev, pb, smem, st);
     }
     return TRIM_OK;

@@ -37,13 +37,22 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
                                           cudaStream_t st) {
     const uint32_t S = (p.k + 31) / 32;
     const dim3 grid(static_cast<unsigned>(p.nq));
+    if (p.plan) { // seeds + plan precomputed (trim_knn_setup_kernel)
+        if (S <= 1)
+            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);
+        if (S <= 2)
+            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true>, grid, smem, st, ix, p);
+        if (S <= 4)
+            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true>, grid, smem, st, ix, p);
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true>, grid, smem, st, ix, p);
+    }
     if (S <= 1)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1>, grid, smem, st, ix, p);
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1, false>, grid, smem, st, ix, p);
     if (S <= 2)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2>, grid, smem, st, ix, p);
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2, false>, grid, smem, st, ix, p);
     if (S <= 4)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4>, grid, smem, st, ix, p);
-    return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8>, grid, smem, st, ix, p);
+        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4, false>, grid, smem, st, ix, p);
+    return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8, false>, grid, smem, st, ix, p);
 }
 
 cudaError_t TRIM_CAT(launch_range_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,

@@ -204,6 +204,24 @@ struct KnnParams {
     uint64_t dap_ld;
     const float* xnorm;    // |x| per row, rounded up
     const float* xnorm2;   // |x|^2 per row
+    const uint32_t* plan;  // per-query setup records (trim_knn_setup_kernel), or null: set up in the kernel
+};
+
+// Per-query setup record written by trim_knn_setup_kernel (u32 words): the
+// stream length, the seeds' (d, id) in stream order, the seeded threshold and
+// the compacted stream after the list-level plan — what the replay warp of
+// trim_knn_kernel otherwise computes itself before the workers may start.
+struct KnnPlanLayout {
+    uint32_t cum, base, sd, sid, words;
+    __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k) {
+        KnnPlanLayout o;
+        o.cum = 8;                          // [0] total [1] nseed [2] nk [3] total2 [4] T0 bits
+        o.base = (o.cum + np + 1 + 1) & ~1u; // u64-aligned
+        o.sd = o.base + 2 * np;
+        o.sid = o.sd + k;
+        o.words = (o.sid + k + 1) & ~1u;
+        return o;
+    }
 };
 
 constexpr uint32_t kTimeline = 32;
@@ -351,7 +369,9 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // cum/base. Chunks c >= 1 walk the compacted stream. Counters are unchanged:
 // skipped entries are evaluated-and-pruned positions.
 // --------------------------------------------------------------------------
-template <int M, int KS, int S>
+// PRE: the seeds and the plan come from trim_knn_setup_kernel's record
+// (p.plan); the in-kernel setup code is compiled out (fewer live registers).
+template <int M, int KS, int S, bool PRE>
 __global__ void __launch_bounds__(kThreads, (M == 0 || M > 64) ? 2 : 3)
 trim_knn_kernel(DevIndex ix, KnnParams p) {
     unsigned char* smem = trim_dyn_smem;
@@ -406,8 +426,24 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         *s_T = kInf;
     }
     __syncthreads();
-    const uint32_t total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
-                                       p.np, st); // ends with a barrier
+    // the stream (probe order, ascending ids) — from the setup record when
+    // trim_knn_setup_kernel ran, else built here
+    const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words : nullptr;
+    uint32_t total;
+    if constexpr (PRE) {
+        const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+        const uint32_t nk = __ldg(rec + 2);
+        for (uint32_t i = tid; i <= nk; i += kThreads)
+            st.cum[i] = __ldg(rec + lo.cum + i);
+        const uint64_t* rb = reinterpret_cast<const uint64_t*>(rec + lo.base);
+        for (uint32_t i = tid; i < nk; i += kThreads)
+            st.base[i] = __ldg(rb + i);
+        total = __ldg(rec);
+        __syncthreads();
+    } else {
+        total = load_stream(ix, p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr,
+                            p.np, st); // ends with a barrier
+    }
     // seeds [0, nseed) are the replay warp's; the candidate stream is the kept
     // part of [nseed, total), compacted into cum/base by the plan
     const uint32_t nseed = min(p.k, total);
@@ -418,8 +454,20 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         TRIM_TL(if (tl && lane == 0) tl[1] = gtime();)
         WarpTopK<S> topk;
         topk.init(p.k);
+        uint32_t carry = 0, nk = 0;
+        if constexpr (PRE) { // seeds and plan from trim_knn_setup_kernel
+            const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+            for (uint32_t j = 0; j < nseed; ++j)
+                topk.offer(__uint_as_float(__ldg(rec + lo.sd + j)), __ldg(rec + lo.sid + j));
+            nk = __ldg(rec + 2);
+            carry = __ldg(rec + 3);
+            if (lane == 0) {
+                *s_total2 = carry;
+                *reinterpret_cast<volatile float*>(s_T) = topk.wd;
+            }
+        }
         // seeds (ivf.hpp:264-271): evaluated unconditionally, in stream order
-        for (uint32_t b0 = 0; b0 < nseed; b0 += kWarp) {
+        for (uint32_t b0 = 0; !PRE && b0 < nseed; b0 += kWarp) {
             const uint32_t i = b0 + lane;
             float d = 0.0f;
             uint32_t id = 0;
@@ -442,8 +490,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         // is >= T0 (>= T_live at all its positions), compact the rest in place
         const bool skip = p.skip_lists && p.probe && total > nseed;
         const uint32_t* pl = p.probe ? p.probe + static_cast<size_t>(q) * p.np : nullptr;
-        uint32_t carry = 0, nk = 0;
-        for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) {
+        for (uint32_t b0 = 0; !PRE && b0 < p.np; b0 += kWarp) {
             const uint32_t i = b0 + lane;
             uint32_t len = 0;
             uint64_t bs = 0;
@@ -480,7 +527,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             nk += __popc(keep);
             __syncwarp();
         }
-        if (lane == 0) {
+        if (lane == 0 && !PRE) {
             st.cum[nk] = carry;
             *s_total2 = carry;
             *reinterpret_cast<volatile float*>(s_T) = T0;
@@ -1051,6 +1098,126 @@ trim_range_flat_kernel(DevIndex ix, RangeParams p, uint32_t qt) {
 #include "trim_probe_mma.cuh"
 #include "trim_flat_mma.cuh"
 namespace trimgpu {
+// --------------------------------------------------------------------------
+// trim_knn_setup_kernel — what trim_knn_kernel's replay warp does before its
+// workers may start (ivf.hpp:256-271 and the list-level plan), for a batch,
+// one warp per query: the stream of the probed lists, the k seeds' exact
+// distances in stream order (evaluated unconditionally, ivf.hpp:264-271), the
+// seeded threshold T0 = max_dis, and the plan — every probed list after the
+// seeds whose list_lower_bound is >= T0 is dropped (the reference prunes each
+// of its entries, ivf.hpp:275), the rest compacted. Moving it out of the
+// filter kernel frees that kernel's shared-memory slot ~25 us sooner per query.
+// Dynamic shared memory: (np + 1) u32 + np u64.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnParams p, uint32_t* recs) {
+    const uint32_t q = blockIdx.x;
+    if (q >= p.nq)
+        return;
+    const uint32_t lane = threadIdx.x;
+    StreamSmem st;
+    st.base = reinterpret_cast<uint64_t*>(trim_dyn_smem);
+    st.cum = reinterpret_cast<uint32_t*>(st.base + p.np);
+    const uint32_t* pl = p.probe + static_cast<size_t>(q) * p.np;
+    const float* qv = p.queries + static_cast<size_t>(q) * ix.dim_stride;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) { // load_stream, one warp
+        const uint32_t li = b0 + lane;
+        uint32_t v = 0;
+        if (li < p.np) {
+            const uint32_t l = __ldg(pl + li);
+            st.base[li] = __ldg(ix.list_offsets + l);
+            v = static_cast<uint32_t>(__ldg(ix.list_offsets + l + 1) - st.base[li]);
+        }
+#pragma unroll
+        for (int o = 1; o < kWarp; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= static_cast<uint32_t>(o))
+                v += t;
+        }
+        if (li < p.np)
+            st.cum[li + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, kWarp - 1);
+    }
+    if (lane == 0)
+        st.cum[0] = 0;
+    __syncwarp();
+    const uint32_t total = carry;
+    const uint32_t nseed = min(p.k, total);
+    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+    uint32_t* rec = recs + static_cast<size_t>(q) * lo.words;
+    // seeds (ivf.hpp:264-271): exact distances in stream order; T0 = max_dis
+    // after them (the largest (d, id), or +inf when fewer than k)
+    float T0 = nseed < p.k ? __int_as_float(0x7f800000) : 0.0f;
+    for (uint32_t b0 = 0; b0 < nseed; b0 += kWarp) {
+        const uint32_t i = b0 + lane;
+        if (i < nseed) {
+            uint32_t li = 0;
+            while (st.cum[li + 1] <= i)
+                ++li;
+            const uint64_t e = st.base[li] + (i - st.cum[li]);
+            const uint32_t id = __ldg(ix.list_ids + e);
+            const float d = euclid_sq_vec4(qv, ix.vectors + static_cast<size_t>(id - ix.id_base) * ix.dim_stride,
+                                           ix.dim, true);
+            rec[lo.sd + i] = __float_as_uint(d);
+            rec[lo.sid + i] = id;
+            if (nseed == p.k)
+                T0 = fmaxf(T0, d);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        T0 = fmaxf(T0, __shfl_xor_sync(0xffffffffu, T0, o));
+    // plan (as trim_knn_kernel's replay warp)
+    const bool skip = p.skip_lists && total > nseed;
+    uint32_t kept = 0, nk = 0;
+    for (uint32_t b0 = 0; b0 < p.np; b0 += kWarp) {
+        const uint32_t i = b0 + lane;
+        uint32_t len = 0;
+        uint64_t bs = 0;
+        if (i < p.np) {
+            const uint32_t c0 = st.cum[i], c1 = st.cum[i + 1];
+            bool drop = c1 <= nseed;
+            if (!drop && skip && c0 >= nseed) {
+                const uint32_t l = __ldg(pl + i);
+                const float dq = euclid_sq_vec4(qv, ix.coarse + static_cast<size_t>(l) * ix.dim_stride, ix.dim);
+                drop = list_lower_bound(dq, __ldg(ix.list_R + l), __ldg(ix.list_xmin + l), __ldg(ix.list_xmax + l),
+                                        p) >= T0;
+            }
+            if (!drop) {
+                const uint32_t s0 = max(c0, nseed);
+                len = c1 - s0;
+                bs = st.base[i] + (s0 - c0);
+            }
+        }
+        const uint32_t keep = __ballot_sync(0xffffffffu, len != 0);
+        uint32_t v = len;
+#pragma unroll
+        for (int o = 1; o < kWarp; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= static_cast<uint32_t>(o))
+                v += t;
+        }
+        if (len != 0) {
+            const uint32_t j = nk + __popc(keep & ((1u << lane) - 1u));
+            reinterpret_cast<uint64_t*>(rec + lo.base)[j] = bs;
+            rec[lo.cum + j] = kept + v - len;
+        }
+        kept += __shfl_sync(0xffffffffu, v, kWarp - 1);
+        nk += __popc(keep);
+    }
+    if (lane == 0) {
+        rec[lo.cum + nk] = kept;
+        rec[0] = total;
+        rec[1] = nseed;
+        rec[2] = nk;
+        rec[3] = kept;
+        rec[4] = __float_as_uint(T0);
+        const uint32_t rest = total - nseed;
+        if (p.skipped && rest != kept)
+            atomicAdd(p.skipped, static_cast<unsigned long long>(rest - kept));
+    }
+}
+
 // --------------------------------------------------------------------------
 // trim_probe_kernel — probe_order (ivf.hpp:173-187): coarse distances in the
 // reference's arithmetic, sorted by (dist, list id) in shared memory, first

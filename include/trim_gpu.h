@@ -311,7 +311,7 @@ int trim_graph_destroy(trim_graph_t graph);
  * query with fewer than k results pads with id 0xFFFFFFFF / +inf.
  * counters_out: nq (hops = expanded nodes, coarse_dc = 0), may be NULL.
  * k == 0 or k > ef -> TRIM_EINVAL (search.hpp:193-194); gamma < 0 ->
- * TRIM_EINVAL (uncalibrated profile, search.hpp:195-196); ef <= 256.
+ * TRIM_EINVAL (uncalibrated profile, search.hpp:195-196); ef <= 1024.
  */
 int trim_graph_search_knn(trim_graph_t graph, const float* queries, uint64_t nq, uint32_t k,
                           uint32_t ef, float gamma, uint32_t* ids_out, float* dist_out,
@@ -326,7 +326,7 @@ int trim_graph_search_knn_device(trim_graph_t graph, const float* d_queries, uin
  * graph::search_trim_range (graph/search.hpp:267-347). radius: nq plain radii
  * (negative -> TRIM_EINVAL). Results as trim_search_range: offsets_out nq+1,
  * library-allocated *ids_out / *dist_out (trim_free), ascending (dist_sq, id).
- * 1 <= ef <= 256.
+ * 1 <= ef <= 1024.
  */
 int trim_graph_search_range(trim_graph_t graph, const float* queries, uint64_t nq,
                             const float* radius, uint32_t ef, float gamma, uint64_t* offsets_out,

@@ -1751,8 +1751,8 @@ int trim_graph_search_knn(trim_graph_t gr, const float* queries, uint64_t nq, ui
         return set_err(TRIM_EINVAL, "search_trim_knn: need 1 <= k <= ef");
     if (!(gamma >= 0.0f))
         return set_err(TRIM_EINVAL, "search_trim_knn: uncalibrated pruning profile");
-    if (ef > 256)
-        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 256 is not supported on the GPU path");
+    if (ef > 1024)
+        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 1024 is not supported on the GPU path");
     if (nq == 0)
         return TRIM_OK;
     return guarded([&]() -> int {
@@ -1783,8 +1783,8 @@ int trim_graph_search_knn_device(trim_graph_t gr, const float* d_queries, uint64
         return set_err(TRIM_EINVAL, "search_trim_knn: need 1 <= k <= ef");
     if (!(gamma >= 0.0f))
         return set_err(TRIM_EINVAL, "search_trim_knn: uncalibrated pruning profile");
-    if (ef > 256)
-        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 256 is not supported on the GPU path");
+    if (ef > 1024)
+        return set_err(TRIM_EINVAL, "search_trim_knn: ef > 1024 is not supported on the GPU path");
     if (nq == 0)
         return TRIM_OK;
     return guarded([&]() -> int {
@@ -1817,8 +1817,8 @@ int trim_graph_search_range(trim_graph_t gr, const float* queries, uint64_t nq, 
             return set_err(TRIM_EINVAL, "search_trim_range: negative radius");
     if (!(gamma >= 0.0f))
         return set_err(TRIM_EINVAL, "search_trim_range: uncalibrated pruning profile");
-    if (ef == 0 || ef > 256)
-        return set_err(TRIM_EINVAL, "search_trim_range: the GPU path needs 1 <= ef <= 256");
+    if (ef == 0 || ef > 1024)
+        return set_err(TRIM_EINVAL, "search_trim_range: the GPU path needs 1 <= ef <= 1024");
     offsets_out[0] = 0;
     if (nq == 0) {
         *ids_out = static_cast<uint32_t*>(std::malloc(4));

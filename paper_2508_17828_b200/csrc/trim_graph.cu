@@ -1,5 +1,5 @@
 // trim_graph.cu — instantiates trim_graph_kernel (trim_graph.cuh) for the
-// candidate-queue capacities 32*S, S in {1, 2, 4, 8}.
+// candidate-queue capacities 32*S, S in {1, 2, 4, 8, 16, 32} (ef <= 1024).
 #define TRIM_M 1000 // trim_kernels.cuh's non-template kernels are compiled in trim_capi.cu
 #include "trim_graph.cuh"
 #include "trim_launch.h"
@@ -14,6 +14,8 @@ cudaError_t launch_graph(const GraphDev& g, const GraphParams& p, uint32_t S, si
     case 2: kern = trim_graph_kernel<2>; break;
     case 4: kern = trim_graph_kernel<4>; break;
     case 8: kern = trim_graph_kernel<8>; break;
+    case 16: kern = trim_graph_kernel<16>; break;
+    case 32: kern = trim_graph_kernel<32>; break;
     default: return cudaErrorInvalidValue;
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -42,6 +42,25 @@ def test_facade_adapts_reference_types(tmp_path):
     assert r.returncode == 0, r.stderr
 
 
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not present")
+def test_graph_facade_adapts_reference_types(tmp_path):
+    """trim_b200::graph::from_reference() instantiates with the reference's own
+    GraphIndex / LandmarkStore / VectorDataset / PruningProfile (compile-only)."""
+    src = tmp_path / "adapt_graph.cpp"
+    src.write_text(
+        '#include "trimsearch/graph/search.hpp"\n#include "trim_b200/graph.hpp"\n'
+        "using namespace trimsearch;\n"
+        "int run(const graph::GraphIndex& g, const trim::LandmarkStore& lm, const VectorDataset& ds,\n"
+        "        const trim::PruningProfile& p, VectorView q) {\n"
+        "  auto gg = trim_b200::graph::from_reference(g, lm, ds);\n"
+        "  auto r = trim_b200::graph::search_trim_knn(gg, p, q, 10, 64);\n"
+        "  auto s = trim_b200::graph::search_trim_range(gg, p, q, 1.0f, 64);\n"
+        "  return int(r.ids.size() + s.ids.size());\n}\n")
+    r = subprocess.run(["g++", "-std=c++20", "-c", "-I", REF_INC, "-I", os.path.join(ROOT, "include"),
+                        str(src), "-o", str(tmp_path / "adapt_graph.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
 @pytest.mark.gpu
 def test_facade_program_on_gpu(tmp_path):
     exe = str(tmp_path / "t")

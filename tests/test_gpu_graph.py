@@ -70,7 +70,7 @@ def test_graph_single_query_facade(graphs):
     assert r.counters.evaluated == c["counters"][3][3] and r.counters.hops == c["counters"][3][4]
 
 
-@pytest.mark.parametrize("kw", [dict(k=0, ef=8), dict(k=9, ef=8), dict(k=4, ef=300)])
+@pytest.mark.parametrize("kw", [dict(k=0, ef=8), dict(k=9, ef=8), dict(k=4, ef=2000)])
 def test_graph_knn_argument_errors(graphs, kw):
     from paper_2508_17828_b200 import graph as G
     from paper_2508_17828_b200.ivf import InvalidArgument, PruningProfile
@@ -117,3 +117,36 @@ def test_graph_live_reference(seed):
             seg = slice(int(offs[i]), int(offs[i + 1]))
             assert (rids[seg] == wi[i, :wc[i]]).all() and (_bits(rd[seg]) == _bits(wd[i, :wc[i]])).all()
         assert (rct[:, :5] == wct[:, :5]).all()
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(goldens.GOLDEN, "..", "..", "oracle", "_ref", "libtrimref.so")),
+                    reason="oracle/_ref not built")
+def test_graph_gamma0_exhaustive_ef_equals_brute_force():
+    """proj/tests/test_graph.cpp:132-159: with gamma = 0 and ef = n, TRIM graph
+    kNN returns the brute-force top 10 and range search the brute-force ball
+    (here on the GPU; ef = 600 uses the 1,024-slot candidate queue)."""
+    from oracle.oracle import COracle, RefOracle, make_reference_graph
+    from paper_2508_17828_b200 import graph as G
+    from paper_2508_17828_b200.ivf import PruningProfile
+    ref, co = RefOracle(), COracle()
+    base = ref.make_normal(600, 16, 100)
+    qs = ref.make_normal(25, 16, 101)
+    # TrimFixture(600, 16, 100, 4, 32) (test_graph.cpp:29-51): M = 8, ef_construction = 100,
+    # PQ m = 4 with c = 32 centroids (a ksub < 256 codebook), 8 k-means iterations
+    hg = make_reference_graph(ref, base, M=8, efc=100, graph_seed=101, m=4, c=32, iters=8, pq_seed=102)
+    gg = G.GpuGraph(G.GraphArrays.from_any(hg))
+    zero = PruningProfile.manual(0.0)
+    ids, dist, ct = G.search_trim_knn_batch(gg, zero, qs, 10, 600)
+    truth_ids, truth_d = co.brute_force_knn(base, qs, 10)
+    assert (ids == truth_ids).all()
+    radius = 4.2
+    offs, rids, rd, rct = G.search_trim_range_batch(gg, zero, qs, radius, 600)
+    r2 = np.float32(radius) * np.float32(radius)
+    for i in range(len(qs)):
+        d = np.array([co.euclidean_sq(qs[i], base[j]) for j in range(len(base))], np.float32)
+        want = sorted((float(d[j]), j) for j in range(len(base)) if d[j] <= r2)
+        got = rids[int(offs[i]):int(offs[i + 1])]
+        assert [j for _, j in want] == got.tolist()
+    # and the whole output is the reference's own
+    w = ref.graph_search(hg, qs, "trim_knn", k=10, ef=600, gamma=0.0)
+    assert (w[0] == ids).all() and (w[3][:, :5] == ct[:, :5]).all()

@@ -66,7 +66,7 @@ def test_graph_search_argument_errors_without_gpu():
     q = np.zeros(8, np.float32)
     ids = np.zeros(8, np.uint32)
     d = np.zeros(8, np.float32)
-    for k, ef, gam in ((0, 8, 0.5), (9, 8, 0.5), (4, 8, -1.0), (4, 300, 0.5)):
+    for k, ef, gam in ((0, 8, 0.5), (9, 8, 0.5), (4, 8, -1.0), (4, 2000, 0.5)):
         with pytest.raises(_lib.InvalidArgument):
             _lib.check(lib.trim_graph_search_knn(C.c_void_p(1), q.ctypes.data, 1, k, ef, gam, ids.ctypes.data,
                                                  d.ctypes.data, None))

@@ -31,6 +31,10 @@ template <typename K, typename... A>
 cudaError_t launch(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
     return launch_t(kern, grid, kThreads, smem, st, args...);
 }
+template <typename K, typename... A>
+cudaError_t launch_knn_t(K kern, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+    return launch_t(kern, grid, knn_threads(TRIM_M), smem, st, args...);
+}
 } // namespace
 
 cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p, size_t smem,
@@ -39,20 +43,20 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
     const dim3 grid(static_cast<unsigned>(p.nq));
     if (p.plan) { // seeds + plan precomputed (trim_knn_setup_kernel)
         if (S <= 1)
-            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);
+            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);
         if (S <= 2)
-            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true>, grid, smem, st, ix, p);
+            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true>, grid, smem, st, ix, p);
         if (S <= 4)
-            return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true>, grid, smem, st, ix, p);
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true>, grid, smem, st, ix, p);
+            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true>, grid, smem, st, ix, p);
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true>, grid, smem, st, ix, p);
     }
     if (S <= 1)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 1, false>, grid, smem, st, ix, p);
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, false>, grid, smem, st, ix, p);
     if (S <= 2)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 2, false>, grid, smem, st, ix, p);
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, false>, grid, smem, st, ix, p);
     if (S <= 4)
-        return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 4, false>, grid, smem, st, ix, p);
-    return launch(trim_knn_kernel<TRIM_M, TRIM_KS, 8, false>, grid, smem, st, ix, p);
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, false>, grid, smem, st, ix, p);
+    return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, false>, grid, smem, st, ix, p);
 }
 
 cudaError_t TRIM_CAT(launch_range_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,

@@ -249,8 +249,19 @@ constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per 
 constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
 static_assert(kLaneU == 1, "bin_mask records one ballot per worker chunk");
 
+// Warps per filter CTA by code length: a long code (m = 120: a 128 KB LUT, one
+// CTA per SM) gets 16 warps (15 workers, 128 registers: measured best of 8/16/24/32)
+// so the SM is not left with 8 warps; otherwise 8 (3 CTAs per SM).
+#ifndef TRIM_WIDE_WARPS
+#define TRIM_WIDE_WARPS 16
+#endif
+__host__ __device__ constexpr uint32_t knn_warps(int mt) { return mt > 64 ? TRIM_WIDE_WARPS : kWarps; }
+__host__ __device__ constexpr uint32_t knn_threads(int mt) { return knn_warps(mt) * kWarp; }
+__host__ __device__ constexpr uint32_t knn_chunk(int mt) { return (knn_warps(mt) - 1) * kPerWorker; }
+
 __host__ __device__ inline size_t knn_smem_bytes(int mt, uint32_t m, uint32_t dim_stride,
                                                  uint32_t np) {
+    const size_t kChunkW = knn_chunk(mt), kWorkers = knn_warps(mt) - 1;
     size_t b = lut_bytes(mt, m);                 // blocked lut at offset 0
     b += sizeof(float) * dim_stride;             // query
     b += sizeof(uint64_t) * np;                  // base
@@ -372,8 +383,12 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // PRE: the seeds and the plan come from trim_knn_setup_kernel's record
 // (p.plan); the in-kernel setup code is compiled out (fewer live registers).
 template <int M, int KS, int S, bool PRE>
-__global__ void __launch_bounds__(kThreads, (M == 0 || M > 64) ? 2 : 3)
+__global__ void __launch_bounds__(knn_threads(M), M > 64 ? 1 : (M == 0 ? 2 : 3))
 trim_knn_kernel(DevIndex ix, KnnParams p) {
+    // this instantiation's CTA shape (knn_warps): warp 0 replays, the rest filter
+    constexpr uint32_t kThreads = knn_threads(M);
+    constexpr uint32_t kWorkers = knn_warps(M) - 1;
+    constexpr uint32_t kChunkW = knn_chunk(M);
     unsigned char* smem = trim_dyn_smem;
     const uint32_t q = blockIdx.x;
     if (q >= p.nq)
@@ -574,7 +589,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             const uint32_t* cnts = bin_cnt + s * kWorkers;
             uint32_t inc = lane < kWorkers ? cnts[lane] : 0u;
 #pragma unroll
-            for (uint32_t o = 1; o < 8; o <<= 1) {
+            for (uint32_t o = 1; o < kWarp; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o)
                     inc += t;
@@ -808,8 +823,10 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         if (w == 0)
             for (int i = 0; i < 6; ++i)
                 tl[10 + i] = wc[i];
-        tl[16 + w] = wc[2];          // per worker: ring / chunk-0 waits
-        tl[23 + w] = wc[3] + wc[4];  // per worker: ADC + exact L2
+        if (w < 7) {
+            tl[16 + w] = wc[2];          // per worker: ring / chunk-0 waits
+            tl[23 + w] = wc[3] + wc[4];  // per worker: ADC + exact L2
+        }
     })
 }
 

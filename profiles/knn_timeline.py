@@ -30,8 +30,9 @@ ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--gamma", type=float, default=0.8)
 ap.add_argument("--batch", type=int, default=1024)
 ap.add_argument("--out", default="")
+ap.add_argument("--config", default="c2")
 a = ap.parse_args()
-cfg = dict(bench.CONFIGS["c2"])
+cfg = dict(bench.CONFIGS[a.config])
 if a.n:
     cfg["n"] = a.n
 cfg["nq"] = a.batch
@@ -41,7 +42,7 @@ lib = _lib.load()
 lib.trim__set_knn_timeline.argtypes = [C.c_void_p]
 nq, k = a.batch, cfg["k"]
 npb = min(cfg["nprobe"], cfg["nlist"])
-lists = torch.empty((nq, npb), dtype=torch.int32, device="cuda")
+lists = torch.zeros((nq, npb), dtype=torch.int32, device="cuda")
 ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
 dist = torch.empty((nq, k), dtype=torch.float32, device="cuda")
 cts = torch.zeros((nq, 6), dtype=torch.int64, device="cuda")

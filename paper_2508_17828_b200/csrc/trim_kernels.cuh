@@ -255,7 +255,19 @@ static_assert(kLaneU == 1, "bin_mask records one ballot per worker chunk");
 #ifndef TRIM_WIDE_WARPS
 #define TRIM_WIDE_WARPS 16
 #endif
-__host__ __device__ constexpr uint32_t knn_warps(int mt) { return mt > 64 ? TRIM_WIDE_WARPS : kWarps; }
+#ifndef TRIM_NARROW_WARPS
+#define TRIM_NARROW_WARPS 8
+#endif
+#ifndef TRIM_M16_WARPS
+#define TRIM_M16_WARPS 6 // config 1 (m = 16): 4 CTAs x 6 warps measured 3% over 3 x 8, 4 warps 24% slower
+#endif
+__host__ __device__ constexpr uint32_t knn_warps(int mt) {
+    return mt > 64 ? TRIM_WIDE_WARPS : (mt == 0 ? kWarps : (mt == 16 ? TRIM_M16_WARPS : TRIM_NARROW_WARPS));
+}
+// CTAs per SM the register budget is set for (24 warps per SM in total)
+__host__ __device__ constexpr uint32_t knn_min_blocks(int mt) {
+    return mt == 0 ? 2u : (24u / knn_warps(mt) > 0 ? 24u / knn_warps(mt) : 1u);
+}
 __host__ __device__ constexpr uint32_t knn_threads(int mt) { return knn_warps(mt) * kWarp; }
 __host__ __device__ constexpr uint32_t knn_chunk(int mt) { return (knn_warps(mt) - 1) * kPerWorker; }
 
@@ -383,7 +395,7 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // PRE: the seeds and the plan come from trim_knn_setup_kernel's record
 // (p.plan); the in-kernel setup code is compiled out (fewer live registers).
 template <int M, int KS, int S, bool PRE>
-__global__ void __launch_bounds__(knn_threads(M), M > 64 ? 1 : (M == 0 ? 2 : 3))
+__global__ void __launch_bounds__(knn_threads(M), knn_min_blocks(M))
 trim_knn_kernel(DevIndex ix, KnnParams p) {
     // this instantiation's CTA shape (knn_warps): warp 0 replays, the rest filter
     constexpr uint32_t kThreads = knn_threads(M);

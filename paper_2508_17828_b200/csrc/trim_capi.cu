@@ -894,7 +894,7 @@ void graph_run(trim_graph* gr, const float* d_q, uint64_t nq, uint32_t k, uint32
     // run queries [q0, q0 + nb), or the nb queries listed in d_map
     auto run = [&](uint64_t q0, uint64_t nb, bool global_heap, const uint32_t* d_map, uint32_t* d_status) {
         const uint64_t heap_cap = global_heap ? n + 1 : hs;
-        const size_t smem = graph_smem_bytes(g.ix.m, g.ix.dim_stride, global_heap ? 0 : hs);
+        const size_t smem = graph_smem_bytes(g.ix.m, g.ix.ksub, g.ix.dim_stride, global_heap ? 0 : hs);
         if (smem > kSmemLimit) {
             set_err(TRIM_EINVAL, "graph search: per-query shared memory (%zu B) exceeds 227 KB", smem);
             throw CudaError{TRIM_EINVAL};

@@ -71,8 +71,14 @@ struct GraphParams {
 
 constexpr uint32_t kGraphThreads = 32;
 
-__host__ __device__ inline size_t graph_smem_bytes(uint32_t m, uint32_t dim_stride, uint64_t smem_heap) {
-    const size_t b = (lut_bytes(0, m) + sizeof(float) * dim_stride + 7) & ~size_t(7);
+// The graph kernel's LUT is the reference's own m x ksub table (pq.hpp:158-172),
+// row-major: all lanes look up the same subspace j at once, so bank = code mod
+// 32 (the filter kernel's blocked layout would put them all in bank j mod 32).
+__host__ __device__ inline size_t graph_lut_bytes(uint32_t m, uint32_t ksub) {
+    return (sizeof(float) * m * ksub + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t graph_smem_bytes(uint32_t m, uint32_t ksub, uint32_t dim_stride, uint64_t smem_heap) {
+    const size_t b = (graph_lut_bytes(m, ksub) + sizeof(float) * dim_stride + 7) & ~size_t(7);
     return b + sizeof(unsigned long long) * smem_heap;
 }
 
@@ -147,15 +153,11 @@ struct MinHeap {
 };
 
 // pq::adc_lookup (pq.hpp:186-192) of one code row in the reference order
-// (sequential fp32 sum, j = 0..m-1) over the blocked LUT, as adc_serial, but
-// with the code bytes fetched 16 at a time (rows are 16-byte aligned and
-// zero-padded; a padded byte reads a zeroed LUT column, and acc + 0.0f == acc
-// for the non-negative running sum), the next 16 in flight while the current
-// ones are summed.
-__device__ __forceinline__ float adc_serial_row(const uint8_t* __restrict__ code, uint32_t m) {
-    const LutShape sh = LutShape::of(m);
+// (sequential fp32 sum, j = 0..m-1) over the row-major LUT in shared memory,
+// the code bytes fetched 16 at a time (rows are 16-byte aligned), the next 16
+// in flight while the current ones are summed.
+__device__ __forceinline__ float adc_serial_row(const uint8_t* __restrict__ code, uint32_t m, uint32_t ksub) {
     const uint32_t base = lut_saddr();
-    const uint32_t hbase = base + sh.nfull * kFullBytes, hrow = sh.half_row_bytes();
     const uint4* c4 = reinterpret_cast<const uint4*>(code);
     float acc = 0.0f;
     uint4 nxt = __ldg(c4);
@@ -164,13 +166,13 @@ __device__ __forceinline__ float adc_serial_row(const uint8_t* __restrict__ code
         if (j0 + 16 < m)
             nxt = __ldg(c4 + (j0 >> 4) + 1);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-        const uint32_t bb = j0 >> 5, t0 = j0 & 31u;
-        const uint32_t rb = bb < sh.nfull ? base + bb * kFullBytes : hbase;
-        const uint32_t rs = bb < sh.nfull ? 128u : hrow;
+        const uint32_t n = min(16u, m - j0);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xFFu;
-            acc = __fadd_rn(acc, lds_f32(rb + c * rs + 4u * (t0 + t)));
+        for (uint32_t t = 0; t < 16; ++t) {
+            if (t < n) {
+                const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xFFu;
+                acc = __fadd_rn(acc, lds_f32(base + 4u * ((j0 + t) * ksub + c)));
+            }
         }
     }
     return acc;
@@ -203,14 +205,21 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
     const uint32_t q = p.qmap ? p.qmap[slot] : slot;       // query (inputs, outputs)
     const uint32_t lane = threadIdx.x;
     float* lut = reinterpret_cast<float*>(trim_dyn_smem); // offset 0 (lut_saddr)
-    float* qv = lut + lut_bytes(0, ix.m) / sizeof(float);
+    const size_t lb = graph_lut_bytes(ix.m, ix.ksub);
+    float* qv = lut + lb / sizeof(float);
     unsigned long long* sheap = reinterpret_cast<unsigned long long*>(
-        trim_dyn_smem + ((lut_bytes(0, ix.m) + sizeof(float) * ix.dim_stride + 7) & ~size_t(7)));
+        trim_dyn_smem + ((lb + sizeof(float) * ix.dim_stride + 7) & ~size_t(7)));
     const float* qg = p.queries + static_cast<size_t>(q) * ix.dim_stride;
     for (uint32_t i = lane; i < ix.dim_stride; i += kWarp)
         qv[i] = qg[i];
     __syncwarp();
-    build_lut_blocked(ix, qv, lut, lane, kWarp); // pq::build_distance_table (search.hpp:204)
+    // pq::build_distance_table (search.hpp:204; pq.hpp:158-172): entry (j, c) =
+    // euclidean_sq(q_j, C_jc, sub_dim_j) in the reference's arithmetic
+    for (uint32_t i = lane; i < ix.m * ix.ksub; i += kWarp) {
+        const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
+        const uint32_t sd = __ldg(ix.sub_dims + j), off = __ldg(ix.sub_offsets + j);
+        lut[i] = euclid_sq_generic(qv + off, ix.centroids + static_cast<size_t>(ix.ksub) * off + c * sd, sd);
+    }
     __syncwarp();
 
     const uint64_t n = ix.n;
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
     if (lane == 0)
         atomicOr(vis + (cur >> 5), 1u << (cur & 31u));
     {
-        const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(cur) * ix.code_stride, ix.m));
+        const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(cur) * ix.code_stride, ix.m, ix.ksub));
         ++edc;
         const float plb = relaxed_lb(glq, __ldg(ix.lx + cur), p.two_gamma);
         if (lane == 0)
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(kGraphThreads) trim_graph_kernel(GraphDev g, G
             }
             float plb = 0.0f, d = 0.0f;
             if (fresh) { // pq::adc_lookup + sqrt + trim::relaxed_lb (search.hpp:229-231)
-                const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(v) * ix.code_stride, ix.m));
+                const float glq = __fsqrt_rn(adc_serial_row(ix.codes + static_cast<size_t>(v) * ix.code_stride, ix.m, ix.ksub));
                 plb = relaxed_lb(glq, __ldg(ix.lx + v), p.two_gamma);
                 // exact distance for every neighbour the replay may evaluate:
                 // cand only grows and max_dis only falls during the hop

@@ -484,9 +484,21 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
     from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(max(1, args.streams))  # client threads: one stream each in the C ABI
 
+    # results land in pinned host buffers (a serving client's staging memory)
+    from paper_2508_17828_b200 import _lib
+    import ctypes as C
+    lib = _lib.load()
+    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy()
+    h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy()
+    h_ct = torch.empty((nq, 6), dtype=torch.int64).pin_memory().numpy()
+
     def one(b):
-        ids, dist, ct = G.search_trim_ivf_knn_batch(gix, prof, hqn[b:b + B], k, cfg["nprobe"])
-        return int(ct[:, 3].sum())
+        nb = min(B, nq - b)
+        _lib.check(lib.trim_search_knn(gix.handle, C.c_void_p(hqn[b:].ctypes.data), nb, k, cfg["nprobe"],
+                                       prof.gamma_f32(), C.c_void_p(h_ids[b:].ctypes.data),
+                                       C.c_void_p(h_d[b:].ctypes.data), C.c_void_p(h_ct[b:].ctypes.data)),
+                   "search_trim_ivf_knn")
+        return int(h_ct[b:b + nb, 3].sum())
 
     def once():
         return sum(pool.map(one, range(0, nq, B)))
@@ -502,7 +514,7 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
     return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
                 h2d_bytes_per_step=nq * cfg["dim"] * 4,
                 d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
-                api=f"trim_search_knn (C ABI, host buffers; pinned source; {max(1, args.streams)} client threads)",
+                api=f"trim_search_knn (C ABI, host buffers; pinned queries and results; {max(1, args.streams)} client threads)",
                 shard_local=world > 1)
 
 

@@ -1002,16 +1002,28 @@ def run_ours_graph(args, cfg):
         pool = ThreadPoolExecutor(max(1, args.streams))
         prof = PruningProfile.manual(head)
 
-        def one(b):
-            _, _, c = GG.search_trim_knn_batch(gg, prof, hq[b:b + B], k, ef)
-            return int(c[:, 3].sum())
+        from paper_2508_17828_b200 import _lib
+        import ctypes as C
+        lib = _lib.load()
+        nh = len(hq)
+        h_ids = torch.empty((nh, k), dtype=torch.int32).pin_memory().numpy()
+        h_d = torch.empty((nh, k), dtype=torch.float32).pin_memory().numpy()
+        h_ct = torch.empty((nh, 6), dtype=torch.int64).pin_memory().numpy()
+
+        def one(b):  # pinned queries in, pinned results out (the serving client's staging memory)
+            nb = min(B, nh - b)
+            _lib.check(lib.trim_graph_search_knn(gg.handle, C.c_void_p(hq[b:].ctypes.data), nb, k, ef,
+                                                 prof.gamma_f32(), C.c_void_p(h_ids[b:].ctypes.data),
+                                                 C.c_void_p(h_d[b:].ctypes.data), C.c_void_p(h_ct[b:].ctypes.data)),
+                       "search_trim_knn")
+            return int(h_ct[b:b + nb, 3].sum())
         sum(pool.map(one, range(0, len(hq), B)))
         t0 = time.perf_counter()
         cand = sum(pool.map(one, range(0, len(hq), B)))
         sec = time.perf_counter() - t0
         out["e2e"] = dict(value=cand / sec, unit="candidates/s", qps=len(hq) / sec,
                           h2d_bytes_per_step=len(hq) * D * 4, d2h_bytes_per_step=len(hq) * (k * 8 + 48),
-                          api=f"trim_graph_search_knn (C ABI, host buffers; {max(1, args.streams)} client threads)")
+                          api=f"trim_graph_search_knn (C ABI, pinned host queries and results; {max(1, args.streams)} client threads)")
         if world == 1 and not args.skip_cpu:
             threads = os.cpu_count() or 1
             sec, n, cct = graph_cpu_timer(ga, cfg, head, queries.cpu().numpy(), args.cpu_seconds, threads)

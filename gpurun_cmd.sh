@@ -1,4 +1,3 @@
 #!/bin/bash
-timeout -s KILL 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest.log
-timeout 600 python tests/perf_modes.py --gammas 0.8,0.6 --reps 3 2>&1 | grep gamma | tail -2
-cat gpurun_out/pytest.log
+export BENCH_ALLOW_SHORT=1
+timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu --recall-q 0 2>/dev/null | python -c "import json,sys; j=json.loads(sys.stdin.read()); print('c2', '%.3e'%j['value'], 'e2e %.3e'%j['e2e']['value'], j['e2e']['api'])"

@@ -1,3 +1,4 @@
 #!/bin/bash
 export BENCH_ALLOW_SHORT=1
-timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu --recall-q 0 2>/dev/null | python -c "import json,sys; j=json.loads(sys.stdin.read()); print('c2', '%.3e'%j['value'], 'e2e %.3e'%j['e2e']['value'], j['e2e']['api'])"
+timeout 2400 python bench.py --config c5 --nq 2048 --steps 1 --warmup 3 --cpu-seconds 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.log; echo c5 rc=$?
+tail -3 gpurun_out/bench_c5.log

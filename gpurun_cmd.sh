@@ -1,4 +1,7 @@
 #!/bin/bash
+# The round's GPU checks (run via: gpurun --timeout 3000 -- ./gpurun_cmd.sh):
+# parity suite, smoke, and the default bench line.
 export BENCH_ALLOW_SHORT=1
-timeout 2400 python bench.py --config c5 --nq 2048 --steps 1 --warmup 3 --cpu-seconds 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.log; echo c5 rc=$?
-tail -3 gpurun_out/bench_c5.log
+timeout -s KILL 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log; echo bench rc=$?

@@ -87,6 +87,14 @@ cudaStream_t thread_stream(int device) {
     return streams[device];
 }
 
+// A pinned host word per thread (status readbacks without a pageable copy).
+uint32_t* pinned_word() {
+    thread_local uint32_t* w = nullptr;
+    if (!w)
+        CK(cudaMallocHost(&w, sizeof(uint32_t)));
+    return w;
+}
+
 // RAII stream-ordered device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -1230,15 +1238,15 @@ int trim_search_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t
                                 d_dist.as<float>(), d_ct.as<unsigned long long>(),
                                 d_status.as<uint32_t>(), st))
             return rc;
-        uint32_t status = 0;
+        uint32_t* status_h = pinned_word(); // pinned: the readback stays an async copy
         CK(cudaMemcpyAsync(ids_out, d_ids.p, sizeof(uint32_t) * nq * k, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(dist_out, d_dist.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
         if (counters_out)
             CK(cudaMemcpyAsync(counters_out, d_ct.p, sizeof(trim_counters) * nq,
                                cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&status, d_status.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(status_h, d_status.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (status & 1u)
+        if (*status_h & 1u)
             return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k exceeds probed vectors");
         return TRIM_OK;
     });

@@ -24,7 +24,10 @@
 namespace trimgpu {
 
 constexpr uint32_t kFlatKB = 32;      // floats of K per stage
-constexpr uint32_t kFlatStages = 3;
+#ifndef TRIM_FLAT_STAGES
+#define TRIM_FLAT_STAGES 3
+#endif
+constexpr uint32_t kFlatStages = TRIM_FLAT_STAGES;
 constexpr uint32_t kFlatBlockBytes = kMmaM * kFlatKB * 4; // 16 KB per operand per stage
 
 __host__ __device__ inline uint32_t flat_kpad(uint32_t dim) { return (dim + kFlatKB - 1) / kFlatKB * kFlatKB; }

@@ -394,8 +394,8 @@ def run_ours(args, cfg):
     out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
                          queries=nq, batch=B, m=cfg["m"], nlist=cfg["nlist"],
                          nprobe=cfg["nprobe"], k=k, gamma=head,
-                         parallelism=(f"replicas x{world}" if replicas else f"id-shard x{world}") if world > 1
-                         else "single",
+                         parallelism=(f"replicas x{world}" if replicas else f"id-shard x{world}")
+                         if (world > 1 or sharded) else "single",
                          l2="index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
                          else "index fits L2; reported as-is",
                          data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))

@@ -33,14 +33,14 @@
 extern "C" {
 #endif
 
-#define TRIM_ABI_VERSION 2
+#define TRIM_ABI_VERSION 3
 
 typedef enum {
     TRIM_OK = 0,
     TRIM_EINVAL = 1, /* std::invalid_argument in the reference */
     TRIM_EDATA = 2,  /* trimsearch::DataError */
     TRIM_ECUDA = 3,  /* CUDA runtime / launch failure, or no device */
-    TRIM_ENCCL = 4,  /* reserved for the collective layer */
+    TRIM_ENCCL = 4,  /* NCCL failure in a multi-device (id_shard) index */
     TRIM_ENOMEM = 5
 } trim_status;
 
@@ -59,6 +59,20 @@ typedef enum {
     TRIM_MEM_HOST = 0,  /* descriptor arrays are host pointers */
     TRIM_MEM_DEVICE = 1 /* descriptor arrays are device pointers on `device` */
 } trim_memory;
+
+/* Multi-device layouts. */
+typedef enum {
+    TRIM_SHARD_SINGLE = 0,   /* one device: `device` */
+    TRIM_SHARD_ID = 1,       /* the rows split by id over devices[]: device p holds ids
+                                [p*n/W, (p+1)*n/W) (per list, that sub-range of the list);
+                                codebook + coarse quantizer replicated. A search runs every
+                                shard's filter on its sub-stream of each query, then the
+                                per-shard top-k (dist, id) are all-gathered (ncclAllGather over
+                                NVLink; device-to-device copies when entries of devices[]
+                                repeat, e.g. W shards on one GPU) and merged by (dist, id). */
+    TRIM_SHARD_REPLICAS = 2  /* the whole index on every device; a batch's queries split into
+                                contiguous slices, one per device; no collective */
+} trim_shard_mode;
 
 /*
  * Index descriptor: trimsearch::ivf::IvfIndex (ivf/ivf.hpp:37-51) flattened to
@@ -92,6 +106,15 @@ typedef struct {
     uint64_t id_base;
     int device;
     trim_memory memory;
+    /* ABI 3: multi-device layout. ndevices == 0 (or shard_mode SINGLE): one
+     * device, `device`. Otherwise devices[0..ndevices) (entries may repeat) and
+     * `device` is ignored; the descriptor holds the WHOLE index (id_base 0, host
+     * memory, or device memory on devices[0]); results are returned as for one
+     * index. Per-query counters of an id_shard search are the shards' sums
+     * (coarse_dc: nlist, the probe runs once per query as in the reference). */
+    const int* devices;
+    uint32_t ndevices;
+    trim_shard_mode shard_mode;
 } trim_index_desc;
 
 typedef struct trim_index* trim_index_t;
@@ -100,9 +123,12 @@ typedef struct {
     uint32_t dim, m, ksub, nlist;
     uint64_t n, total_entries, id_base;
     uint64_t max_list_size;
-    uint64_t device_bytes;
-    int device;
+    uint64_t device_bytes;     /* summed over the devices of a multi-device index */
+    int device;                /* the (home) device */
     uint32_t range_query_tile; /* queries sharing one code stream in the flat range scan */
+    uint32_t ndevices;         /* 1 for a single-device index */
+    uint32_t shard_mode;       /* trim_shard_mode */
+    uint32_t nccl;             /* 1: the id_shard exchange runs over NCCL */
 } trim_index_info;
 
 const char* trim_last_error(void);
@@ -159,9 +185,13 @@ int trim_search_baseline_ivfpq(trim_index_t index, const float* queries, uint64_
  * Device-resident variants (inputs already in HBM; used by the serving loop
  * and bench.py's device-timed leg). All pointers are device pointers on the
  * index's device; the call is asynchronous on `stream` (a cudaStream_t, NULL =
- * per-thread default). A query whose probed stream is shorter than k gets
- * ids = 0xFFFFFFFF and dist = +inf, and bit 0 of *status_out (device u32, may
- * be NULL) is set.
+ * per-thread default). A query whose probed stream is shorter than k sets bit
+ * 0 of *status_out (device u32, may be NULL); its row holds the partial top-k
+ * (every entry of the stream, ascending (dist, id)) padded with
+ * (+inf, 0xFFFFFFFF). For a multi-device index the pointers are on its home
+ * device (devices[0]) and `stream` is a home-device stream: the library moves
+ * the queries to the other devices and the results back itself (id_shard:
+ * NCCL broadcast / all-gather), ordered after / before the work on `stream`.
  */
 int trim_search_knn_device(trim_index_t index, const float* d_queries, uint64_t nq, uint32_t k,
                            uint32_t nprobe, float gamma, uint32_t* d_ids, float* d_dist,

@@ -435,6 +435,10 @@ class RefOracle:
         L.ref_session_destroy.argtypes = [C.c_void_p]
         L.ref_session_run.argtypes = [C.c_void_p, C.c_int, _f32p, C.c_uint64, C.c_uint32,
                                       C.c_uint32, C.c_double, C.c_double, _f64p, _u64p]
+        L.ref_session_knn.argtypes = [C.c_void_p, _f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
+                                      _u32p, _f32p, _u64p]
+        L.ref_session_range.argtypes = [C.c_void_p, _f32p, C.c_uint64, _f32p, C.c_uint32, C.c_double,
+                                        C.c_uint64, _u32p, _f32p, _u64p, _u64p]
         L.ref_ground_truth_knn.argtypes = [_f32p, C.c_uint64, C.c_uint32, _f32p, C.c_uint64,
                                            C.c_uint32, _u32p, _f32p]
         L.ref_pick_radius.argtypes = [_f32p, C.c_uint64, C.c_uint32, _f32p, C.c_uint64,
@@ -770,6 +774,40 @@ class RefOracle:
                                            gamma, arg, C.byref(sec), _ptr(ct, _u64p)),
                   "session_run")
         return sec.value, ct
+
+    def session_knn(self, s, qs, k, nprobe, gamma):
+        """ivf::search_trim_ivf_knn per query over a session's index ->
+        (ids[nq,k] u32, dist[nq,k] f32, counters[nq,5] u64, coarse_dc[nq])."""
+        qs = np.ascontiguousarray(qs, np.float32)
+        nq = qs.shape[0]
+        ids = np.zeros((nq, k), np.uint32)
+        dist = np.zeros((nq, k), np.float32)
+        ct = np.zeros((nq, 6), np.uint64)
+        self._err(self.lib.ref_session_knn(s, _ptr(qs, _f32p), nq, k, nprobe, gamma, _ptr(ids, _u32p),
+                                           _ptr(dist, _f32p), _ptr(ct, _u64p)), "search_trim_ivf_knn")
+        return ids, dist, ct[:, :5].copy(), ct[:, 5].copy()
+
+    def session_range(self, s, qs, radius, nprobe, gamma, cap=1024):
+        """ivf::search_trim_ivf_range per query over a session's index ->
+        (offsets[nq+1], ids, dist, counters[nq,5], coarse_dc[nq])."""
+        qs = np.ascontiguousarray(qs, np.float32)
+        nq = qs.shape[0]
+        rad = np.ascontiguousarray(np.broadcast_to(np.float32(radius), (nq,)), np.float32) \
+            if np.ndim(radius) == 0 else np.ascontiguousarray(radius, np.float32)
+        ids = np.zeros((nq, cap), np.uint32)
+        dist = np.zeros((nq, cap), np.float32)
+        cnt = np.zeros(nq, np.uint64)
+        ct = np.zeros((nq, 6), np.uint64)
+        self._err(self.lib.ref_session_range(s, _ptr(qs, _f32p), nq, _ptr(rad, _f32p), nprobe, gamma, cap,
+                                             _ptr(ids, _u32p), _ptr(dist, _f32p), _ptr(cnt, _u64p),
+                                             _ptr(ct, _u64p)), "search_trim_ivf_range")
+        if nq and int(cnt.max()) > cap:
+            return self.session_range(s, qs, rad, nprobe, gamma, cap=int(cnt.max()))
+        offs = np.zeros(nq + 1, np.uint64)
+        offs[1:] = np.cumsum(cnt)
+        oid = np.concatenate([ids[i, :cnt[i]] for i in range(nq)]) if nq else np.zeros(0, np.uint32)
+        od = np.concatenate([dist[i, :cnt[i]] for i in range(nq)]) if nq else np.zeros(0, np.float32)
+        return offs, oid, od, ct[:, :5].copy(), ct[:, 5].copy()
 
     def session_destroy(self, s):
         self.lib.ref_session_destroy(s)

@@ -441,6 +441,65 @@ int ref_session_run(void* p, int kind, const float* qs, std::uint64_t nq, std::u
     });
 }
 
+// Per-query results over a session's index (no per-call copy of a 10M-row
+// index): ivf::search_trim_ivf_knn (ivf.hpp:243-304) for every query of the
+// batch, parallel_for over queries. ids/dist nq*k; counters 6 per query.
+int ref_session_knn(void* p, const float* qs, std::uint64_t nq, std::uint32_t k, std::uint32_t nprobe,
+                    double gamma, std::uint32_t* ids_out, float* dist_out, std::uint64_t* counters_out) {
+    auto* s = static_cast<RefSession*>(p);
+    return guarded([&] {
+        const auto prof = trim::PruningProfile::manual(gamma);
+        std::vector<std::string> errs(nq);
+        parallel_for(nq, [&](std::size_t qi) {
+            try {
+                const auto r = ivf::search_trim_ivf_knn(s->ix, s->ds, prof,
+                                                        VectorView(qs + qi * s->ds.dim, s->ds.dim), k, nprobe);
+                for (std::size_t i = 0; i < r.ids.size(); ++i) {
+                    ids_out[qi * k + i] = r.ids[i];
+                    dist_out[qi * k + i] = r.dist_sq[i];
+                }
+                put_counters(counters_out + qi * 6, r.counters, r.coarse_dc);
+            } catch (const std::exception& e) {
+                errs[qi] = e.what();
+            }
+        });
+        for (const auto& e : errs)
+            if (!e.empty())
+                throw std::invalid_argument(e);
+    });
+}
+
+// ivf::search_trim_ivf_range (ivf.hpp:308-347) over a session's index: query
+// qi's members at ids/dist + qi*cap (truncated to cap), counts_out[qi] = the
+// true count.
+int ref_session_range(void* p, const float* qs, std::uint64_t nq, const float* radius, std::uint32_t nprobe,
+                      double gamma, std::uint64_t cap, std::uint32_t* ids_out, float* dist_out,
+                      std::uint64_t* counts_out, std::uint64_t* counters_out) {
+    auto* s = static_cast<RefSession*>(p);
+    return guarded([&] {
+        const auto prof = trim::PruningProfile::manual(gamma);
+        std::vector<std::string> errs(nq);
+        parallel_for(nq, [&](std::size_t qi) {
+            try {
+                const auto r = ivf::search_trim_ivf_range(s->ix, s->ds, prof,
+                                                          VectorView(qs + qi * s->ds.dim, s->ds.dim), radius[qi],
+                                                          nprobe);
+                counts_out[qi] = r.ids.size();
+                for (std::size_t i = 0; i < r.ids.size() && i < cap; ++i) {
+                    ids_out[qi * cap + i] = r.ids[i];
+                    dist_out[qi * cap + i] = r.dist_sq[i];
+                }
+                put_counters(counters_out + qi * 6, r.counters, r.coarse_dc);
+            } catch (const std::exception& e) {
+                errs[qi] = e.what();
+            }
+        });
+        for (const auto& e : errs)
+            if (!e.empty())
+                throw std::invalid_argument(e);
+    });
+}
+
 // ---- on-disk formats (test infrastructure: pins paper_2508_17828_b200/formats.py)
 // IvfIndex::save (ivf.hpp:53-76), with the codebook's bookkeeping fields set.
 int ref_ivf_save(const FlatIndex* f, double training_mse, std::uint64_t seed, std::uint32_t iters,

@@ -25,174 +25,11 @@
 
 using namespace trimgpu;
 
-namespace {
+#include "trim_host.h"
 
-thread_local std::string g_err;
-// Perf probe (profiles/knn_timeline.py): device buffer of nq*kTimeline u64 that the next kNN
-// launches on this thread fill with per-CTA phase timestamps; null disables.
-thread_local unsigned long long* g_timeline = nullptr;
+using namespace trimhost;
 
-int set_err(int code, const char* fmt, ...) {
-    char buf[1024];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
-    va_end(ap);
-    g_err = buf;
-    return code;
-}
-
-struct CudaError {
-    int code;
-};
-
-#define CK(call)                                                                          \
-    do {                                                                                  \
-        cudaError_t _e = (call);                                                          \
-        if (_e != cudaSuccess) {                                                          \
-            set_err(TRIM_ECUDA, "CUDA error %s (%s) at %s:%d", cudaGetErrorName(_e),      \
-                    cudaGetErrorString(_e), __FILE__, __LINE__);                          \
-            throw CudaError{TRIM_ECUDA};                                                  \
-        }                                                                                 \
-    } while (0)
-
-template <typename Fn>
-int guarded(Fn&& fn) {
-    try {
-        return fn();
-    } catch (const CudaError& e) {
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        return set_err(TRIM_ENOMEM, "host allocation failed");
-    } catch (const std::runtime_error& e) { // a nested trim_* call failed (message kept)
-        return set_err(TRIM_ECUDA, "%s", e.what());
-    }
-}
-
-uint32_t round_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
-
-uint32_t pow2_at_least(uint32_t x) {
-    uint32_t p = 1;
-    while (p < x)
-        p <<= 1;
-    return p;
-}
-
-cudaStream_t thread_stream(int device) {
-    thread_local std::vector<cudaStream_t> streams;
-    if (static_cast<int>(streams.size()) <= device)
-        streams.resize(device + 1, nullptr);
-    if (!streams[device])
-        CK(cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking));
-    return streams[device];
-}
-
-// A pinned host word per thread (status readbacks without a pageable copy).
-uint32_t* pinned_word() {
-    thread_local uint32_t* w = nullptr;
-    if (!w)
-        CK(cudaMallocHost(&w, sizeof(uint32_t)));
-    return w;
-}
-
-// RAII stream-ordered device buffer.
-struct DevBuf {
-    void* p = nullptr;
-    cudaStream_t s = nullptr;
-    DevBuf() = default;
-    DevBuf(size_t bytes, cudaStream_t st) : s(st) {
-        if (bytes)
-            CK(cudaMallocAsync(&p, bytes, st));
-    }
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
-    DevBuf& operator=(DevBuf&& o) noexcept {
-        std::swap(p, o.p);
-        std::swap(s, o.s);
-        return *this;
-    }
-    ~DevBuf() {
-        if (p)
-            cudaFreeAsync(p, s);
-    }
-    template <typename T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-} // namespace
-
-struct trim_index {
-    int device = 0;
-    DevIndex dev{};
-    uint32_t code_stride_host = 0;
-    uint64_t total = 0;
-    std::vector<uint64_t> list_offsets;  // host copy
-    std::vector<uint64_t> top_prefix;    // prefix sums of list sizes sorted descending
-    uint64_t max_list = 0;
-    uint32_t max_sub_dim = 0;
-    unsigned long long* d_skipped = nullptr; // trim_index_skip_stats
-    // tensor-core probe (trim_probe_mma.cuh): pre-tiled centroids and norms
-    float4* coarse_t = nullptr;
-    float* cn2 = nullptr;
-    float* cn = nullptr;
-    // flat kNN distance bounds (trim_flat_mma.cuh): pre-tiled rows + norms, built on first use
-    std::mutex flat_mu;
-    float4* flat_tiles = nullptr;
-    float* xn = nullptr;
-    float* xn2 = nullptr;
-    // flat range search: a block partition of the rows (build_flat_partition), built on first use
-    std::mutex part_mu;
-    bool part_tried = false;
-    uint32_t part_nb = 0;
-    DevIndex part{};
-    float4* part_tiles = nullptr;
-    float* part_cn2 = nullptr;
-    float* part_cn = nullptr;
-    uint64_t bytes = 0;
-    std::vector<void*> allocs;
-
-    ~trim_index() {
-        if (!allocs.empty()) {
-            int prev = 0;
-            cudaGetDevice(&prev);
-            cudaSetDevice(device);
-            for (void* p : allocs)
-                cudaFree(p);
-            cudaSetDevice(prev);
-        }
-    }
-
-    template <typename T>
-    T* alloc(size_t count) {
-        void* p = nullptr;
-        const size_t b = std::max<size_t>(sizeof(T) * count, 16);
-        CK(cudaMalloc(&p, b));
-        allocs.push_back(p);
-        bytes += b;
-        return static_cast<T*>(p);
-    }
-
-    // Upper bound on a query's stream length at `np` probes.
-    uint64_t stream_bound(uint32_t np) const {
-        np = std::min<uint32_t>(np, dev.nlist);
-        return top_prefix[np];
-    }
-};
-
-namespace {
-
-struct DeviceGuard {
-    int prev = 0;
-    explicit DeviceGuard(int d) {
-        CK(cudaGetDevice(&prev));
-        if (prev != d)
-            CK(cudaSetDevice(d));
-    }
-    ~DeviceGuard() { cudaSetDevice(prev); }
-};
+namespace trimhost {
 
 int check_device_present() {
     int n = 0;
@@ -1009,15 +846,36 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
         return set_err(TRIM_EINVAL, "trim_index_create: null array in descriptor");
     if (int rc = check_device_present())
         return rc;
+    if (d->ndevices > 0 && d->shard_mode != TRIM_SHARD_SINGLE) {
+        if (!d->devices)
+            return set_err(TRIM_EINVAL, "trim_index_create: ndevices > 0 needs devices[]");
+        if (d->shard_mode != TRIM_SHARD_ID && d->shard_mode != TRIM_SHARD_REPLICAS)
+            return set_err(TRIM_EINVAL, "trim_index_create: unknown shard_mode %d", (int)d->shard_mode);
+        return guarded([&]() -> int { return group_create(d, out); });
+    }
+    return create_single(d, out);
+}
+
+} // extern "C"
+
+int trimhost::create_single(const trim_index_desc* d, trim_index** out) {
+    *out = nullptr;
     return guarded([&]() -> int {
         const bool host = d->memory == TRIM_MEM_HOST;
         const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         DeviceGuard g(d->device);
-        { // keep stream-ordered workspaces (probe scratch, results) cached in the pool
+        { // keep the per-call stream-ordered workspaces (queries, probe scratch,
+          // results: tens of MB per batch) cached in the device's pool, but
+          // return anything beyond 1 GiB (e.g. a flat-bound slice) to the device
+          // at the next synchronisation, so it never starves other allocators
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
-                uint64_t thr = ~0ull;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                uint64_t thr = 0;
+                cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                if (thr < (1ull << 30)) {
+                    thr = 1ull << 30;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
             }
         }
         auto* ix = new trim_index;
@@ -1173,6 +1031,8 @@ int trim_index_create(const trim_index_desc* d, trim_index_t* out) {
     });
 }
 
+extern "C" {
+
 int trim_index_destroy(trim_index_t index) {
     delete index;
     return TRIM_OK;
@@ -1191,13 +1051,35 @@ int trim_index_get_info(trim_index_t ix, trim_index_info* info) {
     info->max_list_size = ix->max_list;
     info->device_bytes = ix->bytes;
     info->device = ix->device;
-    info->range_query_tile = range_flat_qt(ix->dev);
+    info->range_query_tile = ix->is_group() ? range_flat_qt(ix->parts[0]->dev) : range_flat_qt(ix->dev);
+    info->ndevices = ix->is_group() ? static_cast<uint32_t>(ix->parts.size()) : 1u;
+    info->shard_mode = ix->shard_mode;
+    info->nccl = ix->nccl ? 1u : 0u;
+    if (ix->is_group()) {
+        info->device_bytes = 0;
+        info->max_list_size = 0;
+        for (const trim_index* pt : ix->parts) {
+            info->device_bytes += pt->bytes;
+            info->max_list_size = std::max(info->max_list_size, pt->max_list);
+        }
+    }
     return TRIM_OK;
 }
 
 int trim_index_skip_stats(trim_index_t ix, uint64_t* skipped, int reset) {
     if (!ix || !skipped)
         return set_err(TRIM_EINVAL, "trim_index_skip_stats: null argument");
+    if (ix->is_group()) { // summed over the parts
+        uint64_t tot = 0;
+        for (trim_index* pt : ix->parts) {
+            uint64_t v = 0;
+            if (int rc = trim_index_skip_stats(pt, &v, reset))
+                return rc;
+            tot += v;
+        }
+        *skipped = tot;
+        return TRIM_OK;
+    }
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         CK(cudaDeviceSynchronize());
@@ -1213,6 +1095,8 @@ int trim_index_skip_stats(trim_index_t ix, uint64_t* skipped, int reset) {
 int trim_probe_launches(trim_index_t ix, uint32_t nprobe, uint32_t* launches) {
     if (!ix || !launches)
         return set_err(TRIM_EINVAL, "trim_probe_launches: null argument");
+    if (ix->is_group())
+        ix = ix->parts[0];
     const uint32_t np = std::min(nprobe, ix->dev.nlist);
     *launches = (ix->dev.nlist == 1 || np == 0) ? 0u : (probe_uses_mma(ix, np) ? 2u : 1u);
     return TRIM_OK;
@@ -1227,6 +1111,10 @@ int trim_search_knn(trim_index_t ix, const float* queries, uint64_t nq, uint32_t
         return rc;
     if (nq == 0)
         return TRIM_OK;
+    if (ix->is_group())
+        return guarded([&]() -> int {
+            return group_search_knn(ix, queries, nq, k, nprobe, gamma, ids_out, dist_out, counters_out);
+        });
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = thread_stream(ix->device);
@@ -1261,6 +1149,11 @@ int trim_search_knn_device(trim_index_t ix, const float* d_queries, uint64_t nq,
         return rc;
     if (nq == 0)
         return TRIM_OK;
+    if (ix->is_group())
+        return guarded([&]() -> int {
+            return group_search_knn_device(ix, d_queries, nq, k, nprobe, gamma, d_ids, d_dist, d_counters, d_status,
+                                           stream);
+        });
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1280,6 +1173,8 @@ int trim_probe_device(trim_index_t ix, const float* d_queries, uint64_t nq, uint
         return set_err(TRIM_EINVAL, "probe_order: null index");
     if (nq == 0 || nprobe == 0)
         return TRIM_OK;
+    if (ix->is_group()) // the coarse quantizer is replicated: the home part's probe order
+        ix = ix->parts[0];
     if (ix->dev.dim_stride != ix->dev.dim)
         return set_err(TRIM_EINVAL, "trim_probe_device: dim must be a multiple of 4 (use trim_probe)");
     return guarded([&]() -> int {
@@ -1303,6 +1198,9 @@ int trim_search_knn_preassigned_device(trim_index_t ix, const float* d_queries, 
         return set_err(TRIM_EINVAL, "search_trim_ivf_knn: null index");
     if (int rc = validate_knn(k, gamma))
         return rc;
+    if (ix->is_group())
+        return set_err(TRIM_EINVAL, "trim_search_knn_preassigned_device: takes a single-device index "
+                                    "(a multi-device index: trim_search_knn_device)");
     if (np > ix->dev.nlist)
         return set_err(TRIM_EINVAL, "search_trim_ivf_knn: np > nlist");
     if (ix->dev.dim_stride != ix->dev.dim)
@@ -1334,6 +1232,11 @@ int trim_search_range(trim_index_t ix, const float* queries, uint64_t nq, const 
         *dist_out = static_cast<float*>(std::malloc(4));
         return TRIM_OK;
     }
+    if (ix->is_group())
+        return guarded([&]() -> int {
+            return group_search_range(ix, queries, nq, radius, nprobe, gamma, offsets_out, ids_out, dist_out,
+                                      counters_out);
+        });
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = thread_stream(ix->device);
@@ -1449,6 +1352,9 @@ int trim_search_range_device(trim_index_t ix, const float* d_queries, uint64_t n
         return set_err(TRIM_EINVAL, "search_trim_ivf_range: uncalibrated pruning profile");
     if (cap == 0)
         return set_err(TRIM_EINVAL, "trim_search_range_device: cap must be positive");
+    if (ix->is_group())
+        return set_err(TRIM_EINVAL, "trim_search_range_device: takes a single-device index "
+                                    "(a multi-device index: trim_search_range)");
     if (ix->dev.dim_stride != ix->dev.dim)
         return set_err(TRIM_EINVAL, "trim_search_range_device: dim must be a multiple of 4");
     if (nq == 0)
@@ -1504,6 +1410,11 @@ int trim_ground_truth_knn(trim_index_t ix, const float* queries, uint64_t nq, ui
         return set_err(TRIM_EINVAL, "brute_force_knn: k out of range");
     if (k > kGtCap)
         return set_err(TRIM_EINVAL, "ground_truth_knn: k > 4096 is not supported by the GPU selection");
+    if (ix->is_group()) {
+        if (ix->shard_mode != TRIM_SHARD_REPLICAS)
+            return set_err(TRIM_EINVAL, "ground_truth_knn: needs every row on one device (single or replicas index)");
+        ix = ix->parts[0];
+    }
     if (nq == 0)
         return TRIM_OK;
     return guarded([&]() -> int {
@@ -1554,6 +1465,10 @@ int trim_search_baseline_ivfpq(trim_index_t ix, const float* queries, uint64_t n
         return set_err(TRIM_EINVAL, "search_baseline_ivfpq: nprobe must be positive");
     if (nq == 0)
         return TRIM_OK;
+    if (ix->is_group())
+        return guarded([&]() -> int {
+            return group_search_baseline(ix, queries, nq, k, nprobe, k_prime, ids_out, dist_out, counters_out);
+        });
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = thread_stream(ix->device);
@@ -1570,6 +1485,8 @@ int trim_build_lut(trim_index_t ix, const float* queries, uint64_t nq, float* lu
         return set_err(TRIM_EINVAL, "build_distance_table: null index");
     if (nq == 0)
         return TRIM_OK;
+    if (ix->is_group()) // the codebook is replicated
+        ix = ix->parts[0];
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = thread_stream(ix->device);
@@ -1591,6 +1508,8 @@ int trim_probe(trim_index_t ix, const float* queries, uint64_t nq, uint32_t npro
         return set_err(TRIM_EINVAL, "probe_order: null index");
     if (nq == 0)
         return TRIM_OK;
+    if (ix->is_group()) // the coarse quantizer is replicated
+        ix = ix->parts[0];
     return guarded([&]() -> int {
         DeviceGuard g(ix->device);
         cudaStream_t st = thread_stream(ix->device);

@@ -141,7 +141,9 @@ struct WarpTopK {
         reduce_worst();
     }
 
-    // Rows ascending by (dist, id) (ivf.hpp:292-302).
+    // Rows ascending by (dist, id) (ivf.hpp:292-302). Unfilled slots (fewer
+    // than k entries offered: a shard whose stream is shorter than k) keep their
+    // (+inf, 0xFFFFFFFF) sentinels and sort last; the slot index breaks their ties.
     __device__ __forceinline__ void store_sorted(uint32_t k, uint32_t* ids_out, float* dist_out) {
         const uint32_t lane = lane_id();
 #pragma unroll
@@ -154,7 +156,7 @@ struct WarpTopK {
                     const float od = __shfl_sync(0xffffffffu, d[r2], l);
                     const uint32_t oi = __shfl_sync(0xffffffffu, id[r2], l);
                     const uint32_t os = static_cast<uint32_t>(r2) * kWarp + l;
-                    if (os < k && scored_less(od, oi, d[r], id[r]))
+                    if (os < k && less3(od, oi, os, d[r], id[r], slot))
                         ++rank;
                 }
             }
@@ -678,16 +680,13 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         })
         uint32_t* io = p.ids_out + static_cast<size_t>(q) * p.k;
         float* dout = p.dist_out + static_cast<size_t>(q) * p.k;
-        if (total < p.k) {
-            for (uint32_t i = lane; i < p.k; i += kWarp) {
-                io[i] = kInvalidId;
-                dout[i] = kInf;
-            }
-            if (lane == 0 && p.status)
-                atomicOr(p.status, 1u);
-        } else {
-            topk.store_sorted(p.k, io, dout);
-        }
+        // a stream shorter than k: the reference throws after the scan
+        // (ivf.hpp:289-290) — status bit 0; the rows keep the partial sorted
+        // top-k padded with (+inf, 0xFFFFFFFF), which an id-sharded caller merges
+        // (the error is then decided on the total over the shards)
+        if (total < p.k && lane == 0 && p.status)
+            atomicOr(p.status, 1u);
+        topk.store_sorted(p.k, io, dout);
         if (lane == 0 && p.counters) {
             unsigned long long* cc = p.counters + static_cast<size_t>(q) * 6;
             const uint64_t evaluated = total;

@@ -137,14 +137,18 @@ class ShardedIvfIndex:
                 st = torch.zeros(1, dtype=torch.int32, device=q.device)
                 cnt, ids, d = search_trim_ivf_range_device(self.gpu, PruningProfile.manual(g), q, r, npb, cap=c,
                                                            d_counters=cts, d_status=st)
-                if int(st.item()) & 1:
-                    raise RuntimeError("range result larger than cap")
                 return cnt, ids, d, cts
         cnt, ids, d, cts = range_searcher(queries, radius, nprobe, gamma, cap)
         nq = cnt.shape[0]
         dev = cnt.device
         mx = cnt.max().reshape(1).to(torch.int64) if nq else torch.zeros(1, dtype=torch.int64, device=dev)
+        # the largest member count over every rank; a rank whose result outgrew
+        # `cap` finds out together with all the others (no rank raises alone and
+        # leaves the rest waiting in a collective), and every rank re-runs with
+        # the exact size
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.group)
+        if int(mx.item()) > cap:
+            return self.search_range(queries, radius, nprobe, gamma, range_searcher, cap=int(mx.item()))
         w = max(1, int(mx.item()))
         # (dist bits << 32 | id) sorts like (dist, id) for non-negative dist; padding sorts last
         keys = torch.full((nq, w), -1, dtype=torch.int64, device=dev)
@@ -185,8 +189,17 @@ class ShardedIvfIndex:
         dist.all_gather_into_tensor(g_ids, ids.contiguous(), group=self.group)
         dist.all_gather_into_tensor(g_d, d.contiguous(), group=self.group)
         md, mi = self._merge(g_d.view(self.world, nq, k), g_ids.view(self.world, nq, k), k)
+        # per-query counters summed over the shards. A shard whose share of a
+        # query's probed lists is shorter than k returns its partial top-k
+        # (padded with sentinels, merged above); the reference's "k exceeds
+        # probed vectors" (ivf.hpp:289-290) is decided on the total stream
+        # length, identically on every rank
+        cts = cts.to(torch.int64).contiguous()
+        dist.all_reduce(cts, group=self.group)
+        if nq and bool((cts[:, 3] < k).any()):
+            from ._lib import InvalidArgument
+            raise InvalidArgument("search_trim_ivf_knn: k exceeds probed vectors")
         c = cts[:, :5].sum(0)
-        dist.all_reduce(c, group=self.group)
         return mi, md, c
 
 
@@ -215,8 +228,12 @@ class ReplicaIvfIndex:
             def searcher(q, k, nprobe, gamma):
                 import torch
                 cts = torch.zeros((q.shape[0], 6), dtype=torch.int64, device=q.device)
+                st = torch.zeros(1, dtype=torch.int32, device=q.device)
                 ids, d = search_trim_ivf_knn_device(self.gpu, PruningProfile.manual(gamma), q, k, nprobe,
-                                                    d_counters=cts)
+                                                    d_counters=cts, d_status=st)
+                if int(st.item()) & 1:  # each replica is the single run: ivf.hpp:289-290
+                    from ._lib import InvalidArgument
+                    raise InvalidArgument("search_trim_ivf_knn: k exceeds probed vectors")
                 return ids, d, cts
         self._search = searcher
 

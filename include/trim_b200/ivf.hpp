@@ -123,8 +123,12 @@ class GpuIvfIndex {
 // (dataset.hpp:18-27): reads ix.dim, ix.nlist, ix.codebook.{params.m, params.c,
 // sub_dims, centroids}, ix.coarse_centroids, ix.lists[l].{ids, codes, lx_dist},
 // ds.{count, data}.
+// devices + mode (TRIM_SHARD_ID / TRIM_SHARD_REPLICAS): one index over several
+// GPUs of the box (include/trim_gpu.h trim_shard_mode); searches return the
+// merged answer. An empty `devices` means one device, `device`.
 template <class RefIvfIndex, class RefDataset>
-GpuIvfIndex from_reference(const RefIvfIndex& ix, const RefDataset& ds, int device = 0) {
+GpuIvfIndex from_reference(const RefIvfIndex& ix, const RefDataset& ds, int device,
+                           const std::vector<int>& devices, trim_shard_mode mode) {
     const std::uint32_t m = static_cast<std::uint32_t>(ix.codebook.params.m);
     const std::uint32_t c = static_cast<std::uint32_t>(ix.codebook.params.c);
     std::vector<std::uint32_t> sub(m);
@@ -161,7 +165,17 @@ GpuIvfIndex from_reference(const RefIvfIndex& ix, const RefDataset& ds, int devi
     d.id_base = 0;
     d.device = device;
     d.memory = TRIM_MEM_HOST;
+    if (!devices.empty() && mode != TRIM_SHARD_SINGLE) {
+        d.devices = devices.data();
+        d.ndevices = static_cast<std::uint32_t>(devices.size());
+        d.shard_mode = mode;
+    }
     return GpuIvfIndex(d);
+}
+
+template <class RefIvfIndex, class RefDataset>
+GpuIvfIndex from_reference(const RefIvfIndex& ix, const RefDataset& ds, int device = 0) {
+    return from_reference(ix, ds, device, std::vector<int>{}, TRIM_SHARD_SINGLE);
 }
 
 namespace ivf {

@@ -18,6 +18,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "trim_gpu.h")
 
 TRIM_OK, TRIM_EINVAL, TRIM_EDATA, TRIM_ECUDA, TRIM_ENCCL, TRIM_ENOMEM = range(6)
 TRIM_MEM_HOST, TRIM_MEM_DEVICE = 0, 1
+TRIM_SHARD_SINGLE, TRIM_SHARD_ID, TRIM_SHARD_REPLICAS = 0, 1, 2
+ABI_VERSION = 3
 
 _u8p = C.POINTER(C.c_uint8)
 _u32p = C.POINTER(C.c_uint32)
@@ -39,6 +41,8 @@ class TrimIndexDesc(C.Structure):
         ("code_stride", C.c_uint32), ("list_lx", C.c_void_p),
         ("n", C.c_uint64), ("vectors", C.c_void_p),
         ("id_base", C.c_uint64), ("device", C.c_int), ("memory", C.c_int),
+        # ABI 3: multi-device layout (trim_shard_mode)
+        ("devices", C.c_void_p), ("ndevices", C.c_uint32), ("shard_mode", C.c_int),
     ]
 
 
@@ -46,7 +50,8 @@ class TrimIndexInfo(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("m", C.c_uint32), ("ksub", C.c_uint32),
                 ("nlist", C.c_uint32), ("n", C.c_uint64), ("total_entries", C.c_uint64),
                 ("id_base", C.c_uint64), ("max_list_size", C.c_uint64),
-                ("device_bytes", C.c_uint64), ("device", C.c_int), ("range_query_tile", C.c_uint32)]
+                ("device_bytes", C.c_uint64), ("device", C.c_int), ("range_query_tile", C.c_uint32),
+                ("ndevices", C.c_uint32), ("shard_mode", C.c_uint32), ("nccl", C.c_uint32)]
 
 
 class TrimGraphDesc(C.Structure):
@@ -153,6 +158,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(the TRIM GPU path has no CPU fallback)")
     lib = C.CDLL(path)
+    if lib.trim_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI {lib.trim_abi_version()}, this binding speaks {ABI_VERSION}: rebuild it")
     for name, (res, args) in SIGNATURES.items():
         f = getattr(lib, name)
         f.restype = res

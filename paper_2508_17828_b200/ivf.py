@@ -114,10 +114,20 @@ def _addr(x):
     return C.c_void_p(x.ctypes.data)
 
 
-class GpuIvfIndex:
-    """Device-resident copy of an IvfIndex + VectorDataset (trim_index_create)."""
+SHARD_MODES = {"single": _lib.TRIM_SHARD_SINGLE, "id_shard": _lib.TRIM_SHARD_ID,
+               "replicas": _lib.TRIM_SHARD_REPLICAS}
 
-    def __init__(self, arrays: IvfArrays, device: int = 0):
+
+class GpuIvfIndex:
+    """Device-resident copy of an IvfIndex + VectorDataset (trim_index_create).
+
+    ``devices`` + ``shard_mode`` ("id_shard" | "replicas") build one index over
+    several devices (include/trim_gpu.h trim_shard_mode; entries may repeat,
+    e.g. four shards on cuda:0): ``arrays`` is then the whole index and every
+    search returns the merged answer (id_shard: per-part filters, NCCL
+    all-gather, device merge; replicas: query slices per device)."""
+
+    def __init__(self, arrays: IvfArrays, device: int = 0, devices=None, shard_mode: str = "single"):
         lib = _lib.load()
         a = arrays
         dev_mem = _is_torch_cuda(a.vectors)
@@ -151,6 +161,15 @@ class GpuIvfIndex:
         d.id_base = a.id_base
         d.device = device
         d.memory = _lib.TRIM_MEM_DEVICE if dev_mem else _lib.TRIM_MEM_HOST
+        if shard_mode not in SHARD_MODES:
+            raise InvalidArgument(f"shard_mode must be one of {sorted(SHARD_MODES)}")
+        if devices is not None and shard_mode != "single":
+            devs = np.ascontiguousarray(devices, np.int32)
+            keep.append(devs)
+            d.devices = C.c_void_p(devs.ctypes.data)
+            d.ndevices = len(devs)
+            d.shard_mode = SHARD_MODES[shard_mode]
+            device = int(devs[0])
         h = C.c_void_p()
         _lib.check(lib.trim_index_create(C.byref(d), C.byref(h)), "trim_index_create")
         self._h = h
@@ -161,6 +180,8 @@ class GpuIvfIndex:
         self.n = n
         self.device = device
         self.id_base = a.id_base
+        self.shard_mode = shard_mode
+        self.devices = list(devices) if devices is not None and shard_mode != "single" else [device]
 
     @property
     def handle(self):

@@ -32,7 +32,49 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _lib.load().trim_abi_version() == 2
+    assert _lib.load().trim_abi_version() == 3 == _lib.ABI_VERSION
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of trim_index_desc / trim_index_info / trim_graph_desc /
+    trim_counters have the C sizes and field offsets (a C probe compiled
+    against include/trim_gpu.h)."""
+    import os
+    import subprocess
+    structs = {"trim_index_desc": _lib.TrimIndexDesc, "trim_index_info": _lib.TrimIndexInfo,
+               "trim_graph_desc": _lib.TrimGraphDesc, "trim_counters": _lib.TrimCounters}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{_lib.HEADER}"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} sizeof %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for name, cls in structs.items():
+        assert got[(name, "sizeof")] == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[(name, f)] == getattr(cls, f).offset, (name, f)
+
+
+@pytest.mark.parametrize("kw", [dict(ndevices=2, shard_mode=1), dict(ndevices=1, shard_mode=7)])
+def test_multi_device_descriptor_validation(kw):
+    """ndevices > 0 without devices[] or with an unknown shard_mode is rejected
+    before any device work (TRIM_EINVAL) — or TRIM_ECUDA first when there is no
+    GPU at all (no CPU fallback)."""
+    lib = _lib.load()
+    sub = np.array([4, 4], np.uint32)
+    z = np.zeros(16 * 8, np.float32)
+    offs = np.array([0, 0], np.uint64)
+    d = _desc(sub_dims=sub.ctypes.data, centroids=z.ctypes.data, coarse=z.ctypes.data,
+              list_offsets=offs.ctypes.data, **kw)
+    h = C.c_void_p()
+    rc = lib.trim_index_create(C.byref(d), C.byref(h))
+    assert rc in (_lib.TRIM_EINVAL, _lib.TRIM_ECUDA)
 
 
 def _desc(**kw):

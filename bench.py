@@ -164,90 +164,161 @@ def measured_peaks():
 
 
 def ncu_traffic(workload: str):
-    """Per-launch DRAM bytes of the filter kernel from the committed ncu capture."""
+    """DRAM bytes per launch of the dominant kernel for this workload
+    (dram__bytes_read.sum + dram__bytes_write.sum from one `ncu --set full`
+    capture of the current kernel build), from profiles/ncu_traffic.json —
+    {"dram_bytes_per_launch": B, "source": "<profile file>"} or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    return j.get(workload)
+    v = j.get(workload)
+    if v is None:
+        return None
+    return v if isinstance(v, dict) else {"dram_bytes_per_launch": v, "source": None}
 
 
 # ------------------------------------------------------------------- data
 def build_workload(cfg, rank: int, world: int, device: int, sharded: bool = False):
-    """Seeded synthetic data + index on the device. Rank r holds the id-shard
-    [r*n, (r+1)*n) (weak scaling); codebook and coarse quantizer are trained
-    on rank 0 and broadcast so every shard probes identically."""
+    """Seeded synthetic data + index (bench_fixture: plain torch ops, the same
+    bytes in both arms). Rank r holds the id-shard [r*n, (r+1)*n) (weak
+    scaling); the codebook and coarse quantizer come from the same seeded
+    sample of rank 0's rows on every rank, so every shard probes identically.
+    Returns (fixture namespace, queries)."""
     import torch
 
-    from paper_2508_17828_b200 import builder as B
-    from paper_2508_17828_b200.ivf import IvfArrays
+    import bench_fixture as F
 
-    dev = torch.device(f"cuda:{device}")
-    torch.cuda.set_device(dev)
+    torch.cuda.set_device(device)
     t0 = time.time()
-    if cfg.get("data") == "uniform_normalized":  # dataset.hpp:44-56 normalize_rows
-        base = B.synth_uniform(cfg["n"], cfg["dim"], seed=1 + 7919 * rank, device=device)
-        queries = B.synth_uniform(cfg["nq"], cfg["dim"], seed=2, device=device)
-    else:
-        centers = B.synth_normal(cfg["n_centers"], cfg["dim"], seed=0, device=device)
-        base = B.synth_blobs(centers, cfg["n"], cfg["sigma"], seed=1 + 7919 * rank)
-        queries = B.synth_blobs(centers, cfg["nq"], cfg["sigma"], seed=2)
-    p = B.BuildParams(m=cfg["m"], nlist=cfg["nlist"], pq_seed=3, ivf_seed=4)
-    if not sharded:
-        arrays = B.build_ivf(base, p)
-    else:
-        import torch.distributed as dist
-        if rank == 0:
-            sub, cent = B.pq_train(base, p.m, p.ksub, p.pq_iters, p.pq_seed, p.train_sample)
-            n = base.shape[0]
-            sn = min(n, max(p.nlist, 50 * p.nlist))
-            rows = B.sample_rows(n, sn, p.ivf_seed ^ 0x94D049BB133111EB)
-            coarse = B.kmeans(base[torch.from_numpy(rows.astype(np.int64)).to(dev)].contiguous(),
-                              p.nlist, p.coarse_iters, p.ivf_seed)
-            sub_t = torch.from_numpy(sub.astype(np.int32)).to(dev)
-        else:
-            cent = torch.empty(p.ksub * cfg["dim"], dtype=torch.float32, device=dev)
-            coarse = torch.empty((p.nlist, cfg["dim"]), dtype=torch.float32, device=dev)
-            sub_t = torch.empty(p.m, dtype=torch.int32, device=dev)
-        for t in (cent, coarse, sub_t):
-            dist.broadcast(t, 0)
-        sub = sub_t.cpu().numpy().astype(np.uint32)
-        codes, lx = B.pq_encode(base, p.m, p.ksub, sub, cent)
-        a = B.assign(base, coarse)[0] if p.nlist > 1 else torch.zeros(base.shape[0], dtype=torch.int32, device=dev)
-        offs, ids = B.ivf_lists(a, p.nlist)
-        idl = ids.long()
-        arrays = IvfArrays(dim=cfg["dim"], m=p.m, ksub=p.ksub, sub_dims=sub_t, centroids=cent,
-                           coarse=coarse.reshape(-1), list_offsets=offs,
-                           list_ids=(ids + rank * cfg["n"]).to(torch.int32),
-                           list_codes=codes[idl].contiguous(), list_lx=lx[idl].contiguous(),
-                           vectors=base, id_base=rank * cfg["n"])
-    torch.cuda.synchronize()
+    fx = F.build(cfg, rank if sharded else 0, device)
     log(f"[rank {rank}] built {cfg['workload']} shard in {time.time() - t0:.1f}s")
-    return arrays, queries
+    return fx, fx.queries
+
+
+def merged_host_index(parts):
+    """The whole index of W id-shards (host numpy; shard p = ids [p*n, (p+1)*n)):
+    list l = shard 0's list l, then shard 1's, ... (ids stay ascending inside
+    every list, ivf.hpp:147-152)."""
+    W = len(parts)
+    nlist = len(parts[0].list_offsets) - 1
+    sizes = np.stack([np.diff(p.list_offsets.astype(np.int64)) for p in parts])  # [W, nlist]
+    offs = np.zeros(nlist + 1, np.uint64)
+    offs[1:] = np.cumsum(sizes.sum(0))
+    start = offs[:-1].astype(np.int64)[None, :] + np.cumsum(sizes, 0) - sizes  # [W, nlist]
+    total = int(offs[-1])
+    cs = parts[0].list_codes.shape[1]
+    ids = np.empty(total, np.uint32)
+    codes = np.empty((total, cs), np.uint8)
+    lx = np.empty(total, np.float32)
+    for p, s in enumerate(parts):
+        po = s.list_offsets.astype(np.int64)
+        dest = np.repeat(start[p] - po[:-1], sizes[p]) + np.arange(int(po[-1]), dtype=np.int64)
+        ids[dest] = s.list_ids
+        codes[dest] = s.list_codes
+        lx[dest] = s.list_lx
+    from types import SimpleNamespace
+    return SimpleNamespace(dim=parts[0].dim, m=parts[0].m, ksub=parts[0].ksub, sub_dims=parts[0].sub_dims,
+                           centroids=parts[0].centroids, coarse=parts[0].coarse, list_offsets=offs,
+                           list_ids=ids, list_codes=codes, list_lx=lx,
+                           vectors=np.concatenate([p.vectors for p in parts]), id_base=0)
+
+
+def data_gen_note(cfg):
+    if cfg.get("data") == "uniform_normalized":
+        return "torch Philox uniform [0,1) + L2-normalised rows, seeds base=1+7919*rank queries=2 (bench_fixture.py)"
+    return "torch Philox Gaussian blobs, seeds centers=0 base=1+7919*rank queries=2 (bench_fixture.py)"
+
+
+def config_dict(cfg, head, n_gpus, parallelism, fingerprint, **extra):
+    """`config` of the JSON line — built by the same function in both arms."""
+    c = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"], queries=cfg["nq"], batch=cfg["batch"],
+             m=cfg["m"], nlist=cfg["nlist"], nprobe=cfg["nprobe"], k=cfg["k"], gamma=head, n_gpus=n_gpus,
+             parallelism=parallelism,
+             l2=("index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
+                 else "index fits L2; reported as-is"),
+             data_gen=data_gen_note(cfg), fixture=fingerprint)
+    c.update(extra)
+    return c
+
+
+def parallelism_of(world, mode):
+    if mode == "replicas":
+        return f"replicas x{world}"
+    if mode in ("shard", "group") or world > 1:
+        return f"id-shard x{world}"
+    return "single"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------ our GPU arm
 def run_ours(args, cfg):
+    """Modes: `single` (N=1); `shard` / `replicas` (torchrun, one process per
+    GPU, torch.distributed NCCL all-gather + device merge); `group` (one
+    process drives N GPUs through ONE multi-device index behind the C ABI:
+    trim_index_desc devices[0..N) + TRIM_SHARD_ID, the library's NCCL
+    broadcast / filter / all-gather / merge inside every search call)."""
     import torch
 
     from paper_2508_17828_b200 import _lib
     from paper_2508_17828_b200 import ivf as G
 
     import torch.distributed as dist
+    import bench_fixture as F
 
     world, rank, local = dist_env()
-    replicas = world > 1 and args.parallel == "replicas"
-    sharded = (world > 1 and not replicas) or args.force_shard
-    if sharded or replicas:
+    if world > 1:
+        mode = "replicas" if args.parallel == "replicas" else "shard"
+    elif args.gpus > 1 or args.group:
+        mode = "group"
+    else:
+        mode = "shard" if args.force_shard else "single"
+    ngpu = args.gpus if mode == "group" else world
+    if mode in ("shard", "replicas"):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=rank, world_size=world,
                                 device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    arrays, queries = build_workload(cfg, 0 if replicas else rank, 1 if replicas else world, local, sharded)
-    gix = G.GpuIvfIndex(arrays, device=local)
+    sharded = mode == "shard"
+    if mode == "group":
+        if torch.cuda.device_count() < ngpu:
+            raise SystemExit(f"--gpus {ngpu}: only {torch.cuda.device_count()} CUDA devices visible")
+        parts = []
+        for r in range(ngpu):
+            fx_r, q_r = build_workload(cfg, r, ngpu, r, True)
+            if r == 0:
+                fx, queries = fx_r, q_r
+                fprint = F.fingerprint(fx)
+            parts.append(F.to_host(fx_r))
+            if r:
+                del fx_r, q_r
+        torch.cuda.set_device(dev)
+        t0 = time.time()
+        whole = merged_host_index(parts)
+        del parts
+        gix = G.GpuIvfIndex(G.IvfArrays.from_any(whole), devices=list(range(ngpu)),
+                            shard_mode="replicas" if args.parallel == "replicas" else "id_shard")
+        log(f"multi-device index over {ngpu} GPUs in {time.time() - t0:.1f}s ({gix.info()})")
+        arrays = whole
+    else:
+        fx, queries = build_workload(cfg, 0 if mode == "replicas" else rank, world, local, sharded)
+        fprint = F.fingerprint(fx)
+        arrays = G.IvfArrays.from_any(fx)
+        gix = G.GpuIvfIndex(arrays, device=local)
+    replicas = mode == "replicas"
     q_lo, q_hi = 0, cfg["nq"]
     if replicas:  # every rank: the whole index, a contiguous slice of the queries
         from paper_2508_17828_b200.distributed import shard_bounds
@@ -280,6 +351,7 @@ def run_ours(args, cfg):
 
     n_probe_k = C.c_uint32(0)
     _lib.check(lib.trim_probe_launches(gix.handle, cfg["nprobe"], C.byref(n_probe_k)), "probe_launches")
+    setup_k = 1 if cfg["nlist"] > 1 and os.environ.get("TRIM_KNN_SETUP") != "0" else 0
 
     def step(gamma, filt_events=None):
         launches = 0
@@ -290,6 +362,20 @@ def run_ours(args, cfg):
         for i, (b0, nb) in enumerate(batches):
             st_, sh_ = streams[i % len(streams)], shs[i % len(streams)]
             qoff = b0 * cfg["dim"] * 4
+            if mode == "group":
+                # one C-ABI call: broadcast, every device's probe + filter, all-gather, merge
+                if filt_events is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st_)
+                _lib.check(lib.trim_search_knn_device(
+                    gix.handle, p(queries, qoff), nb, k, cfg["nprobe"], float(np.float32(gamma)),
+                    p(ids, b0 * k * 4), p(dists, b0 * k * 4), p(cts, b0 * 48), p(status), sh_), "knn")
+                launches += ngpu * (n_probe_k.value + 1 + setup_k) + 2  # + merge + counters
+                if filt_events is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(st_)
+                    filt_events.append((e0, e1))
+                continue
             _lib.check(lib.trim_probe_device(gix.handle, p(queries, qoff), nb, cfg["nprobe"],
                                              p(lists, b0 * np_eff * 4), sh_), "probe")
             launches += n_probe_k.value
@@ -301,7 +387,7 @@ def run_ours(args, cfg):
                 float(np.float32(gamma)), p(ids, b0 * k * 4), p(dists, b0 * k * 4),
                 p(cts, b0 * 48), p(status), sh_), "knn")
             # the filter kernel, plus trim_knn_setup_kernel (seeds + plan) on IVF indexes
-            launches += 1 + (1 if cfg["nlist"] > 1 and os.environ.get("TRIM_KNN_SETUP") != "0" else 0)
+            launches += 1 + setup_k
             if filt_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(st_)
@@ -381,27 +467,27 @@ def run_ours(args, cfg):
         step(head)
     gix.skipped_positions(reset=True)  # (synchronises; outside the timed region)
     ms, fms, nl, ct, launches = timed(head, args.steps, 0, clk)
-    skipped = gix.skipped_positions() / args.steps  # list-level bound, per step (this rank)
+    skipped = gix.skipped_positions() / args.steps  # list-level bound, per step (this process)
     evaluated, dc = float(ct[3]), float(ct[0])
     total_cand = evaluated * args.steps
     value = total_cand / (ms / 1e3)
     qps = nq * args.steps / (ms / 1e3)
     out = dict(metric=metric_name(cfg),
-               value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
+               value=value, unit="candidates/s", n_gpus=ngpu, steps=args.steps,
                warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
                scaling="strong" if replicas else "weak", vs_baseline=None, dtype="f32 (u8 PQ codes)",
                data="synthetic")
-    out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
-                         queries=nq, batch=B, m=cfg["m"], nlist=cfg["nlist"],
-                         nprobe=cfg["nprobe"], k=k, gamma=head,
-                         parallelism=(f"replicas x{world}" if replicas else f"id-shard x{world}")
-                         if (world > 1 or sharded) else "single",
-                         l2="index > L2 (no flush needed)" if cfg["n"] * cfg["dim"] * 4 > 126e6
-                         else "index fits L2; reported as-is",
-                         data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))
+    out["config"] = config_dict(cfg, head, ngpu, parallelism_of(ngpu, mode if ngpu > 1 or sharded else "single"),
+                                fprint)
+    out["mode"] = {"single": "one process, one GPU", "shard": "torchrun, one process per GPU (id-shard, "
+                   "torch.distributed NCCL all-gather + trim_merge_topk_device)",
+                   "replicas": "torchrun, one process per GPU (replicas, no collective)",
+                   "group": "one process, one multi-device index behind the C ABI (trim_index_desc "
+                            "devices[], TRIM_SHARD_ID: NCCL broadcast + all-gather + device merge in "
+                            "every trim_search_knn_device call)"}[mode]
     out["qps"] = qps
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
-    out["candidates_per_query"] = evaluated / (nq * (world if False else 1))
+    out["candidates_per_query"] = evaluated / nq
     # roofline of the dominant kernel (the fused filter), per launch
     peak, peak_src = measured_peaks()
     m, D = cfg["m"], cfg["dim"]
@@ -418,34 +504,66 @@ def run_ours(args, cfg):
         alg_bytes_step = scanned * (m + 4) + dc * 4
     else:
         alg_bytes_step = scanned * (m + 4) + dc * (4 * D + 4)
-    per_launch_bytes = alg_bytes_step / max(1, nl // args.steps) / (world if world > 1 else 1)
+    gdiv = ngpu if ngpu > 1 else 1
+    per_launch_bytes = alg_bytes_step / max(1, nl // args.steps) / gdiv
     avg_launch_ms = fms / max(1, nl)  # filter-busy time per launch (overlap-aware)
     achieved = per_launch_bytes / (avg_launch_ms / 1e3) / 1e9
     tr = ncu_traffic(cfg["workload"])
     out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
-                           frac=achieved / peak, traffic=tr, kernel="trim_knn_kernel",
+                           frac=achieved / peak, traffic=tr.get("dram_bytes_per_launch") if tr else None,
+                           traffic_source=tr.get("source") if tr else None,
+                           kernel="trim_knn_kernel", scanned_bytes_per_step=alg_bytes_step,
                            bytes_per_candidate=bytes_per_cand, peak_source=peak_src,
                            filter_share_of_step=fms / ms,
                            list_skip_fraction=skipped_all / max(1.0, evaluated),
                            flat_distance_bounds=flat_bounds,
                            stream_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4))
-                           / max(1, nl // args.steps) / (world if world > 1 else 1)
-                           / (avg_launch_ms / 1e3) / 1e9)
+                           / max(1, nl // args.steps) / gdiv / (avg_launch_ms / 1e3) / 1e9)
+    if mode == "group":
+        out["roofline"]["note"] = ("group mode: one interval per C-ABI call (broadcast + every device's probe "
+                                   "and filter + all-gather + merge), per device")
     out["gpu_launches"] = launches
     out["clocks"] = clk.summary()
     out["sweep"] = sweep
     if rank == 0:
-        out[f"recall@{k}"] = recall(gix, queries, ids, k, args.recall_q, world)
-    # e2e through the C-ABI host call with pinned host buffers
-    out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
-    if cfg.get("baseline_kprime") and rank == 0 and world == 1:
+        out[f"recall@{k}"] = recall(gix, queries, ids, k, args.recall_q, world if mode != "group" else ngpu)
+    # e2e: the public API with host buffers, copies inside the timed region
+    if sharded:
+        out["e2e"] = e2e_sharded(gix, queries, cfg, head, args, world, rank, local)
+    else:
+        out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
+    if mode == "single" and not args.no_group_check:
+        # the same workload through the multi-device C-ABI path at one device
+        # (trim_index_desc devices = [0], TRIM_SHARD_ID): what `--gpus N` runs
+        out["multi_device_abi_1gpu"] = group_check(arrays, queries, cfg, head, args)
+    if cfg.get("baseline_kprime") and rank == 0 and world == 1 and mode == "single":
         out["baseline_ivfpq"] = baseline_line(gix, arrays, queries, cfg, args)
     if rank == 0 and world == 1 and not args.skip_cpu:
-        out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
+        out["cpu_baseline"] = cpu_baseline(F.to_host(fx) if mode != "group" else None, queries, cfg, head, args,
+                                           fx=fx)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if sharded:
+    if sharded or replicas:
         dist.destroy_process_group()
+
+
+def group_check(arrays, queries, cfg, gamma, args):
+    """e2e through a one-device TRIM_SHARD_ID index (the multi-device C-ABI
+    path: broadcast, filter, all-gather, merge) on the bench workload."""
+    import torch
+
+    from paper_2508_17828_b200 import ivf as G
+    t0 = time.time()
+    gg = G.GpuIvfIndex(arrays, devices=[0], shard_mode="id_shard")
+    build_s = time.time() - t0
+    try:
+        r = e2e(gg, queries, cfg, gamma, args, 1, 0)
+    finally:
+        gg.close()
+        torch.cuda.empty_cache()
+    r["index"] = "trim_index_desc devices=[0], shard_mode=TRIM_SHARD_ID"
+    r["create_s"] = build_s
+    return r
 
 
 class _Null:
@@ -461,7 +579,7 @@ def recall(gix, queries, ids, k, nsample, world):
     queries, against the exact ground truth computed on the GPU bit-identically
     to core/ground_truth.hpp (trim_ground_truth_knn). Informational; the local
     shard's results at N > 1 are not comparable (None)."""
-    if world > 1 or nsample <= 0:
+    if world > 1 or nsample <= 0 or getattr(gix, "shard_mode", "single") == "id_shard":
         return None
     if gix.n > (16 << 20):  # the exact GT kernel holds nq x n bounds: not at 100M rows
         return None
@@ -474,6 +592,10 @@ def recall(gix, queries, ids, k, nsample, world):
 
 
 def e2e(gix, queries, cfg, gamma, args, world, rank):
+    """The C-ABI host call trim_search_knn (ivf::search_trim_ivf_knn batched)
+    from pinned host queries into pinned host results, `--streams` client
+    threads; H2D, search, D2H all inside the timed region. For a multi-device
+    index that call also broadcasts, all-gathers and merges."""
     import torch
 
     from paper_2508_17828_b200 import ivf as G
@@ -484,7 +606,6 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
     steps = max(1, min(args.steps, 3))
 
     from concurrent.futures import ThreadPoolExecutor
-    pool = ThreadPoolExecutor(max(1, args.streams))  # client threads: one stream each in the C ABI
 
     # results land in pinned host buffers (a serving client's staging memory)
     from paper_2508_17828_b200 import _lib
@@ -502,22 +623,92 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
                    "search_trim_ivf_knn")
         return int(h_ct[b:b + nb, 3].sum())
 
+    with ThreadPoolExecutor(max(1, args.streams)) as pool:  # client threads: one stream each in the C ABI
+        def once():
+            return sum(pool.map(one, range(0, nq, B)))
+
+        once()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cand = 0
+        for _ in range(steps):
+            cand += once()
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+    return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
+                h2d_bytes_per_step=nq * cfg["dim"] * 4,
+                d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
+                api=f"trim_search_knn (C ABI, host buffers; pinned queries and results; {max(1, args.streams)} client threads)")
+
+
+def e2e_sharded(gix, queries, cfg, gamma, args, world, rank, local):
+    """e2e at N ranks, one process per GPU: every batch is copied from pinned
+    host memory, searched on the local shard (trim_search_knn_device), its
+    local top-k all-gathered over NCCL and merged on the device
+    (trim_merge_topk_device), and the merged rows + summed counters copied back
+    to pinned host memory — the exchange is inside the timed region. Wall
+    clock, max over ranks."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_17828_b200 import _lib
+    lib = _lib.load()
+    dev = torch.device(f"cuda:{local}")
+    nq, B, k, D = cfg["nq"], cfg["batch"], cfg["k"], cfg["dim"]
+    hq = queries.cpu().pin_memory()
+    h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    h_ct = torch.empty((nq, 6), dtype=torch.int64).pin_memory()
+    dq = torch.empty((B, D), dtype=torch.float32, device=dev)
+    ids = torch.empty((B, k), dtype=torch.int32, device=dev)
+    dd = torch.empty((B, k), dtype=torch.float32, device=dev)
+    ct = torch.zeros((B, 6), dtype=torch.int64, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    g_ids = torch.empty((world * B, k), dtype=torch.int32, device=dev)
+    g_d = torch.empty((world * B, k), dtype=torch.float32, device=dev)
+    m_ids = torch.empty((B, k), dtype=torch.int32, device=dev)
+    m_d = torch.empty((B, k), dtype=torch.float32, device=dev)
+    sh = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    steps = max(1, min(args.steps, 3))
+
     def once():
-        return sum(pool.map(one, range(0, nq, B)))
+        cand = 0
+        for b in range(0, nq, B):
+            nb = min(B, nq - b)
+            dq[:nb].copy_(hq[b:b + nb], non_blocking=True)
+            _lib.check(lib.trim_search_knn_device(gix.handle, P(dq), nb, k, cfg["nprobe"], float(np.float32(gamma)),
+                                                  P(ids), P(dd), P(ct), P(st), sh), "knn")
+            dist.all_gather_into_tensor(g_ids[:world * nb], ids[:nb])
+            dist.all_gather_into_tensor(g_d[:world * nb], dd[:nb])
+            _lib.check(lib.trim_merge_topk_device(P(g_d), P(g_ids), world, nb, k, P(m_d), P(m_ids), local, sh),
+                       "merge")
+            dist.all_reduce(ct[:nb])
+            h_ids[b:b + nb].copy_(m_ids[:nb], non_blocking=True)
+            h_d[b:b + nb].copy_(m_d[:nb], non_blocking=True)
+            h_ct[b:b + nb].copy_(ct[:nb], non_blocking=True)
+        torch.cuda.synchronize()
+        return int(h_ct[:, 3].sum())
 
     once()
+    dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     cand = 0
     for _ in range(steps):
         cand += once()
-    torch.cuda.synchronize()
     sec = time.perf_counter() - t0
+    t = torch.tensor([sec], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
     return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
-                h2d_bytes_per_step=nq * cfg["dim"] * 4,
-                d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
-                api=f"trim_search_knn (C ABI, host buffers; pinned queries and results; {max(1, args.streams)} client threads)",
-                shard_local=world > 1)
+                h2d_bytes_per_step=nq * D * 4, d2h_bytes_per_step=nq * k * 8 + nq * 48,
+                api="per batch: pinned H2D, trim_search_knn_device on the local shard, NCCL all-gather "
+                    "(torch.distributed), trim_merge_topk_device, counters all-reduce, pinned D2H; "
+                    "wall clock, max over ranks",
+                includes_exchange=True)
 
 
 def baseline_line(gix, arrays, queries, cfg, args):
@@ -547,10 +738,8 @@ def baseline_line(gix, arrays, queries, cfg, args):
                 api="trim_search_baseline_ivfpq (C ABI, host buffers)")
 
 
-def _host_index(arrays):
+def _host_index(h):
     from oracle.oracle import HostIndex
-    from paper_2508_17828_b200.builder import to_host
-    h = to_host(arrays)
     return HostIndex(dim=h.dim, m=h.m, ksub=h.ksub, sub_dims=h.sub_dims, centroids=h.centroids,
                      coarse=h.coarse, list_offsets=h.list_offsets, list_ids=h.list_ids,
                      list_codes=h.list_codes, list_lx=h.list_lx, vectors=h.vectors)
@@ -576,17 +765,30 @@ class RefTimer:
             self.co = O.COracle()
             self.hix = hix
 
-    def run(self, qsub):
-        """-> (seconds, evaluated, dc, pruned) for one parallel batch."""
-        rng = self.cfg.get("kind") == "range"
+    def set_threads(self, t):
+        self.threads = t
         if self.kind == "reference":
-            sec, ct = self.ref.session_run(self.sess, 1 if rng else 0, qsub, self.cfg["k"], self.cfg["nprobe"],
-                                           self.gamma, arg=self.cfg.get("radius", 0.0))
+            self.ref.set_threads(t)
+
+    def run(self, qsub, kind=None, arg=None):
+        """-> (seconds, evaluated, dc, pruned) for one parallel batch. kind:
+        0 kNN (default; 1 for range configs), 2 = search_baseline_ivfpq (arg = k')."""
+        rng = self.cfg.get("kind") == "range"
+        if kind is None:
+            kind = 1 if rng else 0
+        if arg is None:
+            arg = self.cfg.get("radius", 0.0)
+        if self.kind == "reference":
+            sec, ct = self.ref.session_run(self.sess, kind, qsub, self.cfg["k"], self.cfg["nprobe"],
+                                           self.gamma, arg=arg)
             return sec, int(ct[3]), int(ct[0]), int(ct[2])
         t0 = time.perf_counter()
-        if rng:
+        if kind == 1:
             _, _, _, ct, _ = self.co.search_range(self.hix, qsub, self.cfg["radius"], self.cfg["nprobe"],
                                                   self.gamma, threads=self.threads)
+        elif kind == 2:
+            _, _, ct = self.co.search_baseline(self.hix, qsub, self.cfg["k"], self.cfg["nprobe"], int(arg),
+                                               threads=self.threads)[:3]
         else:
             _, _, ct, _ = self.co.search_knn(self.hix, qsub, self.cfg["k"], self.cfg["nprobe"], self.gamma,
                                              threads=self.threads)
@@ -596,42 +798,70 @@ class RefTimer:
         if self.kind == "reference":
             self.ref.session_destroy(self.sess)
 
-    def calibrate(self, qs):
-        n0 = min(len(qs), max(4 * self.threads, 64))
-        sec, *_ = self.run(qs[:n0])
+    def calibrate(self, qs, kind=None, arg=None):
+        n0 = min(len(qs), max(4 * self.threads, 64 if self.threads > 1 else 8))
+        sec, *_ = self.run(qs[:n0], kind, arg)
         return n0 / max(sec, 1e-9)  # queries/s
 
+    def bounded(self, qs, seconds, kind=None, arg=None):
+        """A sample sized to ~`seconds` of CPU work -> dict(value, qps, n, sec, prune_ratio)."""
+        qps = self.calibrate(qs, kind, arg)
+        n = int(min(len(qs), max(4 * self.threads, seconds * qps)))
+        sec, ev, dc, pr = self.run(qs[:n], kind, arg)
+        return dict(value=ev / sec, qps=n / sec, n=n, sec=sec, prune_ratio=pr / max(1, pr + dc))
 
-def cpu_baseline(arrays, queries, cfg, gamma, args):
+
+def cpu_baseline(hfx, queries, cfg, gamma, args, fx=None):
+    """The reference's CPU path on this box's host cores, on bounded samples of
+    the same workload: all hardware threads (the reported `value`), one thread
+    (the paper's protocol), and for config 2 the IVFPQ baseline
+    search_baseline_ivfpq at k' = 1000 (ivf.hpp:193-237)."""
+    import bench_fixture as F
     t0 = time.time()
-    hix = _host_index(arrays)
+    if hfx is None:
+        hfx = F.to_host(fx)
+    hix = _host_index(hfx)
     qs = queries.cpu().numpy()
     log(f"host copy for the CPU baseline: {time.time() - t0:.1f}s")
     threads = os.cpu_count() or 1
     rt = RefTimer(hix, cfg, gamma, threads)
-    qps = rt.calibrate(qs)
-    n = int(min(len(qs), max(4 * threads, args.cpu_seconds * qps)))
-    sec, ev, dc, pr = rt.run(qs[:n])
-    rt.close()
-    return dict(value=ev / sec, unit="candidates/s", cores=threads, kind=rt.kind,
-                sample=f"first {n} of {len(qs)} queries of {cfg['workload']} at gamma={gamma}, "
-                       f"{threads} threads, {sec:.1f}s",
-                qps=n / sec, prune_ratio=pr / max(1, pr + dc))
+    try:
+        r = rt.bounded(qs, args.cpu_seconds)
+        out = dict(value=r["value"], unit="candidates/s", cores=threads, kind=rt.kind,
+                   sample=f"first {r['n']} of {len(qs)} queries of {cfg['workload']} at gamma={gamma}, "
+                          f"{threads} threads, {r['sec']:.1f}s",
+                   qps=r["qps"], prune_ratio=r["prune_ratio"], cpu_model=cpu_model(),
+                   timing="steady_clock around parallel_for over queries (sweep.hpp:121-152)")
+        rt.set_threads(1)
+        r1 = rt.bounded(qs, max(2.0, args.cpu_seconds / 3))
+        out["single_thread"] = dict(value=r1["value"], unit="candidates/s", qps=r1["qps"], cores=1,
+                                    sample=f"first {r1['n']} queries, 1 thread, {r1['sec']:.1f}s")
+        if cfg.get("baseline_kprime"):
+            rt.set_threads(threads)
+            rb = rt.bounded(qs, max(2.0, args.cpu_seconds / 3), kind=2, arg=float(cfg["baseline_kprime"]))
+            out["baseline_ivfpq"] = dict(k_prime=cfg["baseline_kprime"], qps=rb["qps"], cand_per_s=rb["value"],
+                                         cores=threads, sample=f"first {rb['n']} queries, {threads} threads, "
+                                                               f"{rb['sec']:.1f}s")
+    finally:
+        rt.close()
+    return out
 
 
 # ------------------------------------------------------ config 3: range
-def calibrate_radius(arrays, queries, cfg):
+def calibrate_radius(vectors, queries, cfg):
     """bench::pick_radius_for_fraction (bench/radius.hpp:20-55): the
     e_fraction = result_size/N quantile (EmpiricalCdf: linear between order
     statistics) of pooled query-to-row distances over 20,000 sampled rows x 200
-    sampled queries (the reference's Fisher-Yates sampler, seeds 1 and 2).
-    Distances by torch.cdist (a workload parameter, not a parity value)."""
+    sampled queries (seeded torch.randperm samples, seeds 1 and 2).
+    Distances by torch.cdist in float64 (a workload parameter, not a parity value)."""
     import torch
 
-    from paper_2508_17828_b200 import builder as B
-    x = arrays.vectors
-    rows = torch.from_numpy(B.sample_rows(x.shape[0], min(20000, x.shape[0]), 1).astype(np.int64)).to(x.device)
-    qi = torch.from_numpy(B.sample_rows(queries.shape[0], min(200, queries.shape[0]), 2).astype(np.int64)).to(x.device)
+    x = vectors
+    g = torch.Generator(device=x.device)
+    g.manual_seed(1)
+    rows = torch.randperm(x.shape[0], generator=g, device=x.device)[:min(20000, x.shape[0])]
+    g.manual_seed(2)
+    qi = torch.randperm(queries.shape[0], generator=g, device=x.device)[:min(200, queries.shape[0])]
     d = torch.cdist(queries[qi].double(), x[rows].double()).reshape(-1)
     d, _ = torch.sort(d)
     p = cfg["result_size"] / x.shape[0]
@@ -650,13 +880,16 @@ def run_ours_range(args, cfg):
     from paper_2508_17828_b200 import _lib
     from paper_2508_17828_b200 import ivf as G
 
+    import bench_fixture as F
+
     world, rank, local = dist_env()
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
-    arrays, queries = build_workload(cfg, rank, world, local, False)
-    gix = G.GpuIvfIndex(arrays, device=local)
+    fx, queries = build_workload(cfg, rank, world, local, False)
+    fprint = F.fingerprint(fx)
+    gix = G.GpuIvfIndex(G.IvfArrays.from_any(fx), device=local)
     lib = _lib.load()
-    radius = calibrate_radius(arrays, queries, cfg)
+    radius = calibrate_radius(fx.vectors, queries, cfg)
     cfg["radius"] = radius
     nq, B, cap = cfg["nq"], cfg["batch"], 4096
     d_rad = torch.full((nq,), radius, dtype=torch.float32, device=dev)
@@ -758,11 +991,8 @@ def run_ours_range(args, cfg):
                value=value, unit="candidates/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
                ms_per_step=ms / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
                dtype="f32 (u8 PQ codes)", data="synthetic")
-    out["config"] = dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"], queries=nq, batch=B,
-                         m=cfg["m"], nlist=1, gamma=head, radius=radius,
-                         radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)",
-                         parallelism="single", l2="index > L2 (no flush needed)",
-                         data_gen=("device Philox uniform [0,1) + L2-normalised rows, seeds base=1 queries=2" if cfg.get("data") == "uniform_normalized" else "device Philox blobs, seeds centers=0 base=1 queries=2"))
+    out["config"] = config_dict(cfg, head, world, parallelism_of(world, "single"), fprint, radius=radius,
+                                radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)")
     out["qps"] = nq * args.steps / (ms / 1e3)
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
     out["mean_result_size"] = float(counts.double().mean())
@@ -776,7 +1006,8 @@ def run_ours_range(args, cfg):
         alg = (nq + qt - 1) // qt * cfg["n"] * (m + 4) + dc * (4 * D + 4)
     achieved = alg / (busy / args.steps / 1e3) / 1e9
     out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                           traffic=ncu_traffic(cfg["workload"]),
+                           traffic=(ncu_traffic(cfg["workload"]) or {}).get("dram_bytes_per_launch"),
+                           traffic_source=(ncu_traffic(cfg["workload"]) or {}).get("source"),
                            kernel="trim_range_kernel (block partition)" if skipped > 0 else "trim_range_flat_kernel",
                            bytes_per_step=alg, query_tile=qt, peak_source=peak_src,
                            block_skip_fraction=skipped / max(1.0, evaluated),
@@ -810,7 +1041,7 @@ def run_ours_range(args, cfg):
                       d2h_bytes_per_step=nres * 8 + (nq + 1) * 8 + nq * 48,
                       api=f"trim_search_range (C ABI, host buffers; {max(1, args.streams)} client threads)")
     if rank == 0 and not args.skip_cpu:
-        out["cpu_baseline"] = cpu_baseline(arrays, queries, cfg, head, args)
+        out["cpu_baseline"] = cpu_baseline(None, queries, cfg, head, args, fx=fx)
     print(json.dumps(out), flush=True)
 
 
@@ -989,7 +1220,8 @@ def run_ours_graph(args, cfg):
                prune_ratio=float(ct[2] / max(1, ct[2] + ct[0])), hops_per_query=float(ct[4]) / nq,
                candidates_per_query=evaluated / nq)
     out["roofline"] = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                           traffic=ncu_traffic(cfg["workload"]), kernel="trim_graph_kernel",
+                           traffic=(ncu_traffic(cfg["workload"]) or {}).get("dram_bytes_per_launch"),
+                           kernel="trim_graph_kernel",
                            bytes_per_candidate=bpc, peak_source=peak_src, filter_share_of_step=busy / ms,
                            note="one warp per query walks the graph: latency-bound (dependent hops), not "
                                 "bandwidth-bound")
@@ -1071,48 +1303,63 @@ def run_reference_graph(args, cfg):
 
 # ------------------------------------------------------ reference CPU arm
 def run_reference(args, cfg):
+    """The reference arm: the unmodified reference (oracle/_ref, its own
+    ivf::search_trim_ivf_knn / search_trim_ivf_range, parallel_for over queries
+    like run_queries) on this box's host cores, on the same workload bytes as
+    our arm (bench_fixture: plain torch; this process never loads
+    libtrim_b200.so). Rank 0 only under torchrun."""
     world, rank, local = dist_env()
     if rank != 0:
         return
     import torch
+
+    import bench_fixture as F
     torch.cuda.set_device(local)
-    arrays, queries = build_workload(cfg, 0, 1, local)
-    hix = _host_index(arrays)
-    qs = queries.cpu().numpy()
-    arrays_r = arrays
-    threads = os.cpu_count() or 1
+    fx, queries = build_workload(cfg, 0, 1, local, False)
+    fprint = F.fingerprint(fx)
+    ngpu = world if world > 1 else args.gpus
     head = args.gamma if args.gamma else cfg["gamma"]
+    extra = {}
     if cfg.get("kind") == "range":
-        import torch as _t
-        cfg["radius"] = calibrate_radius(arrays_r, queries, cfg)
+        cfg["radius"] = calibrate_radius(fx.vectors, queries, cfg)
+        extra = dict(radius=cfg["radius"], radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)")
+    mode = "single" if ngpu == 1 else ("replicas" if args.parallel == "replicas" else "shard")
+    if cfg.get("kind") == "range":
+        mode = "single"
+    conf = config_dict(cfg, head, ngpu, parallelism_of(ngpu, mode), fprint, **extra)
+    hix = _host_index(F.to_host(fx))
+    qs = queries.cpu().numpy()
+    del fx, queries
+    torch.cuda.empty_cache()
+    threads = os.cpu_count() or 1
     rt = RefTimer(hix, cfg, head, threads)
     qps = rt.calibrate(qs)
     per_step_s = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
     nstep = int(min(len(qs), max(4 * threads, per_step_s * qps)))
-    secs, evs = 0.0, 0
+    secs, evs, dcs, prs = 0.0, 0, 0, 0
     for i in range(args.warmup + args.steps):
         start = (i * nstep) % len(qs)
         sub = qs[start:start + nstep]
         if len(sub) < nstep:
             sub = np.concatenate([sub, qs[:nstep - len(sub)]])
-        sec, ev, _, _ = rt.run(sub)
+        sec, ev, dc, pr = rt.run(sub)
         if i >= args.warmup:
             secs += sec
             evs += ev
+            dcs += dc
+            prs += pr
     rt.close()
     value = evs / secs
     out = dict(metric=metric_name(cfg),
-               value=value, unit="candidates/s", n_gpus=world, steps=args.steps,
+               value=value, unit="candidates/s", n_gpus=ngpu, steps=args.steps,
                warmup=args.warmup, ms_per_step=secs * 1e3 / args.steps, higher_is_better=True,
-               scaling="weak", vs_baseline=None, dtype="f32 (u8 PQ codes)", data="synthetic",
-               impl="reference",
-               config=dict(workload=cfg["workload"], n_per_gpu=cfg["n"], dim=cfg["dim"],
-                           queries=cfg["nq"], m=cfg["m"], nlist=cfg["nlist"],
-                           nprobe=cfg["nprobe"], k=cfg["k"], gamma=head),
-               qps=nstep * args.steps / secs,
+               scaling="strong" if mode == "replicas" else "weak", vs_baseline=None, dtype="f32 (u8 PQ codes)",
+               data="synthetic", impl="reference", config=conf,
+               qps=nstep * args.steps / secs, prune_ratio=prs / max(1, prs + dcs),
                cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind=rt.kind,
                                  sample=f"{nstep} queries per step (of {len(qs)}) of {cfg['workload']}, "
-                                        f"{threads} threads"),
+                                        f"{threads} threads" + (" (rank 0's shard)" if ngpu > 1 else ""),
+                                 cpu_model=cpu_model()),
                e2e=dict(value=value, unit="candidates/s", h2d_bytes_per_step=0,
                         d2h_bytes_per_step=0))
     print(json.dumps(out), flush=True)
@@ -1138,7 +1385,16 @@ def main():
                          "(whole index per GPU, queries partitioned, strong scaling, no collective)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the id-sharded path (all-gather + device merge) even at N=1")
+    ap.add_argument("--group", action="store_true",
+                    help="one process drives --gpus devices through one multi-device C-ABI index "
+                         "(the default when --gpus N > 1 without torchrun)")
+    ap.add_argument("--no-group-check", action="store_true",
+                    help="skip the N=1 e2e line through the one-device TRIM_SHARD_ID index")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (torchrun --nproc-per-node must "
+                         f"equal --gpus)")
     cfg = dict(CONFIGS[args.config])
     if args.n:
         cfg["n"] = args.n

@@ -66,55 +66,75 @@ __host__ __device__ inline size_t lut_bytes(int /*M_template*/, uint32_t m) { re
 
 // pq::build_distance_table (pq.hpp:158-172) into the blocked layout. Entry
 // values are the reference's euclidean_sq, bit for bit.
-// Entry (j, c) = euclidean_sq of a 2- or 4-wide subspace, the reference's
+// Entry (j, c) = euclidean_sq of a 2-, 4- or 8-wide subspace, the reference's
 // four-accumulator order collapsed: acc_i = 0 + d_i^2 exactly, unused
-// accumulators are +0.0f.
+// accumulators are +0.0f; at 8, acc_i = d_i^2 + d_{i+4}^2.
 template <uint32_t SD>
 __device__ __forceinline__ float sub_dist(const float* q, const float* c) {
     if (SD == 2) {
         const float2 v = __ldg(reinterpret_cast<const float2*>(c));
         const float d0 = __fsub_rn(q[0], v.x), d1 = __fsub_rn(q[1], v.y);
         return __fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1));
-    } else {
+    } else if (SD == 4) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(c));
         const float d0 = __fsub_rn(q[0], v.x), d1 = __fsub_rn(q[1], v.y);
         const float d2 = __fsub_rn(q[2], v.z), d3 = __fsub_rn(q[3], v.w);
         return __fadd_rn(__fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1)),
                          __fadd_rn(__fmul_rn(d2, d2), __fmul_rn(d3, d3)));
+    } else {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(c));
+        const float4 w = __ldg(reinterpret_cast<const float4*>(c) + 1);
+        const float d0 = __fsub_rn(q[0], v.x), d1 = __fsub_rn(q[1], v.y);
+        const float d2 = __fsub_rn(q[2], v.z), d3 = __fsub_rn(q[3], v.w);
+        const float e0 = __fsub_rn(q[4], w.x), e1 = __fsub_rn(q[5], w.y);
+        const float e2 = __fsub_rn(q[6], w.z), e3 = __fsub_rn(q[7], w.w);
+        const float a0 = __fadd_rn(__fmul_rn(d0, d0), __fmul_rn(e0, e0));
+        const float a1 = __fadd_rn(__fmul_rn(d1, d1), __fmul_rn(e1, e1));
+        const float a2 = __fadd_rn(__fmul_rn(d2, d2), __fmul_rn(e2, e2));
+        const float a3 = __fadd_rn(__fmul_rn(d3, d3), __fmul_rn(e3, e3));
+        return __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
     }
 }
 
-// Uniform 2- or 4-wide subspaces: entries are independent, so each thread
-// keeps 8 centroid loads in flight (the generic loop below is latency-bound).
+// Store entry (j, c) of the blocked table (bank = column j & 31).
+__device__ __forceinline__ void lut_store(float* lut, const LutShape& sh, uint32_t j, uint32_t c, float v) {
+    const uint32_t b = j >> 5, t = j & 31u;
+    if (b < sh.nfull) {
+        lut[b * (kFullBytes / 4) + c * 32 + t] = v;
+    } else {
+        float* hblk = lut + sh.nfull * (kFullBytes / 4);
+        const uint32_t hrow = sh.half_row_bytes() / 4;
+        hblk[c * hrow + t] = v;
+        if (sh.hdup)
+            hblk[c * hrow + t + 16] = v;
+    }
+}
+
+// Uniform 2-, 4- or 8-wide subspaces. Entry i -> (c = i / m, j = i % m):
+// consecutive threads take consecutive subspaces of one code, so a warp reads
+// one contiguous run of the code-major centroid copy (ix.centroids_t, 32*SD
+// floats) and writes 32 distinct banks of one table row (the j-major order,
+// c fastest, put all 32 lanes of a store in one bank). 8 entries in flight
+// per thread.
 template <uint32_t SD>
 __device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const float* q_smem, float* lut,
                                                   const LutShape& sh, uint32_t t0, uint32_t nt) {
-    const uint32_t hrow = sh.half_row_bytes() / 4;
-    float* hblk = lut + sh.nfull * (kFullBytes / 4);
-    const uint32_t total = ix.m * ix.ksub;
+    const uint32_t m = ix.m, total = m * ix.ksub;
     for (uint32_t i0 = t0; i0 < total; i0 += 8 * nt) {
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t i = i0 + u * nt;
-            const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
-            v[u] = i < total ? sub_dist<SD>(q_smem + j * SD, ix.centroids + (static_cast<size_t>(ix.ksub) * j + c) * SD)
-                             : 0.0f;
+            const uint32_t c = i / m, j = i - c * m;
+            v[u] = i < total ? sub_dist<SD>(q_smem + j * SD, ix.centroids_t + static_cast<size_t>(i) * SD) : 0.0f;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t i = i0 + u * nt;
             if (i >= total)
                 break;
-            const uint32_t j = i / ix.ksub, c = i - j * ix.ksub;
-            const uint32_t b = j >> 5, t = j & 31u;
-            if (b < sh.nfull) {
-                lut[b * (kFullBytes / 4) + c * 32 + t] = v[u];
-            } else {
-                hblk[c * hrow + t] = v[u];
-                if (sh.hdup)
-                    hblk[c * hrow + t + 16] = v[u];
-            }
+            const uint32_t c = i / m, j = i - c * m;
+            lut_store(lut, sh, j, c, v[u]);
         }
     }
 }
@@ -129,23 +149,16 @@ __device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const floa
         build_lut_uniform<2>(ix, q_smem, lut, sh, t0, nt);
     else if (ix.sd_uniform == 4)
         build_lut_uniform<4>(ix, q_smem, lut, sh, t0, nt);
-    else
-    for (uint32_t j = 0; j < ix.m; ++j) {
-        const uint32_t sd = ix.sub_dims[j];
-        const uint32_t off = ix.sub_offsets[j];
-        const float* cb = ix.centroids + static_cast<size_t>(ix.ksub) * off;
-        const uint32_t b = j >> 5, t = j & 31u;
-        for (uint32_t c = t0; c < ix.ksub; c += nt) {
-            const float v = euclid_sq_generic(q_smem + off, cb + c * sd, sd);
-            if (b < sh.nfull) {
-                lut[b * (kFullBytes / 4) + c * 32 + t] = v;
-            } else {
-                hblk[c * hrow + t] = v;
-                if (sh.hdup)
-                    hblk[c * hrow + t + 16] = v;
-            }
+    else if (ix.sd_uniform == 8)
+        build_lut_uniform<8>(ix, q_smem, lut, sh, t0, nt);
+    else // mixed widths: the same code-major order, widths and offsets per subspace
+        for (uint32_t i = t0; i < ix.m * ix.ksub; i += nt) {
+            const uint32_t c = i / ix.m, j = i - c * ix.m;
+            const uint32_t off = __ldg(ix.sub_offsets + j);
+            lut_store(lut, sh, j, c,
+                      euclid_sq_generic(q_smem + off, ix.centroids_t + static_cast<size_t>(c) * ix.dim + off,
+                                        __ldg(ix.sub_dims + j)));
         }
-    }
     // zero every non-live column of the last block: both schedules read all
     // columns, and +0.0f leaves the sum unchanged
     const uint32_t rem = ix.m & 31u;

@@ -335,6 +335,21 @@ bool ensure_flat_partition(trim_index* ix) {
 
 // Query-tile size of the flat range kernel: as many LUTs as fit while two
 // CTAs stay resident per SM (1 = no tiling).
+// Code-major copy of the codebook (code c's sub-centroid j at c*dim +
+// sub_off[j]): the read order of build_lut_blocked, one contiguous run per
+// warp. `cent` is the device copy in the descriptor layout.
+float* centroids_code_major(float* out, const float* cent, uint32_t ksub, uint32_t dim,
+                            const std::vector<uint32_t>& sub, const std::vector<uint32_t>& off) {
+    std::vector<float> h(static_cast<size_t>(ksub) * dim), t(h.size());
+    CK(cudaMemcpy(h.data(), cent, sizeof(float) * h.size(), cudaMemcpyDeviceToHost));
+    for (size_t j = 0; j < sub.size(); ++j)
+        for (uint32_t c = 0; c < ksub; ++c)
+            for (uint32_t e = 0; e < sub[j]; ++e)
+                t[static_cast<size_t>(c) * dim + off[j] + e] = h[static_cast<size_t>(ksub) * off[j] + c * sub[j] + e];
+    CK(cudaMemcpy(out, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
+    return out;
+}
+
 uint32_t range_flat_qt(const DevIndex& v) {
     if (v.nlist != 1 || !probe_mma_enabled_range())
         return 1;
@@ -968,6 +983,8 @@ int trimhost::create_single(const trim_index_desc* d, trim_index** out) {
             float* cent = ix->alloc<float>(static_cast<size_t>(d->ksub) * d->dim);
             CK(cudaMemcpy(cent, d->centroids, sizeof(float) * d->ksub * d->dim, kind));
             v.centroids = cent;
+            v.centroids_t = centroids_code_major(ix->alloc<float>(static_cast<size_t>(d->ksub) * d->dim), cent,
+                                                 d->ksub, d->dim, sub, suboff);
             float* coarse = ix->alloc<float>(static_cast<size_t>(d->nlist) * v.dim_stride);
             CK(cudaMemset(coarse, 0, sizeof(float) * d->nlist * v.dim_stride));
             CK(cudaMemcpy2D(coarse, sizeof(float) * v.dim_stride, d->coarse, sizeof(float) * d->dim,
@@ -1631,6 +1648,8 @@ int trim_graph_create(const trim_graph_desc* d, trim_graph_t* out) {
             float* cent = gr->alloc<float>(static_cast<size_t>(d->ksub) * d->dim);
             CK(cudaMemcpy(cent, d->centroids, sizeof(float) * d->ksub * d->dim, kind));
             v.centroids = cent;
+            v.centroids_t = centroids_code_major(gr->alloc<float>(static_cast<size_t>(d->ksub) * d->dim), cent,
+                                                 d->ksub, d->dim, sub, suboff);
             uint8_t* codes = gr->alloc<uint8_t>(n * v.code_stride);
             CK(cudaMemset(codes, 0, n * v.code_stride));
             CK(cudaMemcpy2D(codes, v.code_stride, d->codes, d->code_stride, d->m, n, kind));

@@ -28,6 +28,7 @@ struct DevIndex {
     const uint32_t* sub_dims;    // m
     const uint32_t* sub_offsets; // m
     const float* centroids;      // ksub*dim; subspace j at ksub*sub_offsets[j]
+    const float* centroids_t;    // ksub*dim code-major: code c's sub-centroid j at c*dim + sub_offsets[j]
     const float* coarse;         // nlist*dim_stride
     const uint64_t* list_offsets;
     const uint32_t* list_ids;

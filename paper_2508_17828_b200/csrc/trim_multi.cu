@@ -113,6 +113,12 @@ bool nccl_wanted() {
 
 struct NcclGroup {
     std::vector<ncclComm_t> comms; // one per part, rank p = part p
+    // Every collective is enqueued on all W communicators inside one
+    // ncclGroupStart/End; concurrent host calls on the index take this lock
+    // around each such group, so every communicator sees the same sequence of
+    // collectives (two threads interleaving per-communicator enqueues could
+    // order them differently on two devices and deadlock).
+    std::mutex mu;
     ~NcclGroup() {
         for (ncclComm_t c : comms)
             if (c)
@@ -501,6 +507,7 @@ int trimhost::group_search_knn_device(trim_index* ix, const float* d_queries, ui
     }
     // 1. the query batch to every part: NCCL broadcast from the home rank, or copies
     if (ix->nccl) {
+        std::lock_guard<std::mutex> lk(ix->nccl->mu);
         NK(nccl().group_start());
         for (uint32_t p = 0; p < W; ++p)
             NK(nccl().broadcast(p == 0 ? q : nullptr, bq[p].p, nq * ds, ncclFloat32, 0, ix->nccl->comms[p], sts[p]));
@@ -520,6 +527,7 @@ int trimhost::group_search_knn_device(trim_index* ix, const float* d_queries, ui
     }
     // 3. the exchange: all-gather of the per-part top-k and counters
     if (ix->nccl) {
+        std::lock_guard<std::mutex> lk(ix->nccl->mu);
         NK(nccl().group_start());
         for (uint32_t p = 0; p < W; ++p) {
             NK(nccl().all_gather(bi[p].p, gi[p].p, nres, ncclUint32, ix->nccl->comms[p], sts[p]));
@@ -753,6 +761,7 @@ int trimhost::group_search_range(trim_index* ix, const float* queries, uint64_t 
         gc[p] = DevBuf(sizeof(unsigned int) * nq * W, sts[p]);
     }
     if (ix->nccl) {
+        std::lock_guard<std::mutex> lk(ix->nccl->mu);
         NK(nccl().group_start());
         for (uint32_t p = 0; p < W; ++p) {
             NK(nccl().all_gather(bk[p].p, gk[p].p, per, ncclUint64, ix->nccl->comms[p], sts[p]));

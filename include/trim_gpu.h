@@ -156,7 +156,8 @@ int trim_probe_launches(trim_index_t index, uint32_t nprobe, uint32_t* launches)
  * (dist_sq, id). counters_out: nq (host, may be NULL).
  * gamma is float(profile.gamma) (ivf.hpp:250); gamma < 0 is an uncalibrated
  * profile (ivf.hpp:246-247). k > probed vectors of any query -> TRIM_EINVAL
- * (ivf.hpp:289-290). k <= 256.
+ * (ivf.hpp:289-290). k <= 4096 (k > 256: a shared-memory top-k in the
+ * runtime-(m, ksub) kernel).
  */
 int trim_search_knn(trim_index_t index, const float* queries, uint64_t nq, uint32_t k,
                     uint32_t nprobe, float gamma, uint32_t* ids_out, float* dist_out,

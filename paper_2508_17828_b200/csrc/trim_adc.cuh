@@ -116,10 +116,10 @@ __device__ __forceinline__ void lut_store(float* lut, const LutShape& sh, uint32
 // floats) and writes 32 distinct banks of one table row (the j-major order,
 // c fastest, put all 32 lanes of a store in one bank). 8 entries in flight
 // per thread.
-template <uint32_t SD>
+template <uint32_t SD, int M>
 __device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const float* q_smem, float* lut,
                                                   const LutShape& sh, uint32_t t0, uint32_t nt) {
-    const uint32_t m = ix.m, total = m * ix.ksub;
+    const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m, total = m * ix.ksub; // M: constant divisor
     for (uint32_t i0 = t0; i0 < total; i0 += 8 * nt) {
         float v[8];
 #pragma unroll
@@ -140,17 +140,19 @@ __device__ __forceinline__ void build_lut_uniform(const DevIndex& ix, const floa
 }
 
 // Threads t0 (of nt participating) build the table; defaults: the whole CTA.
+// M > 0: the kernel's compile-time code length (= ix.m).
+template <int M = 0>
 __device__ __forceinline__ void build_lut_blocked(const DevIndex& ix, const float* q_smem, float* lut,
                                                   uint32_t t0 = threadIdx.x, uint32_t nt = blockDim.x) {
     const LutShape sh = LutShape::of(ix.m);
     const uint32_t hrow = sh.half_row_bytes() / 4;          // floats per HALF row
     float* hblk = lut + sh.nfull * (kFullBytes / 4);
     if (ix.sd_uniform == 2)
-        build_lut_uniform<2>(ix, q_smem, lut, sh, t0, nt);
+        build_lut_uniform<2, M>(ix, q_smem, lut, sh, t0, nt);
     else if (ix.sd_uniform == 4)
-        build_lut_uniform<4>(ix, q_smem, lut, sh, t0, nt);
+        build_lut_uniform<4, M>(ix, q_smem, lut, sh, t0, nt);
     else if (ix.sd_uniform == 8)
-        build_lut_uniform<8>(ix, q_smem, lut, sh, t0, nt);
+        build_lut_uniform<8, M>(ix, q_smem, lut, sh, t0, nt);
     else // mixed widths: the same code-major order, widths and offsets per subspace
         for (uint32_t i = t0; i < ix.m * ix.ksub; i += nt) {
             const uint32_t c = i / ix.m, j = i - c * ix.m;

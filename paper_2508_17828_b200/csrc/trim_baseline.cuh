@@ -49,7 +49,7 @@ trim_bl_est_kernel(DevIndex ix, BlParams p) {
     if (begin >= total)
         return;
     const uint32_t end = min(total, begin + p.slice);
-    build_lut_blocked(ix, qv, lut);
+    build_lut_blocked<M>(ix, qv, lut);
     __syncthreads();
     uint32_t lo = 0, hi = p.np;
     while (lo + 1 < hi) {

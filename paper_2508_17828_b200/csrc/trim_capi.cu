@@ -61,6 +61,10 @@ int check_device_present() {
     } while (0)
 
 void launch_knn(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
+    if (p.k > 256) { // the shared-memory top-k is instantiated in the runtime-(m, ksub) kernel only
+        CK(launch_knn_0(ix, p, smem, st));
+        return;
+    }
     TRIM_DISPATCH(launch_knn_, ix, p, smem, st);
 }
 
@@ -461,9 +465,9 @@ int validate_knn(uint32_t k, float gamma) {
         return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k must be positive");
     if (!(gamma >= 0.0f))
         return set_err(TRIM_EINVAL, "search_trim_ivf_knn: uncalibrated pruning profile");
-    if (k > 256)
-        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k > 256 is not supported by the GPU "
-                                    "top-k (warp register slots)");
+    if (k > kSmemTopKMax)
+        return set_err(TRIM_EINVAL, "search_trim_ivf_knn: k > %u is not supported by the GPU "
+                                    "top-k (shared-memory slots)", kSmemTopKMax);
     return TRIM_OK;
 }
 
@@ -515,7 +519,12 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
                unsigned long long* d_ct, uint32_t* d_status, cudaStream_t st) {
     if (nq == 0)
         return TRIM_OK;
-    const size_t smem = knn_smem_bytes(dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
+    size_t smem = knn_smem_bytes(k > 256 ? 0 : dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
+    uint32_t topk_off = 0;
+    if (k > 256) { // SmemTopK keys after the kernel's own layout
+        topk_off = static_cast<uint32_t>((smem + 15) & ~size_t(15));
+        smem = topk_off + sizeof(unsigned long long) * smem_topk_slots(k);
+    }
     if (smem > kSmemLimit)
         return set_err(TRIM_EINVAL,
                        "search_trim_ivf_knn: per-query state (%zu B for m=%u, ksub=%u, "
@@ -534,6 +543,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     p.dist_out = d_dist;
     p.counters = d_ct;
     p.status = d_status;
+    p.topk_off = topk_off;
     // list-level bound slack (list_lower_bound): relative error bounds of the
     // fp32 coarse distance (dim terms), of sqrt of the reference ADC (LUT entries of
     // <= max_sd terms summed over m), and of relaxed_lb's evaluation; u = 2^-24

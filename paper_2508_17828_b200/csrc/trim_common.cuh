@@ -129,6 +129,40 @@ __device__ __forceinline__ void build_lut_smem(const DevIndex& ix, const float* 
     }
 }
 
+// euclidean_sq (core/distance.hpp:11-29) of one row by a QUAD of lanes:
+// lane `sub` (0..3) of the quad owns accumulator acc_sub and adds
+// (q[4t+sub] - x[4t+sub])^2 for t = 0, 1, ... — exactly the reference's
+// chain for that accumulator (the tail, dim % 4, goes to acc0 = sub 0); then
+// (acc0 + acc1) + (acc2 + acc3) by two xor-shuffles (fp addition is
+// commutative, so every lane of the quad ends with the same bits). A third
+// of the instructions of one lane walking the whole row, and 8 rows per warp
+// pass. Warp-collective: all 32 lanes call it (`row` may be null on idle
+// quads); q in shared memory, rows 16-byte aligned.
+__device__ __forceinline__ float euclid_sq_quad(const float* __restrict__ q, const float* __restrict__ row,
+                                                uint32_t dim, uint32_t sub) {
+    float acc = 0.0f;
+    if (row) {
+        const uint32_t nv = dim >> 2;
+        // the row's 128-byte lines in flight at once (one DRAM round trip)
+        for (uint32_t o = sub * 128u; o < dim * 4u; o += 512u)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(row) + o));
+        const float* x = row + sub;
+        const float* qq = q + sub;
+#pragma unroll 8
+        for (uint32_t t = 0; t < nv; ++t) {
+            const float d = __fsub_rn(qq[4 * t], __ldg(x + 4 * t));
+            acc = __fadd_rn(acc, __fmul_rn(d, d));
+        }
+        if (sub == 0)
+            for (uint32_t i = nv << 2; i < dim; ++i) {
+                const float d = __fsub_rn(q[i], __ldg(row + i));
+                acc = __fadd_rn(acc, __fmul_rn(d, d));
+            }
+    }
+    const float t = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    return __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 } // namespace trimgpu

@@ -41,6 +41,11 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
                                           cudaStream_t st) {
     const uint32_t S = (p.k + 31) / 32;
     const dim3 grid(static_cast<unsigned>(p.nq));
+#if TRIM_M == 0
+    if (S > 8) // k > 256: shared-memory top-k (the host routes every such call here)
+        return p.plan ? launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, true>, grid, smem, st, ix, p)
+                      : launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, false>, grid, smem, st, ix, p);
+#endif
     if (p.plan) { // seeds + plan precomputed (trim_knn_setup_kernel)
         if (S <= 1)
             return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);

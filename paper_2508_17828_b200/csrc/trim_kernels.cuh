@@ -81,7 +81,7 @@ struct WarpTopK {
     uint32_t wid;
     uint32_t wslot;
 
-    __device__ __forceinline__ void init(uint32_t k) {
+    __device__ __forceinline__ void init(uint32_t k, void* = nullptr) {
         const uint32_t lane = lane_id();
 #pragma unroll
         for (int r = 0; r < S; ++r) {
@@ -169,6 +169,108 @@ struct WarpTopK {
 };
 
 // --------------------------------------------------------------------------
+// Shared-memory top-k for k > 256 (the reference's priority_queue has no cap,
+// ivf.hpp:256-302). Entries are 64-bit keys (dist bits << 32 | id): dist >= 0,
+// so key order is ScoredId order (core/ground_truth.hpp:39-50) and
+// `(d, id) < top` is `key < worst key`. Slots start as (+inf, 0xFFFFFFFF)
+// sentinels like WarpTopK's; the replay warp owns the array (slot s: lane
+// s % 32), tracks the worst by a lane scan + butterfly, and sorts the final
+// rows with a warp bitonic sort in place (padding keys ~0 sort last).
+// --------------------------------------------------------------------------
+constexpr uint32_t kSmemTopKMax = 4096;
+__host__ __device__ inline uint32_t smem_topk_slots(uint32_t k) {
+    uint32_t p = 32;
+    while (p < k)
+        p <<= 1;
+    return p;
+}
+
+struct SmemTopK {
+    unsigned long long* key; // smem_topk_slots(k) entries
+    uint32_t k, P;
+    float wd;
+    uint32_t wid;
+    uint32_t wslot;
+    unsigned long long wkey;
+
+    __device__ __forceinline__ void init(uint32_t k_, void* buf) {
+        key = static_cast<unsigned long long*>(buf);
+        k = k_;
+        P = smem_topk_slots(k_);
+        const uint32_t lane = lane_id();
+        for (uint32_t s = lane; s < P; s += kWarp)
+            key[s] = s < k ? (static_cast<unsigned long long>(0x7f800000u) << 32) | kInvalidId : ~0ull;
+        __syncwarp();
+        reduce_worst();
+    }
+    __device__ __forceinline__ void reduce_worst() {
+        const uint32_t lane = lane_id();
+        unsigned long long b = 0;
+        uint32_t bs = lane;
+        for (uint32_t s = lane; s < k; s += kWarp) {
+            const unsigned long long v = key[s];
+            if (v > b || s == lane) {
+                b = v;
+                bs = s;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+            const uint32_t os = __shfl_xor_sync(0xffffffffu, bs, o);
+            if (ob > b || (ob == b && os > bs)) {
+                b = ob;
+                bs = os;
+            }
+        }
+        wkey = b;
+        wslot = bs;
+        wd = __uint_as_float(static_cast<uint32_t>(b >> 32));
+        wid = static_cast<uint32_t>(b);
+    }
+    // `cand < result.top()` then pop/push (ivf.hpp:277-282). Warp-uniform.
+    __device__ __forceinline__ void offer(float cd, uint32_t cid) {
+        const unsigned long long c = (static_cast<unsigned long long>(__float_as_uint(cd)) << 32) | cid;
+        if (!(c < wkey))
+            return;
+        if (lane_id() == (wslot & 31u))
+            key[wslot] = c;
+        __syncwarp();
+        reduce_worst();
+    }
+    // Rows ascending by (dist, id) (ivf.hpp:292-302), sentinels last.
+    __device__ __forceinline__ void store_sorted(uint32_t, uint32_t* ids_out, float* dist_out) {
+        const uint32_t lane = lane_id();
+        for (uint32_t size = 2; size <= P; size <<= 1)
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = lane; i < P / 2; i += kWarp) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const unsigned long long a = key[lo], b = key[hi];
+                    if ((a > b) == up) {
+                        key[lo] = b;
+                        key[hi] = a;
+                    }
+                }
+                __syncwarp();
+            }
+        for (uint32_t s = lane; s < k; s += kWarp) {
+            ids_out[s] = static_cast<uint32_t>(key[s]);
+            dist_out[s] = __uint_as_float(static_cast<uint32_t>(key[s] >> 32));
+        }
+    }
+};
+
+template <int S>
+struct TopKOf {
+    using type = WarpTopK<S>;
+};
+template <>
+struct TopKOf<0> {
+    using type = SmemTopK;
+};
+
+// --------------------------------------------------------------------------
 // trim_knn_kernel — one CTA owns one query's candidate stream.
 //
 // The reference threshold max_dis is sequential state (ivf.hpp:256-287,
@@ -207,6 +309,7 @@ struct KnnParams {
     const float* xnorm;    // |x| per row, rounded up
     const float* xnorm2;   // |x|^2 per row
     const uint32_t* plan;  // per-query setup records (trim_knn_setup_kernel), or null: set up in the kernel
+    uint32_t topk_off;     // k > 256: byte offset of the SmemTopK keys in dynamic shared memory
 };
 
 // Per-query setup record written by trim_knn_setup_kernel (u32 words): the
@@ -249,6 +352,12 @@ constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per 
 #define TRIM_KRING 6
 #endif
 constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
+#ifndef TRIM_EARLY_FETCH
+#define TRIM_EARLY_FETCH 1 // workers issue chunk 0's loads before building the LUT (setup-record path)
+#endif
+#ifndef TRIM_QUAD_L2
+#define TRIM_QUAD_L2 1     // members' exact L2 by lane quads (euclid_sq_quad), 8 rows per warp pass
+#endif
 static_assert(kLaneU == 1, "bin_mask records one ballot per worker chunk");
 
 // Warps per filter CTA by code length: a long code (m = 120: a 128 KB LUT, one
@@ -481,8 +590,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         // ------------------------------------------------ replay warp
         // (the worker warps build the LUT meanwhile)
         TRIM_TL(if (tl && lane == 0) tl[1] = gtime();)
-        WarpTopK<S> topk;
-        topk.init(p.k);
+        typename TopKOf<S>::type topk; // S = 0: k > 256, the shared-memory top-k
+        topk.init(p.k, smem + p.topk_off);
         uint32_t carry = 0, nk = 0;
         if constexpr (PRE) { // seeds and plan from trim_knn_setup_kernel
             const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
@@ -701,6 +810,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     }
 
     // ---------------------------------------------------- worker warps
+    constexpr bool kEarlyFetch = PRE && TRIM_EARLY_FETCH;
     // flat scans with tensor-core bounds: |q| and |q|^2 rounded up (for E)
     float qn = 0.0f, qn2 = 0.0f;
     if (p.dap) {
@@ -711,24 +821,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     TRIM_TL(const bool wtl = tl && lane == 0; // lane 0 of every worker records (worker 0: slots 10-15)
             unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
             unsigned long long wk = wtl ? clock64() : 0;)
-    build_lut_blocked(ix, qv, lut, tid - kWarp, kThreads - kWarp);
-    named_sync(kBarWorkers, kThreads - kWarp); // workers only
+    // the compacted stream length: from the setup record right away (PRE), else
+    // published by the replay warp with the plan
     const uint32_t w = warp - 1;
-    LaneAdc la;
-    la.init(lane, LutShape::of(m));
-    TRIM_TL(if (wtl) {
-        const unsigned long long t = clock64();
-        wc[0] = t - wk;
-        wk = t;
-    })
-    named_sync(kBarPlan, kThreads); // seeds done, compacted stream ready
-    TRIM_TL(if (wtl) {
-        const unsigned long long t = clock64();
-        wc[1] = t - wk;
-        wk = t;
-    })
-    const uint32_t bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
-    const uint32_t nchunks = (bound + kChunkW - 1) / kChunkW;
+    uint32_t bound = kEarlyFetch ? __ldg(rec + 3) : 0u;
+    uint32_t nchunks = (bound + kChunkW - 1) / kChunkW;
     uint32_t li = 0; // list cursor (positions of a lane only increase)
     struct Cand {
         FastCode<M> fc;
@@ -760,6 +857,28 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             }
         }
     };
+    if (kEarlyFetch) // the first chunk's codes in flight while the LUT is built
+        fetch(0, sa);
+    build_lut_blocked<M>(ix, qv, lut, tid - kWarp, kThreads - kWarp);
+    named_sync(kBarWorkers, kThreads - kWarp); // workers only
+    LaneAdc la;
+    la.init(lane, LutShape::of(m));
+    TRIM_TL(if (wtl) {
+        const unsigned long long t = clock64();
+        wc[0] = t - wk;
+        wk = t;
+    })
+    named_sync(kBarPlan, kThreads); // seeds done, compacted stream ready
+    TRIM_TL(if (wtl) {
+        const unsigned long long t = clock64();
+        wc[1] = t - wk;
+        wk = t;
+    })
+    if (!kEarlyFetch) {
+        bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
+        nchunks = (bound + kChunkW - 1) / kChunkW;
+        fetch(0, sa);
+    }
     auto process = [&](uint32_t c, Slot& cur) {
         const uint32_t s = c % kRing;
         TRIM_TL(const unsigned long long k0 = wtl ? clock64() : 0;)
@@ -785,10 +904,12 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         TRIM_TL(const unsigned long long k2 = wtl ? clock64() : 0;)
         uint32_t id = 0;
         float d = 0.0f;
+        bool exact = false;
+        uint64_t rw = 0;
         if (keep) { // exact L2 (ivf.hpp:276) of every member the replay may evaluate
             id = __ldg(ix.list_ids + x.e);
-            const uint64_t rw = id - ix.id_base;
-            bool exact = true;
+            rw = id - ix.id_base;
+            exact = true;
             if (p.dap) { // d >= D~ - E > T_pub >= T_live: cannot replace the top (ivf.hpp:277)
                 const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(p.xnorm + rw)), 1.0f / 128.0f),
                                           __fmul_ru(__fadd_ru(qn2, __ldg(p.xnorm2 + rw)), 1.0f / 16384.0f));
@@ -798,8 +919,28 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     exact = false;
                 }
             }
-            if (exact) // the whole row in flight at once (one DRAM round trip)
-                d = euclid_sq_vec4(qv, ix.vectors + rw * ix.dim_stride, ix.dim, true);
+        }
+        // the members' exact distances, 8 rows per warp pass: quad g = lane / 4
+        // takes the g-th remaining member (euclid_sq_quad, the reference's
+        // accumulator chains one per lane of the quad)
+        if (!TRIM_QUAD_L2 && exact) // one lane walks the whole row (A/B: TRIM_QUAD_L2=0)
+            d = euclid_sq_vec4(qv, ix.vectors + rw * ix.dim_stride, ix.dim, true);
+        for (uint32_t em = TRIM_QUAD_L2 ? __ballot_sync(0xffffffffu, exact) : 0u; em;) {
+            const uint32_t g = lane >> 2;
+            uint32_t mm = em;
+            for (uint32_t i = 0; i < g; ++i)
+                mm &= mm - 1;
+            const int src = mm ? __ffs(mm) - 1 : -1;
+            const uint64_t rs = __shfl_sync(0xffffffffu, rw, src < 0 ? 0 : src);
+            const float dq = euclid_sq_quad(qv, src < 0 ? nullptr : ix.vectors + rs * ix.dim_stride, ix.dim,
+                                            lane & 3u);
+            const uint32_t rank = __popc(em & ((1u << lane) - 1u));
+            const float mine = __shfl_sync(0xffffffffu, dq, (rank & 7u) * 4u);
+            if (exact && rank < 8)
+                d = mine;
+            for (int i = 0; i < 8 && em; ++i) // drop this pass's members
+                em &= em - 1;
+            exact = exact && rank >= 8;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, keep);
         if (keep) {
@@ -820,7 +961,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             wc[4] += clock64() - k2;
         })
     };
-    fetch(0, sa);
     for (uint32_t c = 0; c < nchunks; c += 2) {
         fetch(c + 1, sb); // prefetch: loads in flight while chunk c is filtered
         process(c, sa);
@@ -916,7 +1056,7 @@ trim_range_kernel(DevIndex ix, RangeParams p) {
     if (begin >= total)
         return;
     const uint32_t end = min(total, begin + slice);
-    build_lut_blocked(ix, qv, lut);
+    build_lut_blocked<M>(ix, qv, lut);
     const float r2 = p.radius_sq[q];
     LaneAdc la;
     la.init(lane, LutShape::of(m));
@@ -1054,7 +1194,7 @@ trim_range_flat_kernel(DevIndex ix, RangeParams p, uint32_t qt) {
     const uint32_t end = min(total, begin + p.slice);
     __syncthreads();
     for (uint32_t t = 0; t < nqt; ++t)
-        build_lut_blocked(ix, qvs + t * ix.dim_stride, reinterpret_cast<float*>(smem + static_cast<size_t>(t) * lutb));
+        build_lut_blocked<M>(ix, qvs + t * ix.dim_stride, reinterpret_cast<float*>(smem + static_cast<size_t>(t) * lutb));
     __syncthreads();
     LaneAdc la;
     la.init(lane, LutShape::of(m));

@@ -269,3 +269,40 @@ def test_list_skip_parity(clustered, gamma, k, mode, monkeypatch):
         assert skipped == 0  # no bound for γ(2-γ) <= 0 / disabled
     elif gamma in (0.5, 1.0) and k == 10:
         assert skipped > 0
+
+
+# ------------------------------------------- k > 256 (shared-memory top-k)
+@pytest.mark.parametrize("k", [257, 1000, 4096])
+@pytest.mark.parametrize("gamma", [0.0, 0.8])
+def test_large_k_vs_reference(clustered, k, gamma):
+    """The reference's priority_queue has no cap (ivf.hpp:256-302): k = 257,
+    1000 and 4096 run the shared-memory top-k and must equal the reference
+    itself (oracle/_ref, per query) — ids, dist bits and counters."""
+    hix, qs, gix = clustered
+    ref = RefOracle()
+    sess = ref.session(hix)
+    try:
+        want = ref.session_knn(sess, qs[:40], k, 32, gamma)
+    finally:
+        ref.session_destroy(sess)
+    got = G.search_trim_ivf_knn_batch(gix, G.PruningProfile.manual(gamma), qs[:40], k, 32)
+    np.testing.assert_array_equal(got[0], want[0])
+    assert_bits(got[1], want[1])
+    np.testing.assert_array_equal(got[2][:, :5], want[2])
+    np.testing.assert_array_equal(got[2][:, 5], want[3])
+
+
+def test_large_k_flat_and_cap():
+    ix, qs, cases = goldens.load("flat_d128_m16")
+    if ix is None:
+        pytest.skip("no flat fixture")
+    gix = G.GpuIvfIndex(G.IvfArrays.from_any(ix))
+    hix = goldens.host_index(ix)
+    for k in (300, 999):
+        want = co.search_knn(hix, qs, k, 1, 0.5)
+        got = G.search_trim_ivf_knn_batch(gix, G.PruningProfile.manual(0.5), qs, k, 1)
+        np.testing.assert_array_equal(got[0], want[0])
+        assert_bits(got[1], want[1])
+        np.testing.assert_array_equal(got[2][:, :5], want[2])
+    with pytest.raises(G.InvalidArgument):
+        G.search_trim_ivf_knn_batch(gix, G.PruningProfile.manual(0.5), qs, 4097, 1)

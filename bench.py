@@ -64,8 +64,8 @@ CONFIGS = {
 
 
 def metric_name(cfg):
-    what = "range filter, flat" if cfg.get("kind") == "range" else "kNN filter"
-    return f"candidates filtered/sec (TRIM {what}; QPS, %HBM roofline, prune ratio alongside)"
+    what = "range search, flat" if cfg.get("kind") == "range" else "kNN search"
+    return f"queries/sec (TRIM {what}; candidates filtered/sec, %HBM roofline, prune ratio alongside)"
 
 
 def log(*a):
@@ -473,10 +473,10 @@ def run_ours(args, cfg):
     value = total_cand / (ms / 1e3)
     qps = nq * args.steps / (ms / 1e3)
     out = dict(metric=metric_name(cfg),
-               value=value, unit="candidates/s", n_gpus=ngpu, steps=args.steps,
+               value=qps, unit="queries/s", n_gpus=ngpu, steps=args.steps,
                warmup=args.warmup, ms_per_step=ms / args.steps, higher_is_better=True,
                scaling="strong" if replicas else "weak", vs_baseline=None, dtype="f32 (u8 PQ codes)",
-               data="synthetic")
+               data="synthetic", candidates_per_s=value)
     out["config"] = config_dict(cfg, head, ngpu, parallelism_of(ngpu, mode if ngpu > 1 or sharded else "single"),
                                 fprint)
     out["mode"] = {"single": "one process, one GPU", "shard": "torchrun, one process per GPU (id-shard, "
@@ -485,7 +485,6 @@ def run_ours(args, cfg):
                    "group": "one process, one multi-device index behind the C ABI (trim_index_desc "
                             "devices[], TRIM_SHARD_ID: NCCL broadcast + all-gather + device merge in "
                             "every trim_search_knn_device call)"}[mode]
-    out["qps"] = qps
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
     out["candidates_per_query"] = evaluated / nq
     # roofline of the dominant kernel (the fused filter), per launch
@@ -635,19 +634,20 @@ def e2e(gix, queries, cfg, gamma, args, world, rank):
             cand += once()
         torch.cuda.synchronize()
         sec = time.perf_counter() - t0
-    return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
+    return dict(value=nq * steps / sec, unit="queries/s", candidates_per_s=cand / sec,
                 h2d_bytes_per_step=nq * cfg["dim"] * 4,
                 d2h_bytes_per_step=nq * k * 8 + nq * 48 + 4 * len(range(0, nq, B)),
                 api=f"trim_search_knn (C ABI, host buffers; pinned queries and results; {max(1, args.streams)} client threads)")
 
 
 def e2e_sharded(gix, queries, cfg, gamma, args, world, rank, local):
-    """e2e at N ranks, one process per GPU: every batch is copied from pinned
-    host memory, searched on the local shard (trim_search_knn_device), its
-    local top-k all-gathered over NCCL and merged on the device
-    (trim_merge_topk_device), and the merged rows + summed counters copied back
-    to pinned host memory — the exchange is inside the timed region. Wall
-    clock, max over ranks."""
+    """e2e at N ranks, one process per GPU, per step: the query set copied
+    from pinned host memory, every batch searched on the local shard
+    (trim_search_knn_device, batches alternating over `--streams` streams),
+    the local top-k of all batches all-gathered over NCCL, merged on the device
+    (trim_merge_topk_device), the counters all-reduced, and the merged rows +
+    counters copied back to pinned host memory — the exchange is inside the
+    timed region. Wall clock, max over ranks."""
     import ctypes as C
 
     import torch
@@ -661,34 +661,40 @@ def e2e_sharded(gix, queries, cfg, gamma, args, world, rank, local):
     h_ids = torch.empty((nq, k), dtype=torch.int32).pin_memory()
     h_d = torch.empty((nq, k), dtype=torch.float32).pin_memory()
     h_ct = torch.empty((nq, 6), dtype=torch.int64).pin_memory()
-    dq = torch.empty((B, D), dtype=torch.float32, device=dev)
-    ids = torch.empty((B, k), dtype=torch.int32, device=dev)
-    dd = torch.empty((B, k), dtype=torch.float32, device=dev)
-    ct = torch.zeros((B, 6), dtype=torch.int64, device=dev)
+    dq = torch.empty((nq, D), dtype=torch.float32, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dd = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    ct = torch.zeros((nq, 6), dtype=torch.int64, device=dev)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    g_ids = torch.empty((world * B, k), dtype=torch.int32, device=dev)
-    g_d = torch.empty((world * B, k), dtype=torch.float32, device=dev)
-    m_ids = torch.empty((B, k), dtype=torch.int32, device=dev)
-    m_d = torch.empty((B, k), dtype=torch.float32, device=dev)
-    sh = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    g_ids = torch.empty((world * nq, k), dtype=torch.int32, device=dev)
+    g_d = torch.empty((world * nq, k), dtype=torch.float32, device=dev)
+    m_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    m_d = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    main = torch.cuda.current_stream(dev)
+    streams = [main] + [torch.cuda.Stream(dev) for _ in range(max(1, args.streams) - 1)]
+    sh = C.c_void_p(main.cuda_stream)
+    P = lambda t, off=0: C.c_void_p(t.data_ptr() + off)  # noqa: E731
     steps = max(1, min(args.steps, 3))
 
     def once():
-        cand = 0
-        for b in range(0, nq, B):
+        dq.copy_(hq, non_blocking=True)
+        for x in streams[1:]:
+            x.wait_stream(main)
+        for i, b in enumerate(range(0, nq, B)):
             nb = min(B, nq - b)
-            dq[:nb].copy_(hq[b:b + nb], non_blocking=True)
-            _lib.check(lib.trim_search_knn_device(gix.handle, P(dq), nb, k, cfg["nprobe"], float(np.float32(gamma)),
-                                                  P(ids), P(dd), P(ct), P(st), sh), "knn")
-            dist.all_gather_into_tensor(g_ids[:world * nb], ids[:nb])
-            dist.all_gather_into_tensor(g_d[:world * nb], dd[:nb])
-            _lib.check(lib.trim_merge_topk_device(P(g_d), P(g_ids), world, nb, k, P(m_d), P(m_ids), local, sh),
-                       "merge")
-            dist.all_reduce(ct[:nb])
-            h_ids[b:b + nb].copy_(m_ids[:nb], non_blocking=True)
-            h_d[b:b + nb].copy_(m_d[:nb], non_blocking=True)
-            h_ct[b:b + nb].copy_(ct[:nb], non_blocking=True)
+            x = streams[i % len(streams)]
+            _lib.check(lib.trim_search_knn_device(gix.handle, P(dq, b * D * 4), nb, k, cfg["nprobe"],
+                                                  float(np.float32(gamma)), P(ids, b * k * 4), P(dd, b * k * 4),
+                                                  P(ct, b * 48), P(st), C.c_void_p(x.cuda_stream)), "knn")
+        for x in streams[1:]:
+            main.wait_stream(x)
+        dist.all_gather_into_tensor(g_ids, ids)
+        dist.all_gather_into_tensor(g_d, dd)
+        _lib.check(lib.trim_merge_topk_device(P(g_d), P(g_ids), world, nq, k, P(m_d), P(m_ids), local, sh), "merge")
+        dist.all_reduce(ct)
+        h_ids.copy_(m_ids, non_blocking=True)
+        h_d.copy_(m_d, non_blocking=True)
+        h_ct.copy_(ct, non_blocking=True)
         torch.cuda.synchronize()
         return int(h_ct[:, 3].sum())
 
@@ -703,11 +709,11 @@ def e2e_sharded(gix, queries, cfg, gamma, args, world, rank, local):
     t = torch.tensor([sec], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     sec = float(t.item())
-    return dict(value=cand / sec, unit="candidates/s", qps=nq * steps / sec,
+    return dict(value=nq * steps / sec, unit="queries/s", candidates_per_s=cand / sec,
                 h2d_bytes_per_step=nq * D * 4, d2h_bytes_per_step=nq * k * 8 + nq * 48,
-                api="per batch: pinned H2D, trim_search_knn_device on the local shard, NCCL all-gather "
-                    "(torch.distributed), trim_merge_topk_device, counters all-reduce, pinned D2H; "
-                    "wall clock, max over ranks",
+                api="per step: pinned H2D of the query set, trim_search_knn_device per batch on the local "
+                    "shard, NCCL all-gather (torch.distributed), trim_merge_topk_device, counters all-reduce, "
+                    "pinned D2H; wall clock, max over ranks",
                 includes_exchange=True)
 
 
@@ -739,7 +745,11 @@ def baseline_line(gix, arrays, queries, cfg, args):
 
 
 def _host_index(h):
+    """oracle HostIndex of a fixture namespace / IvfArrays (host numpy or torch tensors)."""
     from oracle.oracle import HostIndex
+    if hasattr(h.vectors, "is_cuda") or hasattr(h.list_ids, "is_cuda"):
+        import bench_fixture as F
+        h = F.to_host(h)
     return HostIndex(dim=h.dim, m=h.m, ksub=h.ksub, sub_dims=h.sub_dims, centroids=h.centroids,
                      coarse=h.coarse, list_offsets=h.list_offsets, list_ids=h.list_ids,
                      list_codes=h.list_codes, list_lx=h.list_lx, vectors=h.vectors)
@@ -827,14 +837,14 @@ def cpu_baseline(hfx, queries, cfg, gamma, args, fx=None):
     rt = RefTimer(hix, cfg, gamma, threads)
     try:
         r = rt.bounded(qs, args.cpu_seconds)
-        out = dict(value=r["value"], unit="candidates/s", cores=threads, kind=rt.kind,
+        out = dict(value=r["qps"], unit="queries/s", candidates_per_s=r["value"], cores=threads, kind=rt.kind,
                    sample=f"first {r['n']} of {len(qs)} queries of {cfg['workload']} at gamma={gamma}, "
                           f"{threads} threads, {r['sec']:.1f}s",
-                   qps=r["qps"], prune_ratio=r["prune_ratio"], cpu_model=cpu_model(),
+                   prune_ratio=r["prune_ratio"], cpu_model=cpu_model(),
                    timing="steady_clock around parallel_for over queries (sweep.hpp:121-152)")
         rt.set_threads(1)
         r1 = rt.bounded(qs, max(2.0, args.cpu_seconds / 3))
-        out["single_thread"] = dict(value=r1["value"], unit="candidates/s", qps=r1["qps"], cores=1,
+        out["single_thread"] = dict(value=r1["qps"], unit="queries/s", candidates_per_s=r1["value"], cores=1,
                                     sample=f"first {r1['n']} queries, 1 thread, {r1['sec']:.1f}s")
         if cfg.get("baseline_kprime"):
             rt.set_threads(threads)
@@ -988,12 +998,12 @@ def run_ours_range(args, cfg):
     evaluated, dc = float(ct[3]), float(ct[0])
     value = evaluated * args.steps / (ms / 1e3)
     out = dict(metric=metric_name(cfg),
-               value=value, unit="candidates/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+               value=nq * args.steps / (ms / 1e3), unit="queries/s", candidates_per_s=value,
+               n_gpus=world, steps=args.steps, warmup=args.warmup,
                ms_per_step=ms / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
                dtype="f32 (u8 PQ codes)", data="synthetic")
     out["config"] = config_dict(cfg, head, world, parallelism_of(world, "single"), fprint, radius=radius,
                                 radius_rule="pick_radius_for_fraction(100/N, 20000 rows, 200 queries)")
-    out["qps"] = nq * args.steps / (ms / 1e3)
     out["prune_ratio"] = float(ct[2] / max(1, ct[2] + ct[0]))
     out["mean_result_size"] = float(counts.double().mean())
     qt = gix.info()["range_query_tile"]
@@ -1036,7 +1046,7 @@ def run_ours_range(args, cfg):
         c, nres = once()
         tot += c
     sec = time.perf_counter() - t0
-    out["e2e"] = dict(value=tot / sec, unit="candidates/s", qps=nq * reps / sec,
+    out["e2e"] = dict(value=nq * reps / sec, unit="queries/s", candidates_per_s=tot / sec,
                       h2d_bytes_per_step=nq * D * 4 + nq * 4,
                       d2h_bytes_per_step=nres * 8 + (nq + 1) * 8 + nq * 48,
                       api=f"trim_search_range (C ABI, host buffers; {max(1, args.streams)} client threads)")
@@ -1349,18 +1359,19 @@ def run_reference(args, cfg):
             dcs += dc
             prs += pr
     rt.close()
-    value = evs / secs
+    value = nstep * args.steps / secs
     out = dict(metric=metric_name(cfg),
-               value=value, unit="candidates/s", n_gpus=ngpu, steps=args.steps,
+               value=value, unit="queries/s", candidates_per_s=evs / secs, n_gpus=ngpu, steps=args.steps,
                warmup=args.warmup, ms_per_step=secs * 1e3 / args.steps, higher_is_better=True,
                scaling="strong" if mode == "replicas" else "weak", vs_baseline=None, dtype="f32 (u8 PQ codes)",
                data="synthetic", impl="reference", config=conf,
-               qps=nstep * args.steps / secs, prune_ratio=prs / max(1, prs + dcs),
-               cpu_baseline=dict(value=value, unit="candidates/s", cores=threads, kind=rt.kind,
+               prune_ratio=prs / max(1, prs + dcs),
+               cpu_baseline=dict(value=value, unit="queries/s", candidates_per_s=evs / secs, cores=threads,
+                                 kind=rt.kind,
                                  sample=f"{nstep} queries per step (of {len(qs)}) of {cfg['workload']}, "
                                         f"{threads} threads" + (" (rank 0's shard)" if ngpu > 1 else ""),
                                  cpu_model=cpu_model()),
-               e2e=dict(value=value, unit="candidates/s", h2d_bytes_per_step=0,
+               e2e=dict(value=value, unit="queries/s", h2d_bytes_per_step=0,
                         d2h_bytes_per_step=0))
     print(json.dumps(out), flush=True)
 

@@ -6,11 +6,14 @@
 // B200 build runs here:
 //   * seeded synthetic data (Philox4x32-10 + Box-Muller; blob rows are
 //     assigned round-robin like make_blob_dataset, core/synthetic.hpp:21-33);
-//   * k-means: k-means++ seeding (one CTA, deterministic reductions), Lloyd
-//     steps with the reference's exact nearest-centroid arithmetic and ties
+//   * k-means, bit-identical to pq::kmeans (kmeans.hpp:89-158): k-means++
+//     seeding with the reference's std::mt19937_64 draws and sequential D^2
+//     sums/scan on the host, distance updates on the device; Lloyd steps with
+//     the reference's exact nearest-centroid arithmetic and ties
 //     (pq/kmeans.hpp:27-41), per-cluster double sums in ascending point order
 //     (kmeans.hpp:129-140) and the reference's empty-cluster repair
-//     (kmeans.hpp:111-127);
+//     (kmeans.hpp:111-127) — so pq::train and build_ivf reproduce the
+//     reference's codebook, coarse quantizer and lists from the same rows;
 //   * PQ encode + Γ(l,x) bit-exact with pq::encode / build_landmarks;
 //   * lists in ascending id order (stable radix sort by list id, ivf.hpp:147-152).
 // Row samples use the reference's own Fisher-Yates sampler with std::mt19937_64
@@ -319,76 +322,21 @@ void launch_assign(const float* x, uint64_t n, uint32_t dim, const float* cent, 
 }
 
 // ------------------------------------------------------------ k-means++
-// One CTA. d2 kept in global (double); thread t owns a contiguous range so
-// the prefix used for D^2 sampling is deterministic.
-constexpr int kPPThreads = 1024;
-
-__global__ void __launch_bounds__(kPPThreads)
-kmeanspp_kernel(const float* __restrict__ x, uint64_t n, uint32_t dim, uint32_t k, uint64_t seed,
-                float* cent, double* d2) {
-    __shared__ double part[kPPThreads];
-    __shared__ uint64_t s_choice;
-    const uint32_t t = threadIdx.x;
-    const uint64_t per = (n + kPPThreads - 1) / kPPThreads;
-    const uint64_t b = min(n, t * per), e = min(n, b + per);
-    auto rnd = [&](uint32_t c) {
-        const uint4 r = philox4x32(make_uint4(c, 0x243F6A88u, 0x85A308D3u, 0x13198A2Eu),
-                                   make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
-        const uint64_t v = (static_cast<uint64_t>(r.x) << 21) ^ (static_cast<uint64_t>(r.y) >> 11);
-        return static_cast<double>(v & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0); // [0,1)
-    };
-    if (t == 0)
-        s_choice = static_cast<uint64_t>(rnd(0) * static_cast<double>(n)) % n;
-    __syncthreads();
-    for (uint32_t j = t; j < dim; j += kPPThreads)
-        cent[j] = x[s_choice * dim + j];
-    __syncthreads();
-    for (uint64_t i = b; i < e; ++i)
-        d2[i] = euclid_sq_generic(x + i * dim, cent, dim);
-    for (uint32_t c = 1; c < k; ++c) {
-        double s = 0.0;
-        for (uint64_t i = b; i < e; ++i)
-            s += d2[i];
-        part[t] = s;
-        __syncthreads();
-        if (t == 0) {
-            double tot = 0.0;
-            for (int i = 0; i < kPPThreads; ++i)
-                tot += part[i];
-            uint64_t chosen;
-            if (tot <= 0.0) {
-                chosen = static_cast<uint64_t>(rnd(c) * static_cast<double>(n)) % n;
-            } else {
-                double target = rnd(c) * tot;
-                int w = 0;
-                for (; w < kPPThreads - 1; ++w) {
-                    if (target - part[w] <= 0.0)
-                        break;
-                    target -= part[w];
-                }
-                const uint64_t wb = min(n, w * per), we = min(n, wb + per);
-                chosen = we ? we - 1 : 0;
-                for (uint64_t i = wb; i < we; ++i) {
-                    target -= d2[i];
-                    if (target <= 0.0) {
-                        chosen = i;
-                        break;
-                    }
-                }
-            }
-            s_choice = chosen;
-        }
-        __syncthreads();
-        float* dst = cent + static_cast<size_t>(c) * dim;
-        for (uint32_t j = t; j < dim; j += kPPThreads)
-            dst[j] = x[s_choice * dim + j];
-        __syncthreads();
-        for (uint64_t i = b; i < e; ++i) {
-            const double d = euclid_sq_generic(x + i * dim, dst, dim);
-            d2[i] = d2[i] < d ? d2[i] : d;
-        }
-        __syncthreads();
-    }
+// detail::kmeanspp_init (kmeans.hpp:43-86), bit for bit: the draws come from
+// the reference's own generator and distributions on the host
+// (std::mt19937_64, uniform_int_distribution<size_t>, uniform_real_distribution
+// <double> — the same libstdc++ as the reference build), the D^2 total is the
+// reference's sequential double sum and the weighted pick its sequential
+// subtraction scan (host, over the device-computed d2 copied back), and the
+// O(n*dim) distance updates run on the device with the reference arithmetic
+// (float euclidean_sq widened to double, d2 = min(d2, d)).
+__global__ void kmeanspp_d2_kernel(const float* __restrict__ x, uint64_t n, uint32_t dim,
+                                   const float* __restrict__ c, double* d2, int first) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const double d = euclid_sq_generic(x + i * dim, c, dim);
+    d2[i] = first ? d : (d < d2[i] ? d : d2[i]);
 }
 
 // Lloyd update: cluster c's centroid = float(sum_{i in c, ascending} x_i * (1/size))
@@ -567,10 +515,49 @@ std::vector<uint64_t> sample_rows(uint64_t n, uint64_t sample_n, uint64_t seed) 
 void kmeans_device(const float* x, uint64_t n, uint32_t dim, uint32_t k, uint32_t iters, uint64_t seed,
                    float* cent, cudaStream_t st) {
     {
+        std::mt19937_64 rng(seed);
+        std::uniform_int_distribution<std::size_t> uni(0, n - 1);
+        const std::size_t first = uni(rng);
+        BK(cudaMemcpyAsync(cent, x + first * dim, sizeof(float) * dim, cudaMemcpyDeviceToDevice, st));
         DArr<double> d2(n);
-        kmeanspp_kernel<<<1, kPPThreads, 0, st>>>(x, n, dim, k, seed, cent, d2.p);
-        BK(cudaGetLastError());
-        BK(cudaStreamSynchronize(st));
+        double* hd2 = nullptr;
+        BK(cudaMallocHost(&hd2, sizeof(double) * n));
+        const unsigned nb = static_cast<unsigned>((n + 255) / 256);
+        try {
+            kmeanspp_d2_kernel<<<nb, 256, 0, st>>>(x, n, dim, cent, d2.p, 1);
+            BK(cudaGetLastError());
+            for (uint32_t c = 1; c < k; ++c) {
+                BK(cudaMemcpyAsync(hd2, d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+                BK(cudaStreamSynchronize(st));
+                double total = 0.0;
+                for (uint64_t i = 0; i < n; ++i)
+                    total += hd2[i];
+                std::size_t chosen;
+                if (total <= 0.0) {
+                    chosen = uni(rng); // all mass collapsed; fall back to uniform
+                } else {
+                    std::uniform_real_distribution<double> ud(0.0, total);
+                    double target = ud(rng);
+                    chosen = n - 1;
+                    for (uint64_t i = 0; i < n; ++i) {
+                        target -= hd2[i];
+                        if (target <= 0.0) {
+                            chosen = i;
+                            break;
+                        }
+                    }
+                }
+                float* dst = cent + static_cast<size_t>(c) * dim;
+                BK(cudaMemcpyAsync(dst, x + chosen * dim, sizeof(float) * dim, cudaMemcpyDeviceToDevice, st));
+                kmeanspp_d2_kernel<<<nb, 256, 0, st>>>(x, n, dim, dst, d2.p, 0);
+                BK(cudaGetLastError());
+            }
+            BK(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaFreeHost(hd2);
+            throw;
+        }
+        cudaFreeHost(hd2);
     }
     DArr<uint32_t> assign(n), skeys(n), order(n);
     DArr<float> pdist(n);

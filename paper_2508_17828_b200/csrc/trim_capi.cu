@@ -502,12 +502,13 @@ bool ensure_flat_tiles(trim_index* ix) {
 
 // D~ for nq queries (tiled) x every row, row tiles in launches of <= 65535 (grid.y).
 void launch_flat_dist(const float4* qtiles, const float* qn2, uint64_t nq, uint64_t nqt, const trim_index* ix,
-                      uint32_t K, float* dap, uint64_t ld, uint64_t nrt, cudaStream_t st) {
+                      uint32_t K, float* dap, uint64_t ld, uint64_t nrt, cudaStream_t st,
+                      __nv_bfloat16* lb = nullptr) {
     for (uint64_t r0 = 0; r0 < nrt; r0 += 65535) {
         const uint64_t ny = std::min<uint64_t>(65535, nrt - r0);
         trim_flat_dist_kernel<<<dim3(static_cast<unsigned>(nqt), static_cast<unsigned>(ny)), kMmaThreads,
                                 flat_mma_smem(), st>>>(qtiles, qn2, nq, ix->flat_tiles, ix->xn2, ix->dev.n, K, dap, ld,
-                                                       r0);
+                                                       r0, lb, ix->xn);
         CK(cudaGetLastError());
     }
 }
@@ -569,7 +570,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     // slices: grid.x <= 2^31-1; with bounds, D~ of a slice (nq x ld floats) within ~8 GB
     uint64_t slice = 1u << 30;
     if (flat_bounds)
-        slice = std::max<uint64_t>(kMmaM, (8ull << 30) / (ld * 4) / kMmaM * kMmaM);
+        slice = std::max<uint64_t>(kMmaM, (8ull << 30) / (ld * 2) / kMmaM * kMmaM);
     for (uint64_t b = 0; b < nq; b += slice) {
         KnnParams pb = p;
         pb.nq = std::min<uint64_t>(slice, nq - b);
@@ -586,14 +587,13 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
             trim_query_norm_kernel<<<static_cast<unsigned>((pb.nq + 255) / 256), 256, 0, st>>>(qb, pb.nq, v.dim_stride,
                                                                                                v.dim, qn2.as<float>());
             CK(cudaGetLastError());
-            dap = DevBuf(sizeof(float) * pb.nq * ld, st);
+            dap = DevBuf(sizeof(__nv_bfloat16) * pb.nq * ld, st); // bf16 lower bounds D~ - E
             CK(cudaFuncSetAttribute(trim_flat_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(flat_mma_smem())));
-            launch_flat_dist(qtiles.as<float4>(), qn2.as<float>(), pb.nq, nqt, ix, K, dap.as<float>(), ld, nrt, st);
-            pb.dap = dap.as<float>();
+            launch_flat_dist(qtiles.as<float4>(), qn2.as<float>(), pb.nq, nqt, ix, K, nullptr, ld, nrt, st,
+                             dap.as<__nv_bfloat16>());
+            pb.dap = dap.as<__nv_bfloat16>();
             pb.dap_ld = ld;
-            pb.xnorm = ix->xn;
-            pb.xnorm2 = ix->xn2;
         }
         pb.queries = d_q + b * ix->dev.dim_stride;
         pb.probe = p.probe ? p.probe + b * np : nullptr;

@@ -8,7 +8,9 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 namespace trimgpu {
 

@@ -19,6 +19,8 @@
 // members that provably cannot enter the top-k.
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "trim_probe_mma.cuh"
 
 namespace trimgpu {
@@ -75,12 +77,23 @@ __global__ void trim_row_norm_kernel(const float* __restrict__ rows, uint64_t nr
     n[r] = __double2float_ru(sqrt(s) * (1.0 + 1e-12));
 }
 
+// Bound on |D~ - |q - x|^2| of the tf32 distance (2x margin); norms rounded up.
+__device__ __forceinline__ float gt_err(float qn, float qn2, float xn, float xn2) {
+    return __fadd_ru(__fmul_ru(__fmul_ru(qn, xn), 1.0f / 128.0f), __fmul_ru(__fadd_ru(qn2, xn2), 1.0f / 16384.0f));
+}
+
 // grid (query tiles, row tiles) — query tiles fastest, so the CTAs sharing a
 // row tile run together and read it from HBM once. kMmaThreads threads.
+// Two outputs: dap (fp32 D~, the exact ground-truth kernel takes D~ +- E), or,
+// when lb is set (the kNN filter), the rigorous lower bound D~ - E (E =
+// 2^-7|q||x| + 2^-14(|q|^2 + |x|^2) from rounded-up norms, gt_err) rounded
+// down to bf16: half the bytes of the nq x rows matrix, and the filter loads
+// no norms.
 __global__ void __launch_bounds__(kMmaThreads, 2)
 trim_flat_dist_kernel(const float4* __restrict__ qtiles, const float* __restrict__ qn2, uint64_t nq,
                       const float4* __restrict__ rtiles, const float* __restrict__ xn2, uint64_t nrows, uint32_t kpad,
-                      float* __restrict__ dap, uint64_t ld, uint64_t rt0) {
+                      float* __restrict__ dap, uint64_t ld, uint64_t rt0, __nv_bfloat16* __restrict__ lb,
+                      const float* __restrict__ xn) {
     extern __shared__ __align__(128) unsigned char fm_smem[];
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     const uint64_t qt = blockIdx.x, rt = rt0 + blockIdx.y; // row tiles launched in groups of <= 65535
@@ -146,6 +159,7 @@ trim_flat_dist_kernel(const float4* __restrict__ qtiles, const float* __restrict
         const uint32_t quarter = warp & 3u;
         const uint64_t q = qt * kMmaM + quarter * 32 + lane;
         const float qq = q < nq ? qn2[q] : 0.0f;
+        const float qq_up = __fmul_ru(qq, 1.0f + 1.0f / 1048576.0f), qn_up = __fsqrt_ru(qq_up);
         mbar_wait_u(done, 0);
         tc_fence_after();
         const uint64_t r0 = rt * kMmaN;
@@ -153,7 +167,27 @@ trim_flat_dist_kernel(const float4* __restrict__ qtiles, const float* __restrict
         for (uint32_t j0 = 0; j0 < kMmaN; j0 += 32) {
             float v[32];
             tc_ld32(tmem + ((quarter * 32u) << 16) + j0, v);
-            if (q < nq) {
+            if (q < nq && lb) {
+                uint4* dst = reinterpret_cast<uint4*>(lb + q * ld + r0 + j0);
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int h = 0; h < 8; h += 2) {
+                        float l2[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const uint64_t r = min(r0 + j0 + j + h + e, nrows - 1);
+                            const float x2 = __ldg(xn2 + r);
+                            const float dt = __fsub_rn(__fadd_rn(qq, x2), __fmul_rn(2.0f, v[j + h + e]));
+                            l2[e] = __fsub_rd(dt, gt_err(qn_up, qq_up, __ldg(xn + r), x2));
+                        }
+                        const __nv_bfloat162 b = __halves2bfloat162(__float2bfloat16_rd(l2[0]), __float2bfloat16_rd(l2[1]));
+                        w[h / 2] = *reinterpret_cast<const uint32_t*>(&b);
+                    }
+                    dst[j / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            } else if (q < nq) {
                 float4* dst = reinterpret_cast<float4*>(dap + q * ld + r0 + j0);
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
@@ -209,9 +243,6 @@ __host__ __device__ inline size_t gt_smem(uint32_t dim_stride) {
     return sizeof(uint64_t) * kGtCap + sizeof(uint32_t) * 2048 + sizeof(float) * dim_stride + 64;
 }
 
-__device__ __forceinline__ float gt_err(float qn, float qn2, float xn, float xn2) {
-    return __fadd_ru(__fmul_ru(__fmul_ru(qn, xn), 1.0f / 128.0f), __fmul_ru(__fadd_ru(qn2, xn2), 1.0f / 16384.0f));
-}
 
 // Radix select over keys produced by key_of(row) for rows [0, n): the prefix
 // after `passes` 11/11/10-bit passes of the rank-th smallest key.

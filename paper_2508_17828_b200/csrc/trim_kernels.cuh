@@ -304,10 +304,8 @@ struct KnnParams {
     unsigned long long* skipped; // positions skipped by the list bound (diagnostic)
     unsigned long long* timeline; // nq*kTimeline phase stamps/cycle counts (perf probe only), or null
     // flat scans: tensor-core distance bounds (trim_flat_mma.cuh), or null
-    const float* dap;      // nq x dap_ld: D~[q][row]
+    const __nv_bfloat16* dap; // nq x dap_ld: rigorous lower bound of |q - x|^2 (tf32 D~ - E, rounded down)
     uint64_t dap_ld;
-    const float* xnorm;    // |x| per row, rounded up
-    const float* xnorm2;   // |x|^2 per row
     const uint32_t* plan;  // per-query setup records (trim_knn_setup_kernel), or null: set up in the kernel
     uint32_t topk_off;     // k > 256: byte offset of the SmemTopK keys in dynamic shared memory
 };
@@ -352,9 +350,6 @@ constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per 
 #define TRIM_KRING 6
 #endif
 constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
-#ifndef TRIM_EARLY_FETCH
-#define TRIM_EARLY_FETCH 1 // workers issue chunk 0's loads before building the LUT (setup-record path)
-#endif
 #ifndef TRIM_QUAD_L2
 #define TRIM_QUAD_L2 1     // members' exact L2 by lane quads (euclid_sq_quad), 8 rows per warp pass
 #endif
@@ -376,8 +371,14 @@ __host__ __device__ constexpr uint32_t knn_warps(int mt) {
     return mt > 64 ? TRIM_WIDE_WARPS : (mt == 0 ? kWarps : (mt == 16 ? TRIM_M16_WARPS : TRIM_NARROW_WARPS));
 }
 // CTAs per SM the register budget is set for (24 warps per SM in total)
+#ifndef TRIM_NARROW_MINB
+#define TRIM_NARROW_MINB 0 // > 0: CTAs per SM the register budget of the narrow (m = 48-class) shape targets
+#endif
 __host__ __device__ constexpr uint32_t knn_min_blocks(int mt) {
-    return mt == 0 ? 2u : (24u / knn_warps(mt) > 0 ? 24u / knn_warps(mt) : 1u);
+    return mt == 0 ? 2u
+                   : (TRIM_NARROW_MINB > 0 && mt <= 64 && mt != 16
+                          ? static_cast<uint32_t>(TRIM_NARROW_MINB)
+                          : (24u / knn_warps(mt) > 0 ? 24u / knn_warps(mt) : 1u));
 }
 __host__ __device__ constexpr uint32_t knn_threads(int mt) { return knn_warps(mt) * kWarp; }
 __host__ __device__ constexpr uint32_t knn_chunk(int mt) { return (knn_warps(mt) - 1) * kPerWorker; }
@@ -810,22 +811,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     }
 
     // ---------------------------------------------------- worker warps
-    constexpr bool kEarlyFetch = PRE && TRIM_EARLY_FETCH;
-    // flat scans with tensor-core bounds: |q| and |q|^2 rounded up (for E)
-    float qn = 0.0f, qn2 = 0.0f;
-    if (p.dap) {
-        for (uint32_t i = 0; i < ix.dim; ++i)
-            qn2 = __fadd_ru(qn2, __fmul_ru(qv[i], qv[i]));
-        qn = __fsqrt_ru(qn2);
-    }
     TRIM_TL(const bool wtl = tl && lane == 0; // lane 0 of every worker records (worker 0: slots 10-15)
             unsigned long long wc[6] = {0, 0, 0, 0, 0, 0}; // lut, plan wait, ring wait, adc, l2, total
             unsigned long long wk = wtl ? clock64() : 0;)
-    // the compacted stream length: from the setup record right away (PRE), else
-    // published by the replay warp with the plan
     const uint32_t w = warp - 1;
-    uint32_t bound = kEarlyFetch ? __ldg(rec + 3) : 0u;
-    uint32_t nchunks = (bound + kChunkW - 1) / kChunkW;
+    uint32_t bound = 0, nchunks = 0; // the compacted stream length, published with the plan
     uint32_t li = 0; // list cursor (positions of a lane only increase)
     struct Cand {
         FastCode<M> fc;
@@ -850,6 +840,12 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     ++li;
                 x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
                 x.kind = 2u;
+#ifdef TRIM_DEBUG_BOUNDS
+                if (x.e >= ix.list_offsets[ix.nlist] || li >= p.np) {
+                    printf("DBG fetch q=%u w=%u lane=%u c=%u pp=%u bound=%u li=%u e=%u\n", q, w, lane, c, pp, bound, li, x.e);
+                    __trap();
+                }
+#endif
                 x.fc.load(ix.codes + static_cast<size_t>(x.e) * ix.code_stride, m, lane);
                 x.lx = __ldg(ix.lx + x.e);
             } else { // dead lanes still step through the schedule: valid rows
@@ -857,8 +853,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             }
         }
     };
-    if (kEarlyFetch) // the first chunk's codes in flight while the LUT is built
-        fetch(0, sa);
     build_lut_blocked<M>(ix, qv, lut, tid - kWarp, kThreads - kWarp);
     named_sync(kBarWorkers, kThreads - kWarp); // workers only
     LaneAdc la;
@@ -874,11 +868,9 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         wc[1] = t - wk;
         wk = t;
     })
-    if (!kEarlyFetch) {
-        bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
-        nchunks = (bound + kChunkW - 1) / kChunkW;
-        fetch(0, sa);
-    }
+    bound = *reinterpret_cast<volatile uint32_t*>(s_total2);
+    nchunks = (bound + kChunkW - 1) / kChunkW;
+    fetch(0, sa);
     auto process = [&](uint32_t c, Slot& cur) {
         const uint32_t s = c % kRing;
         TRIM_TL(const unsigned long long k0 = wtl ? clock64() : 0;)
@@ -909,11 +901,15 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         if (keep) { // exact L2 (ivf.hpp:276) of every member the replay may evaluate
             id = __ldg(ix.list_ids + x.e);
             rw = id - ix.id_base;
+#ifdef TRIM_DEBUG_BOUNDS
+            if (rw >= ix.n) {
+                printf("DBG keep q=%u w=%u lane=%u e=%u id=%u kind=%u\n", q, w, lane, x.e, id, x.kind);
+                __trap();
+            }
+#endif
             exact = true;
             if (p.dap) { // d >= D~ - E > T_pub >= T_live: cannot replace the top (ivf.hpp:277)
-                const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(p.xnorm + rw)), 1.0f / 128.0f),
-                                          __fmul_ru(__fadd_ru(qn2, __ldg(p.xnorm2 + rw)), 1.0f / 16384.0f));
-                const float dl = __fsub_rd(__ldg(p.dap + static_cast<size_t>(q) * p.dap_ld + rw), e);
+                const float dl = __bfloat162float(p.dap[static_cast<size_t>(q) * p.dap_ld + rw]);
                 if (dl > ld_volatile(s_T)) {
                     d = dl;
                     exact = false;
@@ -932,6 +928,12 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 mm &= mm - 1;
             const int src = mm ? __ffs(mm) - 1 : -1;
             const uint64_t rs = __shfl_sync(0xffffffffu, rw, src < 0 ? 0 : src);
+#ifdef TRIM_DEBUG_BOUNDS
+            if (src >= 0 && rs >= ix.n) {
+                printf("DBG quad q=%u w=%u lane=%u src=%d rs=%llu em=%x\n", q, w, lane, src, (unsigned long long)rs, em);
+                __trap();
+            }
+#endif
             const float dq = euclid_sq_quad(qv, src < 0 ? nullptr : ix.vectors + rs * ix.dim_stride, ix.dim,
                                             lane & 3u);
             const uint32_t rank = __popc(em & ((1u << lane) - 1u));

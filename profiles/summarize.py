@@ -87,9 +87,11 @@ if __name__ == "__main__":
         if len(sys.argv) > 3:  # workload key for ncu_traffic.json
             tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json")
             t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-            k = [e for e in res if "knn" in e["kernel"] or "range" in e["kernel"]]
+            k = [e for e in res if "knn_kernel" in e["kernel"] or "range" in e["kernel"] or "graph" in e["kernel"]]
             if k and "dram_bytes_total" in k[0]:
-                t[sys.argv[3]] = k[0]["dram_bytes_total"]
+                t[sys.argv[3]] = {"dram_bytes_per_launch": k[0]["dram_bytes_total"], "kernel": k[0]["kernel"],
+                                  "grid": k[0]["grid"], "duration_ns": k[0].get("duration_ns"),
+                                  "source": "profiles/" + os.path.basename(dst)}
                 json.dump(t, open(tpath, "w"), indent=1)
     json.dump(res, open(dst, "w"), indent=1)
     print(json.dumps(res, indent=1)[:3000])

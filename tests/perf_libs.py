@@ -1,10 +1,13 @@
-"""Same-process A/B of library builds (tools_variant.sh): one bench fixture,
+"""Same-process A/B of library builds (tools/variant.sh): one bench fixture,
 every variant's own index + device search (probe + filter) over the whole
 query set on `--streams` streams, CUDA-event timed, repeated interleaved;
 checks that every variant returns identical ids, distance bits and counters.
 Not a test and not the bench.
 
     python tests/perf_libs.py --libs base=paper_2508_17828_b200/libtrim_b200.so,v=...so [--config c2]
+
+A variant may carry environment settings read per call by the library:
+`name=path@TRIM_FLAT_BOUNDS=0;TRIM_LIST_SKIP=1`.
 """
 import argparse
 import ctypes as C
@@ -40,8 +43,15 @@ def main():
     nq, B, k = cfg["nq"], cfg["batch"], cfg["k"]
     dev = torch.device("cuda:0")
     libs = {}
+    envs = {}
     for item in a.libs.split(","):
-        name, path = item.split("=")
+        name, path = item.split("=", 1)
+        path, _, env = path.partition("@")
+        envs[name] = dict(kv.split("=", 1) for kv in env.split(";") if kv)
+        same = [v for v in libs.values() if v[2] == path]
+        if same:  # env-only variant of a library already loaded: share its index
+            libs[name] = same[0]
+            continue
         lib = C.CDLL(os.path.join(ROOT, path) if not os.path.isabs(path) else path, mode=os.RTLD_LOCAL)
         for fn, (res_t, args_t) in L.SIGNATURES.items():
             f = getattr(lib, fn)
@@ -60,12 +70,15 @@ def main():
         h = C.c_void_p()
         rc = lib.trim_index_create(C.byref(d), C.byref(h))
         assert rc == 0, lib.trim_last_error
-        libs[name] = (lib, h)
+        libs[name] = (lib, h, path)
     streams = [torch.cuda.Stream(dev) for _ in range(a.streams)]
     out = {}
     res = {}
     for rep in range(a.reps):
-        for name, (lib, h) in libs.items():
+        for name, (lib, h, _) in libs.items():
+            for kk in {x for e in envs.values() for x in e}:
+                os.environ.pop(kk, None)
+            os.environ.update(envs[name])
             ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
             dd = torch.empty((nq, k), dtype=torch.float32, device=dev)
             ct = torch.zeros((nq, 6), dtype=torch.int64, device=dev)

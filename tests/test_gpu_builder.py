@@ -112,3 +112,57 @@ def test_device_built_index_search_parity(nlist, m):
     got = G.search_baseline_ivfpq_batch(gix, qs, 10, npb, 200)
     np.testing.assert_array_equal(got[0], want[0])
     np.testing.assert_array_equal(got[2][:, :5], want[2])
+
+
+# ------------------------------------------- reference-equal k-means / build
+def _ref_or_skip():
+    from oracle.oracle import RefOracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    return RefOracle()
+
+
+@pytest.mark.parametrize("n,dim,m,c,iters,seed,sample", [
+    (6000, 16, 4, 256, 8, 3, 0),        # default sample (100*c rows, pq.hpp:67-70)
+    (3000, 24, 3, 64, 12, 11, 2000),    # explicit sample, fewer centroids
+    (800, 8, 1, 200, 5, 1, 0),          # one subspace: plain kmeans over all rows
+    (2000, 10, 3, 100, 6, 7, 0),        # uneven split_sub_dims (4, 3, 3)
+])
+def test_pq_train_equals_reference(n, dim, m, c, iters, seed, sample):
+    """pq::train (pq.hpp:65-113) = sampled rows -> per-subspace pq::kmeans
+    (k-means++ with std::mt19937_64, Lloyd, empty-cluster repair): the device
+    codebook equals the reference's bit for bit on the reference's own rows."""
+    torch = _torch()
+    ref = _ref_or_skip()
+    from paper_2508_17828_b200 import builder as B
+    centers = ref.make_normal(12, dim, 5)
+    data = ref.make_blobs(centers, n, 0.4, 6)
+    sub_r, cent_r = ref.pq_train(data, m, c, iters, seed, sample)
+    sub_g, cent_g = B.pq_train(torch.from_numpy(data).cuda(), m, c, iters, seed, sample)
+    np.testing.assert_array_equal(sub_g, sub_r)
+    np.testing.assert_array_equal(cent_g.cpu().numpy().view(np.uint32), cent_r.view(np.uint32))
+
+
+@pytest.mark.parametrize("nlist,coarse_iters,ivf_seed", [(16, 10, 4), (64, 6, 9), (1, 3, 2)])
+def test_build_ivf_equals_reference(nlist, coarse_iters, ivf_seed):
+    """The whole offline pipeline on the device (pq_train -> encode + Γ(l,x)
+    -> coarse k-means on the reference's row sample -> lists) reproduces the
+    reference's IvfIndex (ivf.hpp:112-154) from the same rows: codebook,
+    coarse centroids, list offsets, ids, codes and lx, bit for bit."""
+    torch = _torch()
+    ref = _ref_or_skip()
+    from oracle.oracle import make_reference_index
+    from paper_2508_17828_b200 import builder as B
+    centers = ref.make_normal(20, 32, 21)
+    data = ref.make_blobs(centers, 12000, 0.3, 22)
+    want = make_reference_index(ref, data, m=8, c=256, iters=6, pq_seed=3, nlist=nlist, ivf_seed=ivf_seed,
+                                coarse_iters=coarse_iters)
+    got = B.to_host(B.build_ivf(torch.from_numpy(data).cuda(),
+                                B.BuildParams(m=8, ksub=256, pq_iters=6, pq_seed=3, nlist=nlist, ivf_seed=ivf_seed,
+                                              coarse_iters=coarse_iters)))
+    for f in ("centroids", "coarse", "list_lx"):
+        np.testing.assert_array_equal(np.asarray(getattr(got, f), np.float32).ravel().view(np.uint32),
+                                      np.asarray(getattr(want, f), np.float32).ravel().view(np.uint32), err_msg=f)
+    for f in ("sub_dims", "list_offsets", "list_ids", "list_codes"):
+        np.testing.assert_array_equal(np.asarray(getattr(got, f)).ravel(), np.asarray(getattr(want, f)).ravel(),
+                                      err_msg=f)

@@ -125,7 +125,7 @@ def test_config3_range_vs_reference():
     from paper_2508_17828_b200 import ivf as G
     b = _Built("c3")
     try:
-        radius = bench.calibrate_radius(b.arrays, b.queries, b.cfg)
+        radius = bench.calibrate_radius(b.arrays.vectors, b.queries, b.cfg)
         q = b.q[:1000]
         for g in (0.8, 0.0):
             offs, ids, dist, ct = G.search_trim_ivf_range_batch(b.gix, G.PruningProfile.manual(g), q, radius, 1)

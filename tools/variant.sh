@@ -3,7 +3,7 @@
 # instantiation TU(s) (trim_inst_<M>.o) by extra -D flags:
 #   ./tools_variant.sh NAME "XFLAGS" [Ms...]   -> paper_2508_17828_b200/libtrim_b200_NAME.so
 set -e
-cd "$(dirname "$0")"
+cd "$(dirname "$0")/.."
 NAME=$1; XF=$2; shift 2; MS=${@:-48}
 C=paper_2508_17828_b200/csrc; O=build/obj; V=build/obj_$NAME
 mkdir -p $V

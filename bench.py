@@ -531,7 +531,7 @@ def run_ours(args, cfg):
         out["e2e"] = e2e_sharded(gix, queries, cfg, head, args, world, rank, local)
     else:
         out["e2e"] = e2e(gix, queries, cfg, head, args, world, rank)
-    if mode == "single" and not args.no_group_check:
+    if mode == "single" and not args.no_group_check and cfg["n"] <= 20_000_000:  # (a second copy of the index)
         # the same workload through the multi-device C-ABI path at one device
         # (trim_index_desc devices = [0], TRIM_SHARD_ID): what `--gpus N` runs
         out["multi_device_abi_1gpu"] = group_check(arrays, queries, cfg, head, args)

@@ -68,6 +68,14 @@ void launch_knn(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_
     TRIM_DISPATCH(launch_knn_, ix, p, smem, st);
 }
 
+void launch_knn_seg(const DevIndex& ix, const KnnParams& p, size_t smem, cudaStream_t st) {
+    if (p.k > 256) {
+        CK(launch_knn_seg_0(ix, p, smem, st));
+        return;
+    }
+    TRIM_DISPATCH(launch_knn_seg_, ix, p, smem, st);
+}
+
 void launch_range(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,
                   cudaStream_t st) {
     TRIM_DISPATCH(launch_range_, ix, p, grid, smem, st);
@@ -267,9 +275,13 @@ bool ensure_flat_partition(trim_index* ix) {
         if (hb)
             return false;
     }
+    // blocks: ~4k rows each, up to 16,384 (several blocks per natural cluster of a large
+    // index keep the per-block radius, and so the list-level bound, tight)
     uint32_t nb = 256;
-    while (nb < 4096 && uint64_t(nb) * 2 * 2048 <= n)
+    while (nb < 16384 && uint64_t(nb) * 2 * 2048 <= n)
         nb *= 2;
+    if (const char* e = std::getenv("TRIM_FLAT_PARTITION_BLOCKS"))
+        nb = std::max<uint32_t>(2, static_cast<uint32_t>(std::strtoul(e, nullptr, 10)));
     // k-means on a row sample (the reference's Fisher-Yates sampler)
     const uint64_t ns = std::min<uint64_t>(n, uint64_t(nb) * 40);
     std::vector<uint64_t> rows(ns);
@@ -281,8 +293,45 @@ bool ensure_flat_partition(trim_index* ix) {
                                                                        ns, v.dim, d_sample.as<float>());
     CK(cudaStreamSynchronize(st));
     float* cent = ix->alloc<float>(static_cast<size_t>(nb) * v.dim);
-    if (int rc = trim_kmeans_device(d_sample.as<float>(), ns, v.dim, nb, 6, 0x5EEDull, cent, ix->device))
-        throw std::runtime_error(trim_last_error());
+    if (nb <= 4096) {
+        if (int rc = trim_kmeans_device(d_sample.as<float>(), ns, v.dim, nb, 6, 0x5EEDull, cent, ix->device))
+            throw std::runtime_error(trim_last_error());
+    } else {
+        // two levels (k-means++ seeding scans the whole sample once per centroid): nb / 256
+        // top clusters, then up to 256 blocks inside each from its own sample rows
+        const uint32_t k1 = nb / 256;
+        DevBuf c1(sizeof(float) * k1 * v.dim, st), a1(sizeof(uint32_t) * ns, st), d1(sizeof(float) * ns, st),
+            order1(sizeof(uint32_t) * ns, st), offs1(sizeof(uint64_t) * (k1 + 1), st), sub(sizeof(float) * ns * v.dim, st);
+        if (int rc = trim_kmeans_device(d_sample.as<float>(), ns, v.dim, k1, 6, 0x5EEDull, c1.as<float>(), ix->device))
+            throw std::runtime_error(trim_last_error());
+        if (int rc = trim_assign_device(d_sample.as<float>(), ns, v.dim, c1.as<float>(), k1, a1.as<uint32_t>(),
+                                        d1.as<float>(), ix->device, st))
+            throw std::runtime_error(trim_last_error());
+        if (int rc = trim_ivf_lists_device(a1.as<uint32_t>(), ns, k1, offs1.as<uint64_t>(), order1.as<uint32_t>(),
+                                           ix->device, st))
+            throw std::runtime_error(trim_last_error());
+        std::vector<uint64_t> ho(k1 + 1);
+        CK(cudaMemcpyAsync(ho.data(), offs1.p, sizeof(uint64_t) * (k1 + 1), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        trim_gather_rows32_kernel<<<static_cast<unsigned>(ns), 128, 0, st>>>(d_sample.as<float>(), v.dim,
+                                                                            order1.as<uint32_t>(), ns, v.dim, sub.as<float>());
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        uint32_t made = 0;
+        for (uint32_t c = 0; c < k1; ++c) {
+            const uint64_t cnt = ho[c + 1] - ho[c];
+            const uint32_t k2 = static_cast<uint32_t>(std::min<uint64_t>(256, cnt / 8));
+            if (k2 == 0)
+                continue;
+            if (int rc = trim_kmeans_device(sub.as<float>() + ho[c] * v.dim, cnt, v.dim, k2, 6, 0x5EEDull + c + 1,
+                                            cent + static_cast<size_t>(made) * v.dim, ix->device))
+                throw std::runtime_error(trim_last_error());
+            made += k2;
+        }
+        if (made < 2)
+            return false;
+        nb = made;
+    }
     DevIndex a = v;
     a.nlist = nb;
     a.coarse = cent; // dim_stride == dim
@@ -295,8 +344,9 @@ bool ensure_flat_partition(trim_index* ix) {
     trim_coarse_norm_kernel<<<(nb + kThreads - 1) / kThreads, kThreads, 0, st>>>(a, ix->part_cn2, ix->part_cn);
     CK(cudaGetLastError());
     // assignment: argmin of the tf32 distance bounds, row chunks of 1M
-    DevBuf assign(sizeof(uint32_t) * n, st);
-    const uint64_t ch = 1u << 20, ld = mma_ld(nb);
+    ix->part_assign = ix->alloc<uint32_t>(n); // kept: the segmented kNN layout regroups by it
+    const uint64_t ld = mma_ld(nb); // D~ of a row chunk: at most 2 GB
+    const uint64_t ch = std::max<uint64_t>(kMmaM, std::min<uint64_t>(1u << 20, (1ull << 29) / ld / kMmaM * kMmaM));
     DevBuf approx(sizeof(float) * ch * ld, st);
     CK(cudaFuncSetAttribute(trim_probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(probe_mma_smem(K))));
@@ -306,13 +356,13 @@ bool ensure_flat_partition(trim_index* ix) {
         trim_probe_mma_kernel<<<grid, kMmaThreads, probe_mma_smem(K), st>>>(
             v.vectors + c0 * v.dim_stride, nc, v.dim_stride, K, ix->part_tiles, ix->part_cn2, nb, approx.as<float>());
         trim_argmin_kernel<<<static_cast<unsigned>((nc + 7) / 8), 256, 0, st>>>(approx.as<float>(), nc, nb, ld,
-                                                                                assign.as<uint32_t>() + c0);
+                                                                                ix->part_assign + c0);
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(st));
     uint64_t* offs = ix->alloc<uint64_t>(nb + 1);
     DevBuf order(sizeof(uint32_t) * n, st);
-    if (int rc = trim_ivf_lists_device(assign.as<uint32_t>(), n, nb, offs, order.as<uint32_t>(), ix->device, st))
+    if (int rc = trim_ivf_lists_device(ix->part_assign, n, nb, offs, order.as<uint32_t>(), ix->device, st))
         throw std::runtime_error(trim_last_error());
     uint8_t* codes = ix->alloc<uint8_t>(n * v.code_stride);
     float* lx = ix->alloc<float>(n);
@@ -334,6 +384,71 @@ bool ensure_flat_partition(trim_index* ix) {
     CK(cudaStreamSynchronize(st));
     ix->part = a;
     ix->part_nb = nb;
+    return true;
+}
+
+// TRIM_FLAT_SEGMENTS=0 keeps flat kNN scans in row order (A/B; results and
+// counters are identical either way).
+bool flat_segments_enabled() {
+    const char* e = std::getenv("TRIM_FLAT_SEGMENTS");
+    return !(e && e[0] == '0');
+}
+
+// Segmented layout for flat kNN (trim_knn_seg_plan_kernel): on top of the block
+// partition, rows n0.. regrouped by (segment of seg_len consecutive ids, block),
+// ascending ids inside. n0 rows are scanned in order first (their top-k gives
+// the threshold the blocks are pruned against); seg_len = rows-per-block-run x
+// blocks, so a kept block contributes about one warp-chunk of rows per segment.
+bool ensure_flat_segments(trim_index* ix) {
+    if (!flat_segments_enabled() || !ensure_flat_partition(ix))
+        return false;
+    std::lock_guard<std::mutex> lk(ix->seg_mu);
+    if (ix->seg_tried)
+        return ix->seg_ok;
+    ix->seg_tried = true;
+    const DevIndex& v = ix->dev;
+    const uint64_t n = ix->total;
+    const uint32_t nb = ix->part_nb;
+    uint64_t rpb = 256, n0 = std::max<uint64_t>(uint64_t(std::min<uint32_t>(nb, 4096)) * 32, 16384);
+    if (const char* e = std::getenv("TRIM_SEG_ROWS_PER_BLOCK"))
+        rpb = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    if (const char* e = std::getenv("TRIM_SEG_N0"))
+        n0 = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+    n0 = std::min<uint64_t>(n0, n / 4);
+    const uint64_t seg_len = rpb * nb, rest = n - n0;
+    const uint64_t nseg = (rest + seg_len - 1) / seg_len;
+    if (n0 == 0 || nseg == 0 || nseg * nb >= (1ull << 31) || n >= (1ull << 32))
+        return false;
+    cudaStream_t st = nullptr;
+    DevBuf keys(sizeof(uint32_t) * rest, st), order(sizeof(uint32_t) * rest, st);
+    trim_seg_key_kernel<<<static_cast<unsigned>((rest + 255) / 256), 256, 0, st>>>(ix->part_assign + n0, rest, seg_len, nb,
+                                                                                  keys.as<uint32_t>());
+    CK(cudaGetLastError());
+    ix->seg_off = ix->alloc<uint64_t>(nseg * nb + 1);
+    if (int rc = trim_ivf_lists_device(keys.as<uint32_t>(), rest, static_cast<uint32_t>(nseg * nb), ix->seg_off,
+                                       order.as<uint32_t>(), ix->device, st))
+        throw std::runtime_error(trim_last_error());
+    uint8_t* codes = ix->alloc<uint8_t>(rest * v.code_stride);
+    float* lx = ix->alloc<float>(rest);
+    uint32_t* ids = ix->alloc<uint32_t>(rest);
+    trim_partition_gather_kernel<<<static_cast<unsigned>((rest + 255) / 256), 256, 0, st>>>(
+        order.as<uint32_t>(), rest, v.codes + n0 * v.code_stride, v.code_stride, v.lx + n0, v.list_ids + n0, codes, lx,
+        ids);
+    CK(cudaGetLastError());
+    uint64_t* offs_a = ix->alloc<uint64_t>(2);
+    const uint64_t ha[2] = {0, n0};
+    CK(cudaMemcpyAsync(offs_a, ha, sizeof ha, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    ix->seg = v;
+    ix->seg.codes = codes;
+    ix->seg.lx = lx;
+    ix->seg.list_ids = ids;
+    ix->seg_head = v;
+    ix->seg_head.list_offsets = offs_a;
+    ix->seg_n0 = n0;
+    ix->seg_len = seg_len;
+    ix->seg_nseg = static_cast<uint32_t>(nseg);
+    ix->seg_ok = true;
     return true;
 }
 
@@ -376,7 +491,8 @@ void range_launch(const trim_index* ix, const float* d_q, uint64_t nq, const flo
     p.adc_eps = filter_eps(v.m);
     p.omg_hi = omg_round_up(gamma);
     p.cap = cap;
-    if (!d_probe && ensure_flat_partition(const_cast<trim_index*>(ix))) {
+    if (!d_probe && ensure_flat_partition(const_cast<trim_index*>(ix)) &&
+        range_smem_bytes(dispatch_m(ix->part), ix->part.m, ix->part.dim_stride, ix->part_nb) <= kSmemLimit) {
         // flat scan over the block partition: blocks whose bound proves est > r^2 are skipped
         const DevIndex& a = ix->part;
         const uint32_t nb = ix->part_nb, K = mma_k(v.dim);
@@ -398,8 +514,6 @@ void range_launch(const trim_index* ix, const float* d_q, uint64_t nq, const flo
             kest, kept.as<uint32_t>(), nkept.as<uint32_t>(), ix->d_skipped);
         CK(cudaGetLastError());
         const size_t smem = range_smem_bytes(dispatch_m(a), a.m, a.dim_stride, nb);
-        if (smem > kSmemLimit)
-            throw std::runtime_error("flat range partition: per-query state exceeds shared memory");
         p.np = nb;
         p.np_q = nkept.as<uint32_t>();
         p.eval_override = ix->total;
@@ -513,6 +627,144 @@ void launch_flat_dist(const float4* qtiles, const float* qn2, uint64_t nq, uint6
     }
 }
 
+// Shared memory of the kNN filter kernel for `np` stream runs (+ the SmemTopK keys for k > 256).
+size_t knn_smem_for(const trim_index* ix, uint32_t k, uint32_t np, uint32_t& topk_off) {
+    size_t smem = knn_smem_bytes(k > 256 ? 0 : dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
+    topk_off = 0;
+    if (k > 256) { // SmemTopK keys after the kernel's own layout
+        topk_off = static_cast<uint32_t>((smem + 15) & ~size_t(15));
+        smem = topk_off + sizeof(unsigned long long) * smem_topk_slots(k);
+    }
+    return smem;
+}
+
+// Segmented flat kNN (ensure_flat_segments) for one batch: the first n0 rows in
+// order, the block bounds on tcgen05, the per-query plan, then the block-stream
+// kernel and — for the queries whose plan does not fit — the in-order kernel
+// over rows [n0, n). `pb` carries the batch's queries, outputs and dap.
+constexpr uint32_t kSegRuns = 384;      // stream runs per query of the small launch (12 B of shared memory each)
+constexpr uint32_t kSegRunsLarge = 2048; // ... of the large launch (and of the record layout)
+constexpr uint32_t kSegGroupWords = 128; // 4,096 chunks
+constexpr uint32_t kSegPoolCap = 16384;  // rows of one segment's kept blocks
+bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
+    const DevIndex& v = ix->dev;
+    const uint32_t k = pb.k, nb = ix->part_nb, K = mma_k(v.dim);
+    const uint64_t nq = pb.nq;
+    uint32_t off_a = 0, off_b = 0, off_c = 0;
+    uint32_t runs_small = kSegRuns;
+    if (const char* e = std::getenv("TRIM_SEG_SMALL_RUNS")) // tests: push plans into the large launch
+        runs_small = std::max<uint32_t>(1, std::min<uint32_t>(kSegRuns, std::strtoul(e, nullptr, 10)));
+    const size_t smem_a = knn_smem_for(ix, k, 1, off_a), smem_b = knn_smem_for(ix, k, runs_small, off_b),
+                 smem_c = knn_smem_for(ix, k, kSegRunsLarge, off_c);
+    if (smem_c > kSmemLimit)
+        return false;
+    // the first n0 rows, in order
+    DevBuf ids_a(sizeof(uint32_t) * nq * k, st), dist_a(sizeof(float) * nq * k, st),
+        ct_a(sizeof(unsigned long long) * nq * 6, st);
+    KnnParams pa = pb;
+    pa.np = 1;
+    pa.probe = nullptr;
+    pa.plan = nullptr;
+    pa.ids_out = ids_a.as<uint32_t>();
+    pa.dist_out = dist_a.as<float>();
+    pa.counters = ct_a.as<unsigned long long>();
+    pa.topk_off = off_a;
+    pa.timeline = nullptr;
+    launch_knn(ix->seg_head, pa, smem_a, st);
+    // |q - c_b|^2 bounds to the block centroids
+    const uint32_t ntiles = (nb + kMmaN - 1) / kMmaN;
+    DevBuf approx(sizeof(float) * nq * mma_ld(nb), st);
+    CK(cudaFuncSetAttribute(trim_probe_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(probe_mma_smem(K))));
+    trim_probe_mma_kernel<<<dim3(static_cast<unsigned>((nq + kMmaM - 1) / kMmaM),
+                                 (ntiles + kMmaTilesPerCta - 1) / kMmaTilesPerCta),
+                            kMmaThreads, probe_mma_smem(K), st>>>(pb.queries, nq, v.dim_stride, K, ix->part_tiles,
+                                                                  ix->part_cn2, nb, approx.as<float>());
+    CK(cudaGetLastError());
+    const KnnPlanLayout lo = KnnPlanLayout::of(kSegRunsLarge, k, kSegGroupWords);
+    DevBuf recs(sizeof(uint32_t) * lo.words * nq, st);
+    CK(cudaMemsetAsync(recs.p, 0, sizeof(uint32_t) * lo.words * nq, st));
+    SegPlanParams sp{};
+    sp.queries = pb.queries;
+    sp.nq = nq;
+    sp.k = k;
+    sp.np = kSegRunsLarge;
+    sp.np_small = runs_small;
+    sp.gwords = kSegGroupWords;
+    sp.pool_cap = kSegPoolCap;
+    sp.chunk = knn_chunk(k > 256 ? 0 : dispatch_m(v));
+    sp.n = ix->total;
+    sp.n0 = ix->seg_n0;
+    sp.seg_len = ix->seg_len;
+    sp.nseg = ix->seg_nseg;
+    sp.seg_off = ix->seg_off;
+    sp.approx = approx.as<float>();
+    sp.cn2 = ix->part_cn2;
+    sp.cn = ix->part_cn;
+    sp.ids_a = ids_a.as<uint32_t>();
+    sp.dist_a = dist_a.as<float>();
+    sp.ct_a = ct_a.as<unsigned long long>();
+    sp.omg_lo = pb.omg_lo;
+    sp.omg_hi = pb.omg_hi;
+    sp.kq1 = pb.kq1;
+    sp.kq2 = pb.kq2;
+    sp.kest = pb.kest;
+    sp.recs = recs.as<uint32_t>();
+    sp.skipped = pb.skip_lists ? pb.skipped : nullptr;
+    {
+        const char* e = std::getenv("TRIM_SEG_FORCE_PLAIN"); // tests: every query takes the in-order resume
+        sp.force_plain = (e && e[0] == '1') || !pb.skip_lists ? 1u : 0u;
+    }
+    DevBuf dbg;
+    const bool debug = std::getenv("TRIM_SEG_DEBUG") != nullptr;
+    if (debug) {
+        dbg = DevBuf(sizeof(uint32_t) * 4 * nq, st);
+        sp.dbg = dbg.as<uint32_t>();
+    }
+    trim_knn_seg_plan_kernel<<<static_cast<unsigned>(nq), kThreads, 0, st>>>(ix->part, sp);
+    CK(cudaGetLastError());
+    if (debug) { // plan statistics of the batch (synchronises)
+        std::vector<uint32_t> h(4 * nq);
+        std::vector<float> ta(nq * k);
+        CK(cudaMemcpyAsync(h.data(), dbg.p, sizeof(uint32_t) * 4 * nq, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ta.data(), dist_a.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        uint64_t plain = 0, kept = 0, runs = 0, chunks = 0, kmax = 0;
+        double tsum = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            kept += h[4 * i];
+            kmax = std::max<uint64_t>(kmax, h[4 * i]);
+            plain += h[4 * i + 1];
+            runs += h[4 * i + 2];
+            chunks += h[4 * i + 3];
+            tsum += ta[i * k + k - 1];
+        }
+        std::fprintf(stderr,
+                     "[trim seg] nq=%llu nb=%u n0=%llu seg_len=%llu nseg=%u: plain=%llu kept/q=%.1f (max %llu) "
+                     "runs/q=%.1f chunks/q=%.1f mean T_A=%.3f\n",
+                     (unsigned long long)nq, nb, (unsigned long long)ix->seg_n0, (unsigned long long)ix->seg_len,
+                     ix->seg_nseg, (unsigned long long)plain, double(kept) / nq, (unsigned long long)kmax,
+                     double(runs) / nq, double(chunks) / nq, tsum / nq);
+    }
+    DevBuf pool(sizeof(uint32_t) * 5 * kSegPoolCap * nq, st);
+    pb.plan = recs.as<uint32_t>();
+    pb.np_rec = kSegRunsLarge;
+    pb.probe = nullptr;
+    pb.gwords = kSegGroupWords;
+    pb.pool = pool.as<uint32_t>();
+    pb.pool_cap = kSegPoolCap;
+    pb.np = runs_small;
+    pb.topk_off = off_b;
+    launch_knn(v, pb, smem_b, st); // records of mode 0: in order over the original arrays (the long ones first)
+    pb.seg_mode = 1; // records of mode 1
+    launch_knn_seg(ix->seg, pb, smem_b, st);
+    pb.np = kSegRunsLarge; // records of mode 2
+    pb.seg_mode = 2;
+    pb.topk_off = off_c;
+    launch_knn_seg(ix->seg, pb, smem_c, st);
+    return true;
+}
+
 // kNN filter launch over padded device queries and precomputed probe lists
 // (d_probe null => nlist == 1, the single list 0).
 int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, uint32_t np,
@@ -520,6 +772,8 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
                unsigned long long* d_ct, uint32_t* d_status, cudaStream_t st) {
     if (nq == 0)
         return TRIM_OK;
+    if (ix->dev.nlist == 1 && np == 1)
+        d_probe = nullptr; // a flat index: the one list, whatever the caller's probe array says
     size_t smem = knn_smem_bytes(k > 256 ? 0 : dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, np);
     uint32_t topk_off = 0;
     if (k > 256) { // SmemTopK keys after the kernel's own layout
@@ -571,6 +825,11 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     uint64_t slice = 1u << 30;
     if (flat_bounds)
         slice = std::max<uint64_t>(kMmaM, (8ull << 30) / (ld * 2) / kMmaM * kMmaM);
+    // flat scans of partitioned indexes: segmented block stream (knn_seg_batch)
+    const bool seg = ix->dev.nlist == 1 && !d_probe && np == 1 && ensure_flat_segments(const_cast<trim_index*>(ix)) &&
+                     uint64_t(k) * 4 <= ix->seg_n0;
+    if (seg)
+        slice = std::min<uint64_t>(slice, 1024); // the member pools: 320 KB per query
     for (uint64_t b = 0; b < nq; b += slice) {
         KnnParams pb = p;
         pb.nq = std::min<uint64_t>(slice, nq - b);
@@ -613,6 +872,8 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
             CK(cudaGetLastError());
             pb.plan = recs.as<uint32_t>();
         }
+        if (seg && knn_seg_batch(ix, pb, st))
+            continue;
         launch_knn(ix->dev, pb, smem, st);
     }
     return TRIM_OK;

@@ -197,6 +197,16 @@ struct trim_index {
     float4* part_tiles = nullptr;
     float* part_cn2 = nullptr;
     float* part_cn = nullptr;
+    uint32_t* part_assign = nullptr; // block of every row
+    // flat kNN: rows n0.. regrouped by (segment of seg_len consecutive ids, block) for the
+    // segmented block scan (ensure_flat_segments), built on first use
+    std::mutex seg_mu;
+    bool seg_tried = false, seg_ok = false;
+    uint64_t seg_n0 = 0, seg_len = 0;
+    uint32_t seg_nseg = 0;
+    uint64_t* seg_off = nullptr;  // nseg * part_nb + 1
+    trimgpu::DevIndex seg{};      // dev with the regrouped codes / lx / ids
+    trimgpu::DevIndex seg_head{}; // dev restricted to rows [0, n0)
     uint64_t bytes = 0;
     std::vector<void*> allocs;
     // multi-device layouts (trim_index_desc.ndevices > 0, trim_multi.cu): this

@@ -64,6 +64,24 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
     return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, false>, grid, smem, st, ix, p);
 }
 
+// segmented flat scans: the SEG instantiation (records of mode 1; the others exit at once)
+cudaError_t TRIM_CAT(launch_knn_seg_, TRIM_M)(const DevIndex& ix, const KnnParams& p, size_t smem,
+                                              cudaStream_t st) {
+    const uint32_t S = (p.k + 31) / 32;
+    const dim3 grid(static_cast<unsigned>(p.nq));
+#if TRIM_M == 0
+    if (S > 8)
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, true, true>, grid, smem, st, ix, p);
+#endif
+    if (S <= 1)
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true, true>, grid, smem, st, ix, p);
+    if (S <= 2)
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true, true>, grid, smem, st, ix, p);
+    if (S <= 4)
+        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true, true>, grid, smem, st, ix, p);
+    return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true, true>, grid, smem, st, ix, p);
+}
+
 cudaError_t TRIM_CAT(launch_range_, TRIM_M)(const DevIndex& ix, const RangeParams& p, dim3 grid,
                                             size_t smem, cudaStream_t st) {
     return launch(trim_range_kernel<TRIM_M, TRIM_KS>, grid, smem, st, ix, p);

@@ -308,6 +308,13 @@ struct KnnParams {
     uint64_t dap_ld;
     const uint32_t* plan;  // per-query setup records (trim_knn_setup_kernel), or null: set up in the kernel
     uint32_t topk_off;     // k > 256: byte offset of the SmemTopK keys in dynamic shared memory
+    // segmented flat scans (trim_knn_seg_plan_kernel): group bitset words per record,
+    // and the replay warp's per-query member pool in global memory (5 x pool_cap words)
+    uint32_t gwords;
+    uint32_t pool_cap;
+    uint32_t* pool;
+    uint32_t np_rec;   // runs the record layout is sized for (0: np)
+    uint32_t seg_mode; // SEG kernel: the record mode this launch serves (1: <= np runs of a small CTA, 2: large)
 };
 
 // Per-query setup record written by trim_knn_setup_kernel (u32 words): the
@@ -315,14 +322,18 @@ struct KnnParams {
 // the compacted stream after the list-level plan — what the replay warp of
 // trim_knn_kernel otherwise computes itself before the workers may start.
 struct KnnPlanLayout {
-    uint32_t cum, base, sd, sid, words;
-    __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k) {
+    uint32_t cum, base, sd, sid, grp, words;
+    // header: [0] total [1] nseed [2] nk [3] total2 [4] T0 bits [5] dc so far (the seeds, or
+    // everything before a resumed scan) [6] entries evaluated unconditionally (edc = evaluated
+    // - this) [7] mode: 0 = stream in order, 1 = segmented block stream (SEG kernel)
+    __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k, uint32_t gwords = 0) {
         KnnPlanLayout o;
-        o.cum = 8;                          // [0] total [1] nseed [2] nk [3] total2 [4] T0 bits
+        o.cum = 8;
         o.base = (o.cum + np + 1 + 1) & ~1u; // u64-aligned
         o.sd = o.base + 2 * np;
         o.sid = o.sd + k;
-        o.words = (o.sid + k + 1) & ~1u;
+        o.grp = o.sid + k;                   // gwords: bit c = chunk c ends a replay group
+        o.words = (o.grp + gwords + 1) & ~1u;
         return o;
     }
 };
@@ -506,9 +517,24 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // --------------------------------------------------------------------------
 // PRE: the seeds and the plan come from trim_knn_setup_kernel's record
 // (p.plan); the in-kernel setup code is compiled out (fewer live registers).
-template <int M, int KS, int S, bool PRE>
+//
+// SEG (with PRE): a segmented block stream over a flat index
+// (trim_knn_seg_plan_kernel). `ix` holds the rows regrouped by (segment of
+// consecutive ids, block), the record resumes the scan after the first n0 rows
+// (top-k, counters) and lists, per segment, the runs of the blocks the
+// list-level bound could not prune (run length in the high word of base[],
+// each segment padded to whole chunks). The blocks of a segment interleave in
+// id order, so the replay warp gathers a segment's members (a replay group: the
+// chunks up to the one whose group bit is set) in a per-query pool and replays
+// them in ascending-id order: members below the smallest id that can change the
+// top-k or needs the reference-order ADC are order-free under the current
+// threshold, that one is handled alone, and so on — the reference's decisions.
+// A CTA whose record is of the other mode exits at once (both kernels are
+// launched over the batch).
+template <int M, int KS, int S, bool PRE, bool SEG = false>
 __global__ void __launch_bounds__(knn_threads(M), knn_min_blocks(M))
 trim_knn_kernel(DevIndex ix, KnnParams p) {
+    static_assert(PRE || !SEG, "segmented streams come from a plan record");
     // this instantiation's CTA shape (knn_warps): warp 0 replays, the rest filter
     constexpr uint32_t kThreads = knn_threads(M);
     constexpr uint32_t kWorkers = knn_warps(M) - 1;
@@ -567,10 +593,14 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     __syncthreads();
     // the stream (probe order, ascending ids) — from the setup record when
     // trim_knn_setup_kernel ran, else built here
-    const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words : nullptr;
+    const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords).words : nullptr;
+    if constexpr (PRE) {
+        if (__ldg(rec + 7) != (SEG ? p.seg_mode : 0u)) // another launch's query
+            return;
+    }
     uint32_t total;
     if constexpr (PRE) {
-        const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+        const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
         const uint32_t nk = __ldg(rec + 2);
         for (uint32_t i = tid; i <= nk; i += kThreads)
             st.cum[i] = __ldg(rec + lo.cum + i);
@@ -595,7 +625,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         topk.init(p.k, smem + p.topk_off);
         uint32_t carry = 0, nk = 0;
         if constexpr (PRE) { // seeds and plan from trim_knn_setup_kernel
-            const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+            const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
             for (uint32_t j = 0; j < nseed; ++j)
                 topk.offer(__uint_as_float(__ldg(rec + lo.sd + j)), __ldg(rec + lo.sid + j));
             nk = __ldg(rec + 2);
@@ -680,7 +710,8 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         __syncwarp();
         named_arrive(kBarPlan, kThreads);
 
-        uint64_t dc = nseed;
+        uint64_t dc = PRE ? __ldg(rec + 5) : nseed;
+        const uint32_t nuncond = PRE ? __ldg(rec + 6) : nseed;
         TRIM_TL(uint32_t members = 0;)
         // The reference-order est of a member whose interval straddles the live
         // threshold (rare): its compacted position from the bin's lane mask, its
@@ -702,6 +733,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             return relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
         };
         TRIM_TL(unsigned long long cyc_wait = 0, cyc_busy = 0;)
+        // SEG: the group's member pool (id, lo, hi, d, entry: pool_cap words each)
+        [[maybe_unused]] uint32_t pn = 0;
+        [[maybe_unused]] const uint32_t pcap = p.pool_cap;
+        [[maybe_unused]] uint32_t* pool = SEG ? p.pool + static_cast<size_t>(q) * 5u * p.pool_cap : nullptr;
+        [[maybe_unused]] const uint32_t glo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords).grp;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t s = c % kRing;
             TRIM_TL(const unsigned long long k0 = tl ? clock64() : 0;)
@@ -719,6 +755,96 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     inc += t;
             }
             const uint32_t nmem = __shfl_sync(0xffffffffu, inc, kWorkers - 1);
+            if constexpr (SEG) {
+                // the chunk's members join the group's pool (with their entry index, recovered
+                // from the bin's lane mask and cum/base); the ring slot is free at once
+                for (uint32_t base = 0; base < nmem; base += kWarp) {
+                    const uint32_t i = base + lane;
+                    uint32_t w = 0, before = 0;
+#pragma unroll
+                    for (uint32_t x = 0; x < kWorkers; ++x) {
+                        const uint32_t ix_ = __shfl_sync(0xffffffffu, inc, x);
+                        if (i >= ix_) {
+                            w = x + 1;
+                            before = ix_;
+                        }
+                    }
+                    if (i < nmem) {
+                        const uint32_t r = i - before;
+                        const uint32_t g = s * kChunkW + w * kPerWorker + r;
+                        const uint32_t pos = __fns(bin_mask[s * kWorkers + w], 0, static_cast<int>(r) + 1);
+                        const uint32_t pp = c * kChunkW + w * kPerWorker + pos;
+                        uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
+                        while (hi - lo > 1) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (st.cum[mid] <= pp)
+                                lo = mid;
+                            else
+                                hi = mid;
+                        }
+                        const uint32_t j = pn + i; // <= pool_cap: the plan bounds a group's rows
+                        __stcg(pool + j, s_e[g]);
+                        __stcg(pool + pcap + j, __float_as_uint(s_lo[g]));
+                        __stcg(pool + 2 * pcap + j, __float_as_uint(s_hi[g]));
+                        __stcg(pool + 3 * pcap + j, __float_as_uint(s_d[g]));
+                        __stcg(pool + 4 * pcap + j, static_cast<uint32_t>(st.base[lo]) + (pp - st.cum[lo]));
+                    }
+                }
+                TRIM_TL(members += nmem;)
+                pn += nmem;
+                __syncwarp();
+                mbar_arrive(empty + s);
+                if (!((__ldg(rec + glo + (c >> 5)) >> (c & 31u)) & 1u))
+                    continue;
+                // replay the group in ascending-id order
+                uint64_t lb = 0; // ids below lb are decided
+                for (;;) {
+                    const float T = topk.wd;
+                    const uint32_t Tid = topk.wid;
+                    uint32_t hid = kInvalidId, hidx = 0; // my smallest member that may change T
+                    for (uint32_t i = lane; i < pn; i += kWarp) {
+                        const uint32_t id = __ldcg(pool + i);
+                        if (id < lb || id >= hid)
+                            continue;
+                        if (!(__uint_as_float(__ldcg(pool + pcap + i)) < T))
+                            continue; // pruned under T (and under any later, smaller threshold)
+                        const float hi = __uint_as_float(__ldcg(pool + 2 * pcap + i));
+                        const float dd = __uint_as_float(__ldcg(pool + 3 * pcap + i));
+                        if (!(hi < T) || scored_less(dd, id, T, Tid)) {
+                            hid = id;
+                            hidx = i;
+                        }
+                    }
+                    const uint32_t f = __reduce_min_sync(0xffffffffu, hid);
+                    uint32_t cnt = 0; // members in [lb, f): evaluated, none replaces (ivf.hpp:275-282)
+                    for (uint32_t i = lane; i < pn; i += kWarp) {
+                        const uint32_t id = __ldcg(pool + i);
+                        if (id >= lb && id < f && __uint_as_float(__ldcg(pool + pcap + i)) < T)
+                            ++cnt;
+                    }
+                    dc += __reduce_add_sync(0xffffffffu, cnt);
+                    if (f == kInvalidId)
+                        break;
+                    const uint32_t src = __ffs(__ballot_sync(0xffffffffu, hid == f)) - 1;
+                    const uint32_t fi = __shfl_sync(0xffffffffu, hidx, src);
+                    bool ev = true;
+                    if (!(__uint_as_float(__ldcg(pool + 2 * pcap + fi)) < T)) { // straddles: reference-order est
+                        const uint32_t e = __ldcg(pool + 4 * pcap + fi);
+                        const float a = adc_serial<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m);
+                        ev = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma) < T;
+                    }
+                    if (ev) {
+                        ++dc;
+                        topk.offer(__uint_as_float(__ldcg(pool + 3 * pcap + fi)), f);
+                    }
+                    lb = static_cast<uint64_t>(f) + 1;
+                }
+                pn = 0;
+                if (lane == 0)
+                    *reinterpret_cast<volatile float*>(s_T) = topk.wd;
+                __syncwarp();
+                continue;
+            }
             for (uint32_t base = 0; base < nmem; base += kWarp) {
                 const uint32_t i = base + lane;
                 const uint32_t cnt = min(static_cast<uint32_t>(kWarp), nmem - base);
@@ -774,7 +900,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                 *reinterpret_cast<volatile float*>(s_T) = topk.wd;
             __syncwarp();
             mbar_arrive(empty + s);
-            if (c == 0 && nchunks > 1) // the workers filter chunk 1 on against this threshold
+            if (!SEG && c == 0 && nchunks > 1) // the workers filter chunk 1 on against this threshold
                 named_arrive(kBarChunk0, kThreads);
             TRIM_TL(if (tl) {
                 cyc_wait += k1 - k0;
@@ -801,7 +927,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             unsigned long long* cc = p.counters + static_cast<size_t>(q) * 6;
             const uint64_t evaluated = total;
             cc[0] = dc;                // dc
-            cc[1] = evaluated - nseed; // edc
+            cc[1] = evaluated - nuncond; // edc
             cc[2] = evaluated - dc;    // pruned (including skipped lists)
             cc[3] = evaluated;         // evaluated
             cc[4] = 0;                 // hops
@@ -838,7 +964,17 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             if (c < nchunks && pp < bound) {
                 while (st.cum[li + 1] <= pp)
                     ++li;
-                x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
+                if constexpr (SEG) { // positions past the run's length pad the segment to whole chunks
+                    const uint64_t b = st.base[li];
+                    const uint32_t o = pp - st.cum[li];
+                    if (o >= static_cast<uint32_t>(b >> 32)) {
+                        x.fc.zero(m);
+                        continue;
+                    }
+                    x.e = static_cast<uint32_t>(b) + o;
+                } else {
+                    x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
+                }
                 x.kind = 2u;
 #ifdef TRIM_DEBUG_BOUNDS
                 if (x.e >= ix.list_offsets[ix.nlist] || li >= p.np) {
@@ -876,7 +1012,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         TRIM_TL(const unsigned long long k0 = wtl ? clock64() : 0;)
         if (c >= kRing)
             mbar_wait(empty + s, ((c / kRing) - 1) & 1u);
-        if (c == 1) // filter the rest against the threshold after chunk 0, not the seeds'
+        if (!SEG && c == 1) // filter the rest against the threshold after chunk 0, not the seeds'
             named_sync(kBarChunk0, kThreads);
         const float T = ld_volatile(s_T);
         TRIM_TL(const unsigned long long k1 = wtl ? clock64() : 0;)
@@ -1313,7 +1449,7 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
     __syncwarp();
     const uint32_t total = carry;
     const uint32_t nseed = min(p.k, total);
-    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
+    const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
     uint32_t* rec = recs + static_cast<size_t>(q) * lo.words;
     // seeds (ivf.hpp:264-271): exact distances in stream order; T0 = max_dis
     // after them (the largest (d, id), or +inf when fewer than k)
@@ -1382,9 +1518,241 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
         rec[2] = nk;
         rec[3] = kept;
         rec[4] = __float_as_uint(T0);
+        rec[5] = nseed; // dc so far
+        rec[6] = nseed; // evaluated unconditionally
+        rec[7] = 0;     // stream in order
         const uint32_t rest = total - nseed;
         if (p.skipped && rest != kept)
             atomicAdd(p.skipped, static_cast<unsigned long long>(rest - kept));
+    }
+}
+
+// --------------------------------------------------------------------------
+// trim_knn_seg_plan_kernel — the plan of a segmented flat kNN scan
+// (ivf.hpp:243-304 with nlist = 1), one CTA per query.
+//
+// The flat stream is the rows in id order and the running threshold only
+// falls, so once the first n0 rows are scanned (an ordinary launch over
+// [0, n0): top-k `ids_a`/`dist_a`, counters `ct_a`) every later row x has
+// est(x) >= T_live(x) whenever the list-level bound L_b of its block
+// (list_lower_bound over the partition's block b, D~ - E from
+// trim_probe_mma_kernel as the coarse distance) is >= T_A = max_dis after n0
+// rows: the reference prunes it (ivf.hpp:275). Rows n0.. are stored regrouped
+// by (segment of `seg_len` consecutive ids, block), ascending ids inside
+// (seg_off: S * nb + 1 offsets). The record lists, segment by segment, the
+// runs of the kept blocks — run length in the high word of base[], the segment
+// padded to whole chunks, the last chunk of a segment flagged in the group
+// bitset — and resumes the top-k and the counters; trim_knn_kernel<SEG>
+// replays each segment's members in id order. A query whose plan does not fit
+// (more than `np` runs, 32 * gwords chunks, `pool_cap` rows in one segment,
+// kSegMaxKept blocks) is planned as one in-order run over rows [n0, n) of the
+// original arrays (mode 0, the PRE kernel without SEG). Mode 1 plans have at
+// most np_small runs (the CTA keeps three per SM), mode 2 up to np.
+// --------------------------------------------------------------------------
+// list_lower_bound for a block of a flat partition
+__device__ __forceinline__ float block_lower_bound(float dq, float R, float xmin, float xmax, float omg_lo, float omg_hi,
+                                                   float kq1, float kq2, float kest) {
+    KnnParams p{};
+    p.omg_lo = omg_lo;
+    p.omg_hi = omg_hi;
+    p.kq1 = kq1;
+    p.kq2 = kq2;
+    p.kest = kest;
+    return list_lower_bound(dq, R, xmin, xmax, p);
+}
+
+struct SegPlanParams {
+    const float* queries;
+    uint64_t nq;
+    uint32_t k, np, np_small, gwords, pool_cap, chunk; // chunk: stream positions per chunk of the filter kernel
+    uint64_t n, n0, seg_len;
+    uint32_t nseg;
+    const uint64_t* seg_off;
+    const float* approx; // nq x mma_ld(nb): tf32 |q - c_b|^2
+    const float* cn2;    // |c_b|^2
+    const float* cn;     // |c_b|
+    const uint32_t* ids_a;
+    const float* dist_a;
+    const unsigned long long* ct_a;
+    float omg_lo, omg_hi, kq1, kq2, kest;
+    uint32_t* recs;
+    unsigned long long* skipped;
+    uint32_t force_plain;
+    uint32_t* dbg; // TRIM_SEG_DEBUG: per query {kept blocks, plain, runs, chunks}, or null
+};
+constexpr uint32_t kSegMaxKept = 64; // kept blocks per query in block mode
+
+__global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex aux, SegPlanParams p) {
+    __shared__ uint32_t ws[16];
+    __shared__ uint32_t s_kept[kSegMaxKept];
+    __shared__ uint32_t s_nkept, s_bad;
+    __shared__ uint32_t s_scan[3][kWarps];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t q = blockIdx.x;
+    if (q >= p.nq)
+        return;
+    const uint32_t nb = aux.nlist;
+    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k, p.gwords);
+    uint32_t* rec = p.recs + q * lo.words;
+    const float* qrow = p.queries + q * aux.dim_stride;
+    float qp = 0.0f;
+    for (uint32_t i = tid; i < aux.dim; i += kThreads)
+        qp = __fadd_ru(qp, __fmul_ru(qrow[i], qrow[i]));
+    for (int o = 16; o > 0; o >>= 1)
+        qp = __fadd_ru(qp, __shfl_xor_sync(0xffffffffu, qp, o));
+    if (lane == 0)
+        ws[warp] = __float_as_uint(qp);
+    if (tid == 0) {
+        s_nkept = 0;
+        s_bad = p.force_plain;
+    }
+    __syncthreads();
+    float qn2 = 0.0f;
+    for (uint32_t w = 0; w < kWarps; ++w)
+        qn2 = __fadd_ru(qn2, __uint_as_float(ws[w]));
+    qn2 = __fmul_ru(qn2, 1.0f + 1.0f / 65536.0f);
+    const float qn = __fsqrt_ru(qn2);
+    const float T = p.dist_a[q * p.k + (p.k - 1)]; // max_dis after the first n0 rows
+    const float* arow = p.approx + q * mma_ld(nb);
+    // the blocks the bound cannot prune, ascending
+    for (uint32_t b0 = 0; b0 < nb; b0 += kThreads) {
+        const uint32_t b = b0 + tid;
+        bool keep = false;
+        if (b < nb) {
+            const float e = __fadd_ru(__fmul_ru(__fmul_ru(qn, __ldg(p.cn + b)), 1.0f / 64.0f),
+                                      __fmul_ru(__fadd_ru(qn2, __ldg(p.cn2 + b)), 1.0f / 16384.0f));
+            const float dq = fmaxf(__fsub_rd(arow[b], e), 0.0f); // <= |q - c_b|^2
+            keep = !(block_lower_bound(dq, __ldg(aux.list_R + b), __ldg(aux.list_xmin + b), __ldg(aux.list_xmax + b),
+                                       p.omg_lo, p.omg_hi, p.kq1, p.kq2, p.kest) >= T);
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0)
+            ws[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = s_nkept, tot = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            before += w < warp ? ws[w] : 0u;
+            tot += ws[w];
+        }
+        if (keep) {
+            const uint32_t j = before + __popc(bal & ((1u << lane) - 1u));
+            if (j < kSegMaxKept)
+                s_kept[j] = b;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_nkept += tot;
+            if (s_nkept > kSegMaxKept)
+                s_bad = 1;
+        }
+        __syncthreads();
+    }
+    const uint32_t nkept = min(s_nkept, kSegMaxKept);
+    // per segment: kept rows, runs and chunks; block-wide exclusive scans
+    uint32_t carry_runs = 0, carry_chunks = 0;
+    unsigned long long kept_rows = 0;
+    for (uint32_t g0 = 0; g0 < p.nseg && !s_bad; g0 += kThreads) {
+        const uint32_t g = g0 + tid;
+        uint32_t rows = 0, runs = 0;
+        if (g < p.nseg) {
+            const uint64_t* so = p.seg_off + static_cast<size_t>(g) * nb;
+            for (uint32_t j = 0; j < nkept; ++j) {
+                const uint32_t len = static_cast<uint32_t>(__ldg(so + s_kept[j] + 1) - __ldg(so + s_kept[j]));
+                rows += len;
+                runs += len != 0;
+            }
+        }
+        const uint32_t chunks = (rows + p.chunk - 1) / p.chunk;
+        uint32_t vr = runs, vc = chunks;
+#pragma unroll
+        for (int o = 1; o < kWarp; o <<= 1) {
+            const uint32_t tr = __shfl_up_sync(0xffffffffu, vr, o);
+            const uint32_t tc = __shfl_up_sync(0xffffffffu, vc, o);
+            if (lane >= static_cast<uint32_t>(o)) {
+                vr += tr;
+                vc += tc;
+            }
+        }
+        if (lane == kWarp - 1) {
+            s_scan[0][warp] = vr;
+            s_scan[1][warp] = vc;
+        }
+        if (rows > p.pool_cap)
+            atomicOr(&s_bad, 1u);
+        __syncthreads();
+        uint32_t br = carry_runs, bc = carry_chunks, tr = 0, tc = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            br += w < warp ? s_scan[0][w] : 0u;
+            bc += w < warp ? s_scan[1][w] : 0u;
+            tr += s_scan[0][w];
+            tc += s_scan[1][w];
+        }
+        const uint32_t r0 = br + vr - runs, c0 = bc + vc - chunks; // my first run / chunk
+        if (carry_runs + tr > p.np || carry_chunks + tc > 32u * p.gwords)
+            atomicOr(&s_bad, 1u);
+        __syncthreads();
+        if (!s_bad && g < p.nseg && rows) {
+            const uint64_t* so = p.seg_off + static_cast<size_t>(g) * nb;
+            uint32_t pos = c0 * p.chunk, r = r0;
+            for (uint32_t j = 0; j < nkept; ++j) {
+                const uint64_t b0 = __ldg(so + s_kept[j]);
+                const uint32_t len = static_cast<uint32_t>(__ldg(so + s_kept[j] + 1) - b0);
+                if (!len)
+                    continue;
+                rec[lo.cum + r] = pos;
+                reinterpret_cast<uint64_t*>(rec + lo.base)[r] = b0 | (static_cast<uint64_t>(len) << 32);
+                pos += len;
+                ++r;
+            }
+            atomicOr(rec + lo.grp + ((c0 + chunks - 1) >> 5), 1u << ((c0 + chunks - 1) & 31u));
+            kept_rows += rows;
+        }
+        carry_runs += tr;
+        carry_chunks += tc;
+        __syncthreads();
+    }
+    // resume state: the top-k after n0 rows as the seeds, its counters
+    for (uint32_t i = tid; i < p.k; i += kThreads) {
+        rec[lo.sd + i] = __float_as_uint(p.dist_a[q * p.k + i]);
+        rec[lo.sid + i] = p.ids_a[q * p.k + i];
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        kept_rows += __shfl_xor_sync(0xffffffffu, kept_rows, o);
+    __shared__ unsigned long long s_rows;
+    if (tid == 0)
+        s_rows = 0;
+    __syncthreads();
+    if (lane == 0 && kept_rows)
+        atomicAdd(&s_rows, kept_rows);
+    __syncthreads();
+    if (tid == 0) {
+        const bool plain = s_bad != 0;
+        if (p.dbg) {
+            p.dbg[q * 4 + 0] = s_nkept;
+            p.dbg[q * 4 + 1] = plain;
+            p.dbg[q * 4 + 2] = carry_runs;
+            p.dbg[q * 4 + 3] = carry_chunks;
+        }
+        rec[0] = static_cast<uint32_t>(p.n);                // evaluated
+        rec[1] = p.k;                                       // entries offered to the top-k
+        rec[4] = __float_as_uint(T);
+        rec[5] = static_cast<uint32_t>(p.ct_a[q * 6 + 0]);  // dc over [0, n0)
+        rec[6] = static_cast<uint32_t>(min(static_cast<uint64_t>(p.k), p.n)); // the seeds
+        if (plain) {
+            rec[2] = 1;
+            rec[3] = static_cast<uint32_t>(p.n - p.n0);
+            rec[7] = 0;
+            rec[lo.cum] = 0;
+            rec[lo.cum + 1] = static_cast<uint32_t>(p.n - p.n0);
+            reinterpret_cast<uint64_t*>(rec + lo.base)[0] = p.n0;
+        } else {
+            rec[2] = carry_runs;
+            rec[3] = carry_chunks * p.chunk;
+            rec[7] = carry_runs <= p.np_small ? 1 : 2; // which SEG launch (shared-memory run table) takes it
+            rec[lo.cum + carry_runs] = carry_chunks * p.chunk;
+            if (p.skipped)
+                atomicAdd(p.skipped, static_cast<unsigned long long>(p.n - p.n0) - s_rows);
+        }
     }
 }
 
@@ -1803,17 +2171,6 @@ trim_list_meta_kernel(DevIndex ix, float* list_R, float* list_xmin, float* list_
 // block centroids comes from trim_probe_mma_kernel. Output: the kept blocks in
 // ascending order (probe stride nb) and their count.
 // --------------------------------------------------------------------------
-__device__ __forceinline__ float block_lower_bound(float dq, float R, float xmin, float xmax, float omg_lo, float omg_hi,
-                                                   float kq1, float kq2, float kest) {
-    KnnParams p{};
-    p.omg_lo = omg_lo;
-    p.omg_hi = omg_hi;
-    p.kq1 = kq1;
-    p.kq2 = kq2;
-    p.kest = kest;
-    return list_lower_bound(dq, R, xmin, xmax, p);
-}
-
 __global__ void __launch_bounds__(kThreads)
 trim_block_select_kernel(DevIndex aux, const float* __restrict__ queries, uint64_t nq, const float* __restrict__ r2,
                          const float* __restrict__ approx, const float* __restrict__ cn2, const float* __restrict__ cn,
@@ -1944,6 +2301,25 @@ __global__ void trim_gather_rows_kernel(const float* __restrict__ src, uint32_t 
         return;
     for (uint32_t j = threadIdx.x; j < dim; j += blockDim.x)
         dst[i * dim + j] = src[rows[i] * stride + j];
+}
+
+// (segment, block) key of rows n0.. for the segmented flat kNN layout: row n0 + i
+// belongs to segment i / seg_len and to the partition's block assign[n0 + i].
+__global__ void trim_seg_key_kernel(const uint32_t* __restrict__ assign, uint64_t cnt, uint64_t seg_len, uint32_t nb,
+                                    uint32_t* __restrict__ keys) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < cnt)
+        keys[i] = static_cast<uint32_t>(i / seg_len) * nb + assign[i];
+}
+
+// the same with 32-bit row indices
+__global__ void trim_gather_rows32_kernel(const float* __restrict__ src, uint32_t stride, const uint32_t* __restrict__ rows,
+                                          uint64_t ns, uint32_t dim, float* __restrict__ dst) {
+    const uint64_t i = blockIdx.x;
+    if (i >= ns)
+        return;
+    for (uint32_t j = threadIdx.x; j < dim; j += blockDim.x)
+        dst[i * dim + j] = src[static_cast<size_t>(rows[i]) * stride + j];
 }
 
 // 1 if list entry e holds row e (id_base + e) for every e (flat lists in row order).

@@ -22,6 +22,8 @@ cudaError_t launch_graph(const GraphDev& g, const GraphParams& p, uint32_t S, si
 #define TRIM_DECLARE_LAUNCHERS(MV)                                                                \
     cudaError_t launch_knn_##MV(const DevIndex& ix, const KnnParams& p, size_t smem,             \
                                 cudaStream_t st);                                                 \
+    cudaError_t launch_knn_seg_##MV(const DevIndex& ix, const KnnParams& p, size_t smem,         \
+                                    cudaStream_t st);                                             \
     cudaError_t launch_range_##MV(const DevIndex& ix, const RangeParams& p, dim3 grid, size_t smem,\
                                   cudaStream_t st);                                               \
     cudaError_t launch_range_flat_##MV(const DevIndex& ix, const RangeParams& p, dim3 grid,        \

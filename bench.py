@@ -516,6 +516,8 @@ def run_ours(args, cfg):
                            filter_share_of_step=fms / ms,
                            list_skip_fraction=skipped_all / max(1.0, evaluated),
                            flat_distance_bounds=flat_bounds,
+                           # flat indexes: rows skipped as whole blocks by the segmented block stream
+                           flat_segments=bool(cfg["nlist"] == 1 and skipped_all > 0),
                            stream_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4))
                            / max(1, nl // args.steps) / gdiv / (avg_launch_ms / 1e3) / 1e9)
     if mode == "group":

@@ -12,6 +12,6 @@ run c2 "--config c2 --nq 2048 --gamma 0.8" 'regex:trim_knn_kernel' 1
 run c1 "--config c1 --gamma 0.0" 'regex:trim_knn_kernel|trim_flat_dist' 0 2
 run c4 "--config c4 --gamma 0.9" 'regex:trim_knn_kernel|trim_flat_dist' 0 2
 run c3 "--config c3 --nq 1024 --gamma 0.8" 'regex:trim_range_flat_kernel|trim_range_kernel' 0
-run c5 "--config c5 --nq 2048" 'regex:trim_knn_kernel' 0
+run c5 "--config c5 --nq 1024" 'regex:trim_knn_kernel|trim_knn_seg_plan' 0 5
 C2="python bench.py --steps 1 --warmup 0 --skip-cpu --nq 4096 --recall-q 0 --no-group-check --gamma 0.8"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:trim_' -c 80 --csv --log-file gpurun_out/${TAG}_c2_launches.csv $C2 > gpurun_out/${TAG}_launch.log 2>&1; echo launches rc=$?

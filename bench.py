@@ -520,6 +520,9 @@ def run_ours(args, cfg):
                            flat_segments=bool(cfg["nlist"] == 1 and skipped_all > 0),
                            stream_equivalent_GBps=(evaluated * (m + 4) + dc * (4 * D + 4))
                            / max(1, nl // args.steps) / gdiv / (avg_launch_ms / 1e3) / 1e9)
+    tp = ncu_traffic("tensor_pipe")  # ncu sm__pipe_tensor_cycles_active of the tcgen05 kernels; none for the LUT
+    if tp:
+        out["roofline"]["tensor_pipe"] = tp
     if mode == "group":
         out["roofline"]["note"] = ("group mode: one interval per C-ABI call (broadcast + every device's probe "
                                    "and filter + all-gather + merge), per device")

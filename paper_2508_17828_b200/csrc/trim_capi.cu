@@ -257,7 +257,7 @@ bool ensure_flat_partition(trim_index* ix) {
     ix->part_tried = true;
     const DevIndex& v = ix->dev;
     const uint64_t n = ix->total;
-    uint64_t min_rows = 1u << 18; // TRIM_FLAT_PARTITION_MIN_ROWS: tests partition small indexes
+    uint64_t min_rows = 1u << 16; // TRIM_FLAT_PARTITION_MIN_ROWS: tests partition small indexes
     if (const char* e = std::getenv("TRIM_FLAT_PARTITION_MIN_ROWS"))
         min_rows = std::strtoull(e, nullptr, 10);
     if (!flat_partition_enabled() || v.nlist != 1 || v.dim_stride != v.dim || mma_k(v.dim) > kMmaMaxK ||
@@ -409,7 +409,7 @@ bool ensure_flat_segments(trim_index* ix) {
     const DevIndex& v = ix->dev;
     const uint64_t n = ix->total;
     const uint32_t nb = ix->part_nb;
-    uint64_t rpb = 256, n0 = std::max<uint64_t>(uint64_t(std::min<uint32_t>(nb, 4096)) * 32, 16384);
+    uint64_t rpb = 256, n0 = std::max<uint64_t>(uint64_t(std::min<uint32_t>(nb, 4096)) * 32, 4096);
     if (const char* e = std::getenv("TRIM_SEG_ROWS_PER_BLOCK"))
         rpb = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     if (const char* e = std::getenv("TRIM_SEG_N0"))
@@ -638,29 +638,36 @@ size_t knn_smem_for(const trim_index* ix, uint32_t k, uint32_t np, uint32_t& top
     return smem;
 }
 
-// Segmented flat kNN (ensure_flat_segments) for one batch: the first n0 rows in
-// order, the block bounds on tcgen05, the per-query plan, then the block-stream
-// kernel and — for the queries whose plan does not fit — the in-order kernel
-// over rows [n0, n). `pb` carries the batch's queries, outputs and dap.
-constexpr uint32_t kSegRuns = 384;      // stream runs per query of the small launch (12 B of shared memory each)
-constexpr uint32_t kSegRunsLarge = 2048; // ... of the large launch (and of the record layout)
-constexpr uint32_t kSegGroupWords = 128; // 4,096 chunks
-constexpr uint32_t kSegPoolCap = 16384;  // rows of one segment's kept blocks
-bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
+// Segmented flat kNN (ensure_flat_segments) for one batch: the first rows in
+// order, the block bounds on tcgen05, the per-query plan (kept blocks merged by
+// id into an entry table), then the table-driven kernel and — for the queries
+// whose plan does not fit — the in-order kernel over the remaining rows.
+// `pb` carries the batch's queries, outputs and dap.
+constexpr uint32_t kSegTabCap = 32768; // table entries (kept rows) per query
+// Whole segments scanned in order after the layout's n0 so that the prefix is long enough for
+// k (n0 is sized for k <= 10: ~3 rows per block and neighbour wanted); false: no segment left.
+bool seg_prefix(const trim_index* ix, uint32_t k, uint32_t& seg0, uint64_t& n_a) {
+    const uint64_t want = std::min<uint64_t>(ix->total / 2, uint64_t(k) * std::min<uint32_t>(ix->part_nb, 4096) * 3);
+    seg0 = want > ix->seg_n0 ? static_cast<uint32_t>((want - ix->seg_n0 + ix->seg_len - 1) / ix->seg_len) : 0;
+    n_a = ix->seg_n0 + seg0 * ix->seg_len;
+    return seg0 < ix->seg_nseg;
+}
+
+void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n_a, cudaStream_t st) {
     const DevIndex& v = ix->dev;
     const uint32_t k = pb.k, nb = ix->part_nb, K = mma_k(v.dim);
     const uint64_t nq = pb.nq;
-    uint32_t off_a = 0, off_b = 0, off_c = 0;
-    uint32_t runs_small = kSegRuns;
-    if (const char* e = std::getenv("TRIM_SEG_SMALL_RUNS")) // tests: push plans into the large launch
-        runs_small = std::max<uint32_t>(1, std::min<uint32_t>(kSegRuns, std::strtoul(e, nullptr, 10)));
-    const size_t smem_a = knn_smem_for(ix, k, 1, off_a), smem_b = knn_smem_for(ix, k, runs_small, off_b),
-                 smem_c = knn_smem_for(ix, k, kSegRunsLarge, off_c);
-    if (smem_c > kSmemLimit)
-        return false;
-    // the first n0 rows, in order
+    uint32_t off_a = 0;
+    const size_t smem_a = knn_smem_for(ix, k, 1, off_a);
+    // the first n_a rows, in order (pb.dap, if any, covers exactly these rows)
     DevBuf ids_a(sizeof(uint32_t) * nq * k, st), dist_a(sizeof(float) * nq * k, st),
-        ct_a(sizeof(unsigned long long) * nq * 6, st);
+        ct_a(sizeof(unsigned long long) * nq * 6, st), offs_a(sizeof(uint64_t) * 2, st);
+    DevIndex head = ix->seg_head;
+    if (seg0) { // (pageable copy of 16 bytes: staged by the runtime before the call returns)
+        const uint64_t ha[2] = {0, n_a};
+        CK(cudaMemcpyAsync(offs_a.p, ha, sizeof ha, cudaMemcpyHostToDevice, st));
+        head.list_offsets = offs_a.as<uint64_t>();
+    }
     KnnParams pa = pb;
     pa.np = 1;
     pa.probe = nullptr;
@@ -670,7 +677,7 @@ bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
     pa.counters = ct_a.as<unsigned long long>();
     pa.topk_off = off_a;
     pa.timeline = nullptr;
-    launch_knn(ix->seg_head, pa, smem_a, st);
+    launch_knn(head, pa, smem_a, st);
     // |q - c_b|^2 bounds to the block centroids
     const uint32_t ntiles = (nb + kMmaN - 1) / kMmaN;
     DevBuf approx(sizeof(float) * nq * mma_ld(nb), st);
@@ -681,23 +688,21 @@ bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
                             kMmaThreads, probe_mma_smem(K), st>>>(pb.queries, nq, v.dim_stride, K, ix->part_tiles,
                                                                   ix->part_cn2, nb, approx.as<float>());
     CK(cudaGetLastError());
-    const KnnPlanLayout lo = KnnPlanLayout::of(kSegRunsLarge, k, kSegGroupWords);
-    DevBuf recs(sizeof(uint32_t) * lo.words * nq, st);
-    CK(cudaMemsetAsync(recs.p, 0, sizeof(uint32_t) * lo.words * nq, st));
+    const KnnPlanLayout lo = KnnPlanLayout::of(1, k);
+    DevBuf recs(sizeof(uint32_t) * lo.words * nq, st), tab(sizeof(uint32_t) * kSegTabCap * nq, st);
     SegPlanParams sp{};
     sp.queries = pb.queries;
     sp.nq = nq;
     sp.k = k;
-    sp.np = kSegRunsLarge;
-    sp.np_small = runs_small;
-    sp.gwords = kSegGroupWords;
-    sp.pool_cap = kSegPoolCap;
-    sp.chunk = knn_chunk(k > 256 ? 0 : dispatch_m(v));
+    sp.np = 1;
+    sp.tab_cap = kSegTabCap;
     sp.n = ix->total;
-    sp.n0 = ix->seg_n0;
+    sp.n0 = n_a;
+    sp.seg0 = seg0;
     sp.seg_len = ix->seg_len;
     sp.nseg = ix->seg_nseg;
     sp.seg_off = ix->seg_off;
+    sp.ids = ix->seg.list_ids;
     sp.approx = approx.as<float>();
     sp.cn2 = ix->part_cn2;
     sp.cn = ix->part_cn;
@@ -710,6 +715,7 @@ bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
     sp.kq2 = pb.kq2;
     sp.kest = pb.kest;
     sp.recs = recs.as<uint32_t>();
+    sp.tab = tab.as<uint32_t>();
     sp.skipped = pb.skip_lists ? pb.skipped : nullptr;
     {
         const char* e = std::getenv("TRIM_SEG_FORCE_PLAIN"); // tests: every query takes the in-order resume
@@ -729,40 +735,33 @@ bool knn_seg_batch(const trim_index* ix, KnnParams pb, cudaStream_t st) {
         CK(cudaMemcpyAsync(h.data(), dbg.p, sizeof(uint32_t) * 4 * nq, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ta.data(), dist_a.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        uint64_t plain = 0, kept = 0, runs = 0, chunks = 0, kmax = 0;
+        uint64_t plain = 0, kept = 0, rows = 0, sorted = 0, kmax = 0;
         double tsum = 0;
         for (uint64_t i = 0; i < nq; ++i) {
             kept += h[4 * i];
             kmax = std::max<uint64_t>(kmax, h[4 * i]);
             plain += h[4 * i + 1];
-            runs += h[4 * i + 2];
-            chunks += h[4 * i + 3];
+            rows += h[4 * i + 2];
+            sorted += h[4 * i + 3];
             tsum += ta[i * k + k - 1];
         }
         std::fprintf(stderr,
-                     "[trim seg] nq=%llu nb=%u n0=%llu seg_len=%llu nseg=%u: plain=%llu kept/q=%.1f (max %llu) "
-                     "runs/q=%.1f chunks/q=%.1f mean T_A=%.3f\n",
-                     (unsigned long long)nq, nb, (unsigned long long)ix->seg_n0, (unsigned long long)ix->seg_len,
+                     "[trim seg] nq=%llu nb=%u rows_in_order=%llu seg_len=%llu segments=%u..%u: plain=%llu kept/q=%.1f "
+                     "(max %llu) table rows/q=%.1f sorted segments/q=%.1f mean T_A=%.3f\n",
+                     (unsigned long long)nq, nb, (unsigned long long)n_a, (unsigned long long)ix->seg_len, seg0,
                      ix->seg_nseg, (unsigned long long)plain, double(kept) / nq, (unsigned long long)kmax,
-                     double(runs) / nq, double(chunks) / nq, tsum / nq);
+                     double(rows) / nq, double(sorted) / nq, tsum / nq);
     }
-    DevBuf pool(sizeof(uint32_t) * 5 * kSegPoolCap * nq, st);
     pb.plan = recs.as<uint32_t>();
-    pb.np_rec = kSegRunsLarge;
+    pb.np = 1;
     pb.probe = nullptr;
-    pb.gwords = kSegGroupWords;
-    pb.pool = pool.as<uint32_t>();
-    pb.pool_cap = kSegPoolCap;
-    pb.np = runs_small;
-    pb.topk_off = off_b;
-    launch_knn(v, pb, smem_b, st); // records of mode 0: in order over the original arrays (the long ones first)
-    pb.seg_mode = 1; // records of mode 1
-    launch_knn_seg(ix->seg, pb, smem_b, st);
-    pb.np = kSegRunsLarge; // records of mode 2
-    pb.seg_mode = 2;
-    pb.topk_off = off_c;
-    launch_knn_seg(ix->seg, pb, smem_c, st);
-    return true;
+    pb.dap = nullptr; // the distance bounds cover the in-order prefix only
+    pb.dap_ld = 0;
+    pb.tab = tab.as<uint32_t>();
+    pb.tab_cap = kSegTabCap;
+    pb.topk_off = off_a;
+    launch_knn(v, pb, smem_a, st);           // records of mode 0: in order over the original arrays (the long ones first)
+    launch_knn_seg(ix->seg, pb, smem_a, st); // records of mode 1: the entry tables
 }
 
 // kNN filter launch over padded device queries and precomputed probe lists
@@ -818,18 +817,23 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     // flat scans: tensor-core distance bounds for every (query, row), so only
     // members that can enter the top-k get the exact distance
     // (up to 16M rows: D~ holds nq x rows floats and the pre-tiled rows another copy of the vectors)
+    // flat scans of partitioned indexes: segmented block stream (knn_seg_batch); the distance
+    // bounds then cover only the rows scanned in order
+    uint32_t seg0 = 0;
+    uint64_t n_a = 0;
+    const bool seg = ix->dev.nlist == 1 && !d_probe && np == 1 && ensure_flat_segments(const_cast<trim_index*>(ix)) &&
+                     uint64_t(k) * 4 <= ix->seg_n0 && seg_prefix(ix, k, seg0, n_a) &&
+                     knn_smem_bytes(k > 256 ? 0 : dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, 1) <= kSmemLimit;
+    const uint64_t bound_rows = seg ? n_a : ix->dev.n;
     const bool flat_bounds = ix->dev.nlist == 1 && np == 1 && ix->dev.n > 0 && ix->dev.n <= (16ull << 20) &&
                              flat_bounds_enabled() && ensure_flat_tiles(const_cast<trim_index*>(ix));
-    const uint64_t ld = flat_bounds ? (ix->dev.n + kMmaN - 1) / kMmaN * kMmaN : 0;
+    const uint64_t ld = flat_bounds ? (bound_rows + kMmaN - 1) / kMmaN * kMmaN : 0;
     // slices: grid.x <= 2^31-1; with bounds, D~ of a slice (nq x ld floats) within ~8 GB
     uint64_t slice = 1u << 30;
     if (flat_bounds)
         slice = std::max<uint64_t>(kMmaM, (8ull << 30) / (ld * 2) / kMmaM * kMmaM);
-    // flat scans of partitioned indexes: segmented block stream (knn_seg_batch)
-    const bool seg = ix->dev.nlist == 1 && !d_probe && np == 1 && ensure_flat_segments(const_cast<trim_index*>(ix)) &&
-                     uint64_t(k) * 4 <= ix->seg_n0;
     if (seg)
-        slice = std::min<uint64_t>(slice, 1024); // the member pools: 320 KB per query
+        slice = std::min<uint64_t>(slice, 2048); // the entry tables: 128 KB per query
     for (uint64_t b = 0; b < nq; b += slice) {
         KnnParams pb = p;
         pb.nq = std::min<uint64_t>(slice, nq - b);
@@ -872,8 +876,10 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
             CK(cudaGetLastError());
             pb.plan = recs.as<uint32_t>();
         }
-        if (seg && knn_seg_batch(ix, pb, st))
+        if (seg) {
+            knn_seg_batch(ix, pb, seg0, n_a, st);
             continue;
+        }
         launch_knn(ix->dev, pb, smem, st);
     }
     return TRIM_OK;

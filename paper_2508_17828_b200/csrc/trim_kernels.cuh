@@ -308,13 +308,9 @@ struct KnnParams {
     uint64_t dap_ld;
     const uint32_t* plan;  // per-query setup records (trim_knn_setup_kernel), or null: set up in the kernel
     uint32_t topk_off;     // k > 256: byte offset of the SmemTopK keys in dynamic shared memory
-    // segmented flat scans (trim_knn_seg_plan_kernel): group bitset words per record,
-    // and the replay warp's per-query member pool in global memory (5 x pool_cap words)
-    uint32_t gwords;
-    uint32_t pool_cap;
-    uint32_t* pool;
-    uint32_t np_rec;   // runs the record layout is sized for (0: np)
-    uint32_t seg_mode; // SEG kernel: the record mode this launch serves (1: <= np runs of a small CTA, 2: large)
+    // segmented flat scans (trim_knn_seg_plan_kernel): per-query entry tables, tab_cap words each
+    const uint32_t* tab;
+    uint32_t tab_cap;
 };
 
 // Per-query setup record written by trim_knn_setup_kernel (u32 words): the
@@ -322,18 +318,17 @@ struct KnnParams {
 // the compacted stream after the list-level plan — what the replay warp of
 // trim_knn_kernel otherwise computes itself before the workers may start.
 struct KnnPlanLayout {
-    uint32_t cum, base, sd, sid, grp, words;
+    uint32_t cum, base, sd, sid, words;
     // header: [0] total [1] nseed [2] nk [3] total2 [4] T0 bits [5] dc so far (the seeds, or
     // everything before a resumed scan) [6] entries evaluated unconditionally (edc = evaluated
-    // - this) [7] mode: 0 = stream in order, 1 = segmented block stream (SEG kernel)
-    __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k, uint32_t gwords = 0) {
+    // - this) [7] mode: 0 = runs in cum/base, 1 = entry table of a segmented block stream (SEG kernel)
+    __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k) {
         KnnPlanLayout o;
         o.cum = 8;
         o.base = (o.cum + np + 1 + 1) & ~1u; // u64-aligned
         o.sd = o.base + 2 * np;
         o.sid = o.sd + k;
-        o.grp = o.sid + k;                   // gwords: bit c = chunk c ends a replay group
-        o.words = (o.grp + gwords + 1) & ~1u;
+        o.words = (o.sid + k + 1) & ~1u;
         return o;
     }
 };
@@ -520,15 +515,11 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 //
 // SEG (with PRE): a segmented block stream over a flat index
 // (trim_knn_seg_plan_kernel). `ix` holds the rows regrouped by (segment of
-// consecutive ids, block), the record resumes the scan after the first n0 rows
-// (top-k, counters) and lists, per segment, the runs of the blocks the
-// list-level bound could not prune (run length in the high word of base[],
-// each segment padded to whole chunks). The blocks of a segment interleave in
-// id order, so the replay warp gathers a segment's members (a replay group: the
-// chunks up to the one whose group bit is set) in a per-query pool and replays
-// them in ascending-id order: members below the smallest id that can change the
-// top-k or needs the reference-order ADC are order-free under the current
-// threshold, that one is handled alone, and so on — the reference's decisions.
+// consecutive ids, block); the record resumes the scan after the first rows
+// (top-k, counters) and the query's entry table (p.tab) lists the rows of the
+// blocks the list-level bound could not prune, merged back into ascending-id
+// order — the reference's stream order with the pruned blocks' rows removed —
+// so stream position pp is entry tab[pp] and the pipeline below runs unchanged.
 // A CTA whose record is of the other mode exits at once (both kernels are
 // launched over the batch).
 template <int M, int KS, int S, bool PRE, bool SEG = false>
@@ -593,14 +584,16 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     __syncthreads();
     // the stream (probe order, ascending ids) — from the setup record when
     // trim_knn_setup_kernel ran, else built here
-    const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords).words : nullptr;
+    const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words : nullptr;
     if constexpr (PRE) {
-        if (__ldg(rec + 7) != (SEG ? p.seg_mode : 0u)) // another launch's query
+        if (__ldg(rec + 7) != (SEG ? 1u : 0u)) // the other launch's query
             return;
     }
+    // SEG: the query's entry table (stream position -> entry of the regrouped arrays)
+    [[maybe_unused]] const uint32_t* tab = SEG ? p.tab + static_cast<size_t>(q) * p.tab_cap : nullptr;
     uint32_t total;
     if constexpr (PRE) {
-        const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
+        const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
         const uint32_t nk = __ldg(rec + 2);
         for (uint32_t i = tid; i <= nk; i += kThreads)
             st.cum[i] = __ldg(rec + lo.cum + i);
@@ -625,7 +618,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         topk.init(p.k, smem + p.topk_off);
         uint32_t carry = 0, nk = 0;
         if constexpr (PRE) { // seeds and plan from trim_knn_setup_kernel
-            const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
+            const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
             for (uint32_t j = 0; j < nseed; ++j)
                 topk.offer(__uint_as_float(__ldg(rec + lo.sd + j)), __ldg(rec + lo.sid + j));
             nk = __ldg(rec + 2);
@@ -720,24 +713,24 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             for (uint32_t r = 0; r < i; ++r)
                 mask &= mask - 1;
             const uint32_t pp = c * kChunkW + w * kPerWorker + (__ffs(mask) - 1);
-            uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (st.cum[mid] <= pp)
-                    lo = mid;
-                else
-                    hi = mid;
+            uint64_t e;
+            if constexpr (SEG) {
+                e = __ldg(tab + pp);
+            } else {
+                uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (st.cum[mid] <= pp)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                e = st.base[lo] + (pp - st.cum[lo]);
             }
-            const uint64_t e = st.base[lo] + (pp - st.cum[lo]);
             const float a = adc_serial<M>(ix.codes + e * ix.code_stride, m);
             return relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma);
         };
         TRIM_TL(unsigned long long cyc_wait = 0, cyc_busy = 0;)
-        // SEG: the group's member pool (id, lo, hi, d, entry: pool_cap words each)
-        [[maybe_unused]] uint32_t pn = 0;
-        [[maybe_unused]] const uint32_t pcap = p.pool_cap;
-        [[maybe_unused]] uint32_t* pool = SEG ? p.pool + static_cast<size_t>(q) * 5u * p.pool_cap : nullptr;
-        [[maybe_unused]] const uint32_t glo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords).grp;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const uint32_t s = c % kRing;
             TRIM_TL(const unsigned long long k0 = tl ? clock64() : 0;)
@@ -755,96 +748,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
                     inc += t;
             }
             const uint32_t nmem = __shfl_sync(0xffffffffu, inc, kWorkers - 1);
-            if constexpr (SEG) {
-                // the chunk's members join the group's pool (with their entry index, recovered
-                // from the bin's lane mask and cum/base); the ring slot is free at once
-                for (uint32_t base = 0; base < nmem; base += kWarp) {
-                    const uint32_t i = base + lane;
-                    uint32_t w = 0, before = 0;
-#pragma unroll
-                    for (uint32_t x = 0; x < kWorkers; ++x) {
-                        const uint32_t ix_ = __shfl_sync(0xffffffffu, inc, x);
-                        if (i >= ix_) {
-                            w = x + 1;
-                            before = ix_;
-                        }
-                    }
-                    if (i < nmem) {
-                        const uint32_t r = i - before;
-                        const uint32_t g = s * kChunkW + w * kPerWorker + r;
-                        const uint32_t pos = __fns(bin_mask[s * kWorkers + w], 0, static_cast<int>(r) + 1);
-                        const uint32_t pp = c * kChunkW + w * kPerWorker + pos;
-                        uint32_t lo = 0, hi = ncum; // largest li with cum[li] <= pp
-                        while (hi - lo > 1) {
-                            const uint32_t mid = (lo + hi) >> 1;
-                            if (st.cum[mid] <= pp)
-                                lo = mid;
-                            else
-                                hi = mid;
-                        }
-                        const uint32_t j = pn + i; // <= pool_cap: the plan bounds a group's rows
-                        __stcg(pool + j, s_e[g]);
-                        __stcg(pool + pcap + j, __float_as_uint(s_lo[g]));
-                        __stcg(pool + 2 * pcap + j, __float_as_uint(s_hi[g]));
-                        __stcg(pool + 3 * pcap + j, __float_as_uint(s_d[g]));
-                        __stcg(pool + 4 * pcap + j, static_cast<uint32_t>(st.base[lo]) + (pp - st.cum[lo]));
-                    }
-                }
-                TRIM_TL(members += nmem;)
-                pn += nmem;
-                __syncwarp();
-                mbar_arrive(empty + s);
-                if (!((__ldg(rec + glo + (c >> 5)) >> (c & 31u)) & 1u))
-                    continue;
-                // replay the group in ascending-id order
-                uint64_t lb = 0; // ids below lb are decided
-                for (;;) {
-                    const float T = topk.wd;
-                    const uint32_t Tid = topk.wid;
-                    uint32_t hid = kInvalidId, hidx = 0; // my smallest member that may change T
-                    for (uint32_t i = lane; i < pn; i += kWarp) {
-                        const uint32_t id = __ldcg(pool + i);
-                        if (id < lb || id >= hid)
-                            continue;
-                        if (!(__uint_as_float(__ldcg(pool + pcap + i)) < T))
-                            continue; // pruned under T (and under any later, smaller threshold)
-                        const float hi = __uint_as_float(__ldcg(pool + 2 * pcap + i));
-                        const float dd = __uint_as_float(__ldcg(pool + 3 * pcap + i));
-                        if (!(hi < T) || scored_less(dd, id, T, Tid)) {
-                            hid = id;
-                            hidx = i;
-                        }
-                    }
-                    const uint32_t f = __reduce_min_sync(0xffffffffu, hid);
-                    uint32_t cnt = 0; // members in [lb, f): evaluated, none replaces (ivf.hpp:275-282)
-                    for (uint32_t i = lane; i < pn; i += kWarp) {
-                        const uint32_t id = __ldcg(pool + i);
-                        if (id >= lb && id < f && __uint_as_float(__ldcg(pool + pcap + i)) < T)
-                            ++cnt;
-                    }
-                    dc += __reduce_add_sync(0xffffffffu, cnt);
-                    if (f == kInvalidId)
-                        break;
-                    const uint32_t src = __ffs(__ballot_sync(0xffffffffu, hid == f)) - 1;
-                    const uint32_t fi = __shfl_sync(0xffffffffu, hidx, src);
-                    bool ev = true;
-                    if (!(__uint_as_float(__ldcg(pool + 2 * pcap + fi)) < T)) { // straddles: reference-order est
-                        const uint32_t e = __ldcg(pool + 4 * pcap + fi);
-                        const float a = adc_serial<M>(ix.codes + static_cast<size_t>(e) * ix.code_stride, m);
-                        ev = relaxed_lb(__fsqrt_rn(a), __ldg(ix.lx + e), p.two_gamma) < T;
-                    }
-                    if (ev) {
-                        ++dc;
-                        topk.offer(__uint_as_float(__ldcg(pool + 3 * pcap + fi)), f);
-                    }
-                    lb = static_cast<uint64_t>(f) + 1;
-                }
-                pn = 0;
-                if (lane == 0)
-                    *reinterpret_cast<volatile float*>(s_T) = topk.wd;
-                __syncwarp();
-                continue;
-            }
             for (uint32_t base = 0; base < nmem; base += kWarp) {
                 const uint32_t i = base + lane;
                 const uint32_t cnt = min(static_cast<uint32_t>(kWarp), nmem - base);
@@ -962,17 +865,11 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
             x.e = 0;
             x.lx = 0.0f;
             if (c < nchunks && pp < bound) {
-                while (st.cum[li + 1] <= pp)
-                    ++li;
-                if constexpr (SEG) { // positions past the run's length pad the segment to whole chunks
-                    const uint64_t b = st.base[li];
-                    const uint32_t o = pp - st.cum[li];
-                    if (o >= static_cast<uint32_t>(b >> 32)) {
-                        x.fc.zero(m);
-                        continue;
-                    }
-                    x.e = static_cast<uint32_t>(b) + o;
+                if constexpr (SEG) { // the plan's entry table: the kept rows in ascending-id order
+                    x.e = __ldg(tab + pp);
                 } else {
+                    while (st.cum[li + 1] <= pp)
+                        ++li;
                     x.e = static_cast<uint32_t>(st.base[li] + (pp - st.cum[li]));
                 }
                 x.kind = 2u;
@@ -1449,7 +1346,7 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
     __syncwarp();
     const uint32_t total = carry;
     const uint32_t nseed = min(p.k, total);
-    const KnnPlanLayout lo = KnnPlanLayout::of(p.np_rec ? p.np_rec : p.np, p.k, p.gwords);
+    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
     uint32_t* rec = recs + static_cast<size_t>(q) * lo.words;
     // seeds (ivf.hpp:264-271): exact distances in stream order; T0 = max_dis
     // after them (the largest (d, id), or +inf when fewer than k)
@@ -1539,15 +1436,14 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
 // trim_probe_mma_kernel as the coarse distance) is >= T_A = max_dis after n0
 // rows: the reference prunes it (ivf.hpp:275). Rows n0.. are stored regrouped
 // by (segment of `seg_len` consecutive ids, block), ascending ids inside
-// (seg_off: S * nb + 1 offsets). The record lists, segment by segment, the
-// runs of the kept blocks — run length in the high word of base[], the segment
-// padded to whole chunks, the last chunk of a segment flagged in the group
-// bitset — and resumes the top-k and the counters; trim_knn_kernel<SEG>
-// replays each segment's members in id order. A query whose plan does not fit
-// (more than `np` runs, 32 * gwords chunks, `pool_cap` rows in one segment,
-// kSegMaxKept blocks) is planned as one in-order run over rows [n0, n) of the
-// original arrays (mode 0, the PRE kernel without SEG). Mode 1 plans have at
-// most np_small runs (the CTA keeps three per SM), mode 2 up to np.
+// (seg_off: S * nb + 1 offsets). For each segment the kept blocks' runs (each
+// ascending in id) are merged by id in shared memory — (id << 32 | entry) keys,
+// bitonic sort — and the entries appended to the query's table: the
+// reference's stream with the pruned blocks' rows removed, in order. The record
+// resumes the top-k and the counters; trim_knn_kernel<SEG> walks the table. A
+// query whose plan does not fit (more than kSegMaxKept blocks, kSegSortCap rows
+// of one segment, `tab_cap` rows in all) is planned as one in-order run over
+// rows [n0, n) of the original arrays (mode 0, the PRE kernel without SEG).
 // --------------------------------------------------------------------------
 // list_lower_bound for a block of a flat partition
 __device__ __forceinline__ float block_lower_bound(float dq, float R, float xmin, float xmax, float omg_lo, float omg_hi,
@@ -1564,36 +1460,43 @@ __device__ __forceinline__ float block_lower_bound(float dq, float R, float xmin
 struct SegPlanParams {
     const float* queries;
     uint64_t nq;
-    uint32_t k, np, np_small, gwords, pool_cap, chunk; // chunk: stream positions per chunk of the filter kernel
-    uint64_t n, n0, seg_len;
-    uint32_t nseg;
+    uint32_t k, np;          // np: the record layout's run capacity (1)
+    uint32_t tab_cap;        // table words per query
+    uint64_t n, n0, seg_len; // n0: rows scanned in order so far (the layout's n0 + seg0 whole segments)
+    uint32_t nseg, seg0;     // segments [seg0, nseg) remain
     const uint64_t* seg_off;
-    const float* approx; // nq x mma_ld(nb): tf32 |q - c_b|^2
-    const float* cn2;    // |c_b|^2
-    const float* cn;     // |c_b|
+    const uint32_t* ids;  // ids of the regrouped entries
+    const float* approx;  // nq x mma_ld(nb): tf32 |q - c_b|^2
+    const float* cn2;     // |c_b|^2
+    const float* cn;      // |c_b|
     const uint32_t* ids_a;
     const float* dist_a;
     const unsigned long long* ct_a;
     float omg_lo, omg_hi, kq1, kq2, kest;
     uint32_t* recs;
+    uint32_t* tab;
     unsigned long long* skipped;
     uint32_t force_plain;
-    uint32_t* dbg; // TRIM_SEG_DEBUG: per query {kept blocks, plain, runs, chunks}, or null
+    uint32_t* dbg; // TRIM_SEG_DEBUG: per query {kept blocks, plain, table rows, segments sorted}, or null
 };
-constexpr uint32_t kSegMaxKept = 64; // kept blocks per query in block mode
+constexpr uint32_t kSegMaxKept = 64;   // kept blocks per query in block mode
+constexpr uint32_t kSegSortCap = 4096; // rows of one segment's kept blocks (32 KB of sort keys)
 
 __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex aux, SegPlanParams p) {
+    __shared__ unsigned long long s_key[kSegSortCap];
     __shared__ uint32_t ws[16];
     __shared__ uint32_t s_kept[kSegMaxKept];
+    __shared__ uint32_t s_roff[kSegMaxKept + 1];
+    __shared__ unsigned long long s_rbase[kSegMaxKept];
     __shared__ uint32_t s_nkept, s_bad;
-    __shared__ uint32_t s_scan[3][kWarps];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint64_t q = blockIdx.x;
     if (q >= p.nq)
         return;
     const uint32_t nb = aux.nlist;
-    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k, p.gwords);
+    const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
     uint32_t* rec = p.recs + q * lo.words;
+    uint32_t* tab = p.tab + q * p.tab_cap;
     const float* qrow = p.queries + q * aux.dim_stride;
     float qp = 0.0f;
     for (uint32_t i = tid; i < aux.dim; i += kThreads)
@@ -1648,67 +1551,98 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
         __syncthreads();
     }
     const uint32_t nkept = min(s_nkept, kSegMaxKept);
-    // per segment: kept rows, runs and chunks; block-wide exclusive scans
-    uint32_t carry_runs = 0, carry_chunks = 0;
-    unsigned long long kept_rows = 0;
-    for (uint32_t g0 = 0; g0 < p.nseg && !s_bad; g0 += kThreads) {
-        const uint32_t g = g0 + tid;
-        uint32_t rows = 0, runs = 0;
-        if (g < p.nseg) {
-            const uint64_t* so = p.seg_off + static_cast<size_t>(g) * nb;
-            for (uint32_t j = 0; j < nkept; ++j) {
-                const uint32_t len = static_cast<uint32_t>(__ldg(so + s_kept[j] + 1) - __ldg(so + s_kept[j]));
-                rows += len;
-                runs += len != 0;
-            }
-        }
-        const uint32_t chunks = (rows + p.chunk - 1) / p.chunk;
-        uint32_t vr = runs, vc = chunks;
+    // segment by segment: the kept blocks' runs merged by id into the table
+    uint32_t total = 0, sorted = 0;
+    for (uint32_t g = p.seg0; g < p.nseg; ++g) {
+        if (s_bad)
+            break;
+        const uint64_t* so = p.seg_off + static_cast<size_t>(g) * nb;
+        if (tid < kWarp) { // run starts and the prefix of their lengths (nkept <= 64: two per lane)
+            uint32_t carry = 0;
+            for (uint32_t j0 = 0; j0 < nkept; j0 += kWarp) {
+                const uint32_t j = j0 + lane;
+                uint32_t len = 0;
+                if (j < nkept) {
+                    const uint64_t b0 = __ldg(so + s_kept[j]);
+                    len = static_cast<uint32_t>(__ldg(so + s_kept[j] + 1) - b0);
+                    s_rbase[j] = b0;
+                }
+                uint32_t v = len;
 #pragma unroll
-        for (int o = 1; o < kWarp; o <<= 1) {
-            const uint32_t tr = __shfl_up_sync(0xffffffffu, vr, o);
-            const uint32_t tc = __shfl_up_sync(0xffffffffu, vc, o);
-            if (lane >= static_cast<uint32_t>(o)) {
-                vr += tr;
-                vc += tc;
+                for (int o = 1; o < kWarp; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= static_cast<uint32_t>(o))
+                        v += t;
+                }
+                if (j < nkept)
+                    s_roff[j] = carry + v - len;
+                carry += __shfl_sync(0xffffffffu, v, kWarp - 1);
             }
+            if (lane == 0)
+                s_roff[nkept] = carry;
         }
-        if (lane == kWarp - 1) {
-            s_scan[0][warp] = vr;
-            s_scan[1][warp] = vc;
-        }
-        if (rows > p.pool_cap)
-            atomicOr(&s_bad, 1u);
         __syncthreads();
-        uint32_t br = carry_runs, bc = carry_chunks, tr = 0, tc = 0;
-        for (uint32_t w = 0; w < kWarps; ++w) {
-            br += w < warp ? s_scan[0][w] : 0u;
-            bc += w < warp ? s_scan[1][w] : 0u;
-            tr += s_scan[0][w];
-            tc += s_scan[1][w];
+        const uint32_t rows = s_roff[nkept];
+        if (rows == 0) {
+            __syncthreads();
+            continue;
         }
-        const uint32_t r0 = br + vr - runs, c0 = bc + vc - chunks; // my first run / chunk
-        if (carry_runs + tr > p.np || carry_chunks + tc > 32u * p.gwords)
-            atomicOr(&s_bad, 1u);
-        __syncthreads();
-        if (!s_bad && g < p.nseg && rows) {
-            const uint64_t* so = p.seg_off + static_cast<size_t>(g) * nb;
-            uint32_t pos = c0 * p.chunk, r = r0;
-            for (uint32_t j = 0; j < nkept; ++j) {
-                const uint64_t b0 = __ldg(so + s_kept[j]);
-                const uint32_t len = static_cast<uint32_t>(__ldg(so + s_kept[j] + 1) - b0);
-                if (!len)
-                    continue;
-                rec[lo.cum + r] = pos;
-                reinterpret_cast<uint64_t*>(rec + lo.base)[r] = b0 | (static_cast<uint64_t>(len) << 32);
-                pos += len;
-                ++r;
+        if (rows > kSegSortCap || total + rows > p.tab_cap) {
+            __syncthreads();
+            if (tid == 0)
+                s_bad = 1;
+            __syncthreads();
+            break;
+        }
+        uint32_t nonempty = 0;
+        for (uint32_t j = 0; j < nkept; ++j)
+            nonempty += s_roff[j + 1] != s_roff[j];
+        if (nonempty == 1) { // one run: already in id order
+            uint32_t j = 0;
+            while (s_roff[j + 1] == s_roff[j])
+                ++j;
+            const uint32_t b0 = static_cast<uint32_t>(s_rbase[j]);
+            for (uint32_t i = tid; i < rows; i += kThreads)
+                tab[total + i] = b0 + i;
+        } else {
+            uint32_t P = 2;
+            while (P < rows)
+                P <<= 1;
+            for (uint32_t i = tid; i < P; i += kThreads) {
+                unsigned long long key = ~0ull;
+                if (i < rows) {
+                    uint32_t a = 0, b = nkept; // the run holding merged-input index i
+                    while (b - a > 1) {
+                        const uint32_t mid = (a + b) >> 1;
+                        if (s_roff[mid] <= i)
+                            a = mid;
+                        else
+                            b = mid;
+                    }
+                    const uint32_t e = static_cast<uint32_t>(s_rbase[a]) + (i - s_roff[a]);
+                    key = (static_cast<unsigned long long>(__ldg(p.ids + e)) << 32) | e;
+                }
+                s_key[i] = key;
             }
-            atomicOr(rec + lo.grp + ((c0 + chunks - 1) >> 5), 1u << ((c0 + chunks - 1) & 31u));
-            kept_rows += rows;
+            __syncthreads();
+            for (uint32_t size = 2; size <= P; size <<= 1)
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t i = tid; i < P / 2; i += kThreads) {
+                        const uint32_t l0 = 2 * i - (i & (stride - 1)), h0 = l0 + stride;
+                        const bool up = (l0 & size) == 0;
+                        const unsigned long long x = s_key[l0], y = s_key[h0];
+                        if ((x > y) == up) {
+                            s_key[l0] = y;
+                            s_key[h0] = x;
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (uint32_t i = tid; i < rows; i += kThreads)
+                tab[total + i] = static_cast<uint32_t>(s_key[i]);
+            ++sorted;
         }
-        carry_runs += tr;
-        carry_chunks += tc;
+        total += rows;
         __syncthreads();
     }
     // resume state: the top-k after n0 rows as the seeds, its counters
@@ -1716,42 +1650,32 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
         rec[lo.sd + i] = __float_as_uint(p.dist_a[q * p.k + i]);
         rec[lo.sid + i] = p.ids_a[q * p.k + i];
     }
-    for (int o = 16; o > 0; o >>= 1)
-        kept_rows += __shfl_xor_sync(0xffffffffu, kept_rows, o);
-    __shared__ unsigned long long s_rows;
-    if (tid == 0)
-        s_rows = 0;
-    __syncthreads();
-    if (lane == 0 && kept_rows)
-        atomicAdd(&s_rows, kept_rows);
-    __syncthreads();
     if (tid == 0) {
         const bool plain = s_bad != 0;
         if (p.dbg) {
             p.dbg[q * 4 + 0] = s_nkept;
             p.dbg[q * 4 + 1] = plain;
-            p.dbg[q * 4 + 2] = carry_runs;
-            p.dbg[q * 4 + 3] = carry_chunks;
+            p.dbg[q * 4 + 2] = total;
+            p.dbg[q * 4 + 3] = sorted;
         }
         rec[0] = static_cast<uint32_t>(p.n);                // evaluated
         rec[1] = p.k;                                       // entries offered to the top-k
         rec[4] = __float_as_uint(T);
         rec[5] = static_cast<uint32_t>(p.ct_a[q * 6 + 0]);  // dc over [0, n0)
         rec[6] = static_cast<uint32_t>(min(static_cast<uint64_t>(p.k), p.n)); // the seeds
+        rec[lo.cum] = 0;
         if (plain) {
             rec[2] = 1;
             rec[3] = static_cast<uint32_t>(p.n - p.n0);
             rec[7] = 0;
-            rec[lo.cum] = 0;
             rec[lo.cum + 1] = static_cast<uint32_t>(p.n - p.n0);
             reinterpret_cast<uint64_t*>(rec + lo.base)[0] = p.n0;
         } else {
-            rec[2] = carry_runs;
-            rec[3] = carry_chunks * p.chunk;
-            rec[7] = carry_runs <= p.np_small ? 1 : 2; // which SEG launch (shared-memory run table) takes it
-            rec[lo.cum + carry_runs] = carry_chunks * p.chunk;
+            rec[2] = 0; // no runs: the stream is the table
+            rec[3] = total;
+            rec[7] = 1;
             if (p.skipped)
-                atomicAdd(p.skipped, static_cast<unsigned long long>(p.n - p.n0) - s_rows);
+                atomicAdd(p.skipped, static_cast<unsigned long long>(p.n - p.n0) - total);
         }
     }
 }

@@ -36,8 +36,11 @@ METRICS = {
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True)
-    rows = list(csv.reader(io.StringIO(out.stdout)))
+    if rep.endswith(".csv"):  # already exported on the GPU box (ncu -i ... --page raw --csv)
+        text = open(rep).read()
+    else:
+        text = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(text)))
     h, units, vals = rows[0], rows[1], rows[2:]
     unit = dict(zip(h, units))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,

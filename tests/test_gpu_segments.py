@@ -4,8 +4,8 @@ trim_knn_kernel<SEG>): ivf::search_trim_ivf_knn with nlist = 1
 
 The rows after the first n0 are regrouped by (segment of consecutive ids,
 block); blocks whose list-level bound is >= the threshold after n0 rows are
-never read and each segment's members are replayed in ascending-id order, so
-ids, distance bits and every counter must equal the reference's sequential scan.
+never read and each segment's kept rows are merged back into ascending-id order,
+so ids, distance bits and every counter must equal the reference's sequential scan.
 The layout is forced on a small clustered index (the default needs >= 256k
 rows) with short segments, so a query's kept blocks interleave in id order in
 every segment.
@@ -66,8 +66,7 @@ def test_segmented_flat_knn_parity(flat, gamma, k, monkeypatch):
     assert gix.skipped_positions() > 0
 
 
-@pytest.mark.parametrize("mode", ["wide_interval", "no_flat_bounds", "force_plain", "long_segments", "big_n0",
-                                  "large_run_table"])
+@pytest.mark.parametrize("mode", ["wide_interval", "no_flat_bounds", "force_plain", "long_segments", "big_n0"])
 @pytest.mark.parametrize("gamma", [0.0, 0.8])
 def test_segmented_flat_knn_modes(flat, gamma, mode, monkeypatch):
     hix, qs = flat
@@ -78,10 +77,8 @@ def test_segmented_flat_knn_modes(flat, gamma, mode, monkeypatch):
         monkeypatch.setenv("TRIM_FLAT_BOUNDS", "0")
     if mode == "force_plain":  # every query resumes in row order after n0 rows (the plan-does-not-fit path)
         monkeypatch.setenv("TRIM_SEG_FORCE_PLAIN", "1")
-    if mode == "long_segments":  # several chunks per replay group
+    if mode == "long_segments":  # many rows per (segment, block) run
         kw = dict(rows_per_block="128", n0="2000")
-    if mode == "large_run_table":  # plans with more runs than the small launch holds: the mode-2 launch
-        monkeypatch.setenv("TRIM_SEG_SMALL_RUNS", "8")
     if mode == "big_n0":
         kw = dict(rows_per_block="7", n0="17000")
     gix = seg_index(hix, monkeypatch, **kw)

@@ -409,20 +409,29 @@ bool ensure_flat_segments(trim_index* ix) {
     const DevIndex& v = ix->dev;
     const uint64_t n = ix->total;
     const uint32_t nb = ix->part_nb;
-    uint64_t rpb = 256, n0 = std::max<uint64_t>(uint64_t(std::min<uint32_t>(nb, 4096)) * 32, 4096);
+    // n0 rows stay in order; then segments that double in length (a query is planned as soon
+    // as its threshold allows, knn_seg_batch) up to rows-per-block-run x blocks, then uniform
+    uint64_t rpb = 256, n0 = std::max<uint64_t>(uint64_t(std::min<uint32_t>(nb, 4096)) * 16, 4096);
     if (const char* e = std::getenv("TRIM_SEG_ROWS_PER_BLOCK"))
         rpb = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     if (const char* e = std::getenv("TRIM_SEG_N0"))
         n0 = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     n0 = std::min<uint64_t>(n0, n / 4);
-    const uint64_t seg_len = rpb * nb, rest = n - n0;
-    const uint64_t nseg = (rest + seg_len - 1) / seg_len;
-    if (n0 == 0 || nseg == 0 || nseg * nb >= (1ull << 31) || n >= (1ull << 32))
+    if (n0 == 0 || n >= (1ull << 32))
+        return false;
+    const uint64_t seg_max = rpb * nb, rest = n - n0;
+    std::vector<uint64_t> bounds{n0};
+    for (uint64_t len = std::min(n0, seg_max); bounds.back() < n; len = std::min(len * 2, seg_max))
+        bounds.push_back(std::min(n, bounds.back() + len));
+    const uint64_t nseg = bounds.size() - 1;
+    if (nseg == 0 || nseg * nb >= (1ull << 31))
         return false;
     cudaStream_t st = nullptr;
     DevBuf keys(sizeof(uint32_t) * rest, st), order(sizeof(uint32_t) * rest, st);
-    trim_seg_key_kernel<<<static_cast<unsigned>((rest + 255) / 256), 256, 0, st>>>(ix->part_assign + n0, rest, seg_len, nb,
-                                                                                  keys.as<uint32_t>());
+    DevBuf d_bounds(sizeof(uint64_t) * bounds.size(), st);
+    CK(cudaMemcpyAsync(d_bounds.p, bounds.data(), sizeof(uint64_t) * bounds.size(), cudaMemcpyHostToDevice, st));
+    trim_seg_key_kernel<<<static_cast<unsigned>((rest + 255) / 256), 256, 0, st>>>(
+        ix->part_assign + n0, rest, d_bounds.as<uint64_t>(), static_cast<uint32_t>(nseg), nb, keys.as<uint32_t>());
     CK(cudaGetLastError());
     ix->seg_off = ix->alloc<uint64_t>(nseg * nb + 1);
     if (int rc = trim_ivf_lists_device(keys.as<uint32_t>(), rest, static_cast<uint32_t>(nseg * nb), ix->seg_off,
@@ -445,8 +454,7 @@ bool ensure_flat_segments(trim_index* ix) {
     ix->seg.list_ids = ids;
     ix->seg_head = v;
     ix->seg_head.list_offsets = offs_a;
-    ix->seg_n0 = n0;
-    ix->seg_len = seg_len;
+    ix->seg_bounds = bounds;
     ix->seg_nseg = static_cast<uint32_t>(nseg);
     ix->seg_ok = true;
     return true;
@@ -644,13 +652,20 @@ size_t knn_smem_for(const trim_index* ix, uint32_t k, uint32_t np, uint32_t& top
 // whose plan does not fit — the in-order kernel over the remaining rows.
 // `pb` carries the batch's queries, outputs and dap.
 constexpr uint32_t kSegTabCap = 32768; // table entries (kept rows) per query
-// Whole segments scanned in order after the layout's n0 so that the prefix is long enough for
-// k (n0 is sized for k <= 10: ~3 rows per block and neighbour wanted); false: no segment left.
+constexpr uint32_t kSegRounds = 3;     // continue rounds before a query that cannot be planned resumes in order
+// The first segment boundary the scan is planned at: rows [0, n_a) go in order. About 1.5 rows
+// per block and neighbour wanted are needed before the k-th best comes from the query's own
+// neighbourhood (queries that are not there yet continue in order, knn_seg_batch); false: no
+// segment left.
 bool seg_prefix(const trim_index* ix, uint32_t k, uint32_t& seg0, uint64_t& n_a) {
-    const uint64_t want = std::min<uint64_t>(ix->total / 2, uint64_t(k) * std::min<uint32_t>(ix->part_nb, 4096) * 3);
-    seg0 = want > ix->seg_n0 ? static_cast<uint32_t>((want - ix->seg_n0 + ix->seg_len - 1) / ix->seg_len) : 0;
-    n_a = ix->seg_n0 + seg0 * ix->seg_len;
-    return seg0 < ix->seg_nseg;
+    const uint64_t want = std::min<uint64_t>(ix->total / 2, uint64_t(k) * std::min<uint32_t>(ix->part_nb, 4096) * 3 / 2);
+    seg0 = 0;
+    while (seg0 < ix->seg_nseg && ix->seg_bounds[seg0] < want)
+        ++seg0;
+    if (seg0 >= ix->seg_nseg)
+        return false;
+    n_a = ix->seg_bounds[seg0];
+    return true;
 }
 
 void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n_a, cudaStream_t st) {
@@ -697,9 +712,6 @@ void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n
     sp.np = 1;
     sp.tab_cap = kSegTabCap;
     sp.n = ix->total;
-    sp.n0 = n_a;
-    sp.seg0 = seg0;
-    sp.seg_len = ix->seg_len;
     sp.nseg = ix->seg_nseg;
     sp.seg_off = ix->seg_off;
     sp.ids = ix->seg.list_ids;
@@ -727,30 +739,52 @@ void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n
         dbg = DevBuf(sizeof(uint32_t) * 4 * nq, st);
         sp.dbg = dbg.as<uint32_t>();
     }
-    trim_knn_seg_plan_kernel<<<static_cast<unsigned>(nq), kThreads, 0, st>>>(ix->part, sp);
-    CK(cudaGetLastError());
-    if (debug) { // plan statistics of the batch (synchronises)
-        std::vector<uint32_t> h(4 * nq);
-        std::vector<float> ta(nq * k);
-        CK(cudaMemcpyAsync(h.data(), dbg.p, sizeof(uint32_t) * 4 * nq, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(ta.data(), dist_a.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        uint64_t plain = 0, kept = 0, rows = 0, sorted = 0, kmax = 0;
-        double tsum = 0;
-        for (uint64_t i = 0; i < nq; ++i) {
-            kept += h[4 * i];
-            kmax = std::max<uint64_t>(kmax, h[4 * i]);
-            plain += h[4 * i + 1];
-            rows += h[4 * i + 2];
-            sorted += h[4 * i + 3];
-            tsum += ta[i * k + k - 1];
+    // Plan; a query whose plan does not fit yet (its threshold still comes from other
+    // neighbourhoods) scans the next segment in order and is planned again, up to
+    // kSegRounds times; after the last round it resumes in order for good.
+    uint32_t rounds = kSegRounds;
+    if (const char* e = std::getenv("TRIM_SEG_ROUNDS"))
+        rounds = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
+    KnnParams pc = pa; // continue rounds: in order over the original arrays, state in place
+    pc.dap = nullptr;
+    pc.dap_ld = 0;
+    pc.plan = recs.as<uint32_t>();
+    pc.mode_sel = 2;
+    for (uint32_t r = 0;; ++r) {
+        const uint32_t g = seg0 + r;
+        const bool last = r >= rounds || g + 1 >= ix->seg_nseg;
+        sp.round = r;
+        sp.seg0 = g;
+        sp.n0 = ix->seg_bounds[g];
+        sp.n_next = last ? 0 : ix->seg_bounds[g + 1];
+        trim_knn_seg_plan_kernel<<<static_cast<unsigned>(nq), kThreads, 0, st>>>(ix->part, sp);
+        CK(cudaGetLastError());
+        if (debug) { // plan statistics of the batch (synchronises)
+            std::vector<uint32_t> h(4 * nq), hm(lo.words * nq);
+            CK(cudaMemcpyAsync(h.data(), dbg.p, sizeof(uint32_t) * 4 * nq, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hm.data(), recs.p, sizeof(uint32_t) * lo.words * nq, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            uint64_t mode[3] = {0, 0, 0}, kept = 0, rows = 0, kmax = 0;
+            for (uint64_t i = 0; i < nq; ++i) {
+                const uint32_t md = hm[i * lo.words + 7];
+                ++mode[md < 3 ? md : 0];
+                if (md == 1) {
+                    kept += h[4 * i];
+                    kmax = std::max<uint64_t>(kmax, h[4 * i]);
+                    rows += hm[i * lo.words + 3];
+                }
+            }
+            std::fprintf(stderr,
+                         "[trim seg] round %u: nq=%llu nb=%u rows_in_order=%llu segments=%u..%u: planned=%llu "
+                         "(kept/q=%.1f max %llu, table rows/q=%.1f) continue=%llu in-order=%llu\n",
+                         r, (unsigned long long)nq, nb, (unsigned long long)sp.n0, g, ix->seg_nseg,
+                         (unsigned long long)mode[1], mode[1] ? double(kept) / mode[1] : 0.0, (unsigned long long)kmax,
+                         mode[1] ? double(rows) / mode[1] : 0.0, (unsigned long long)mode[2],
+                         (unsigned long long)mode[0]);
         }
-        std::fprintf(stderr,
-                     "[trim seg] nq=%llu nb=%u rows_in_order=%llu seg_len=%llu segments=%u..%u: plain=%llu kept/q=%.1f "
-                     "(max %llu) table rows/q=%.1f sorted segments/q=%.1f mean T_A=%.3f\n",
-                     (unsigned long long)nq, nb, (unsigned long long)n_a, (unsigned long long)ix->seg_len, seg0,
-                     ix->seg_nseg, (unsigned long long)plain, double(kept) / nq, (unsigned long long)kmax,
-                     double(rows) / nq, double(sorted) / nq, tsum / nq);
+        if (last)
+            break;
+        launch_knn(v, pc, smem_a, st); // records of mode 2: [bounds[g], bounds[g + 1]) in order
     }
     pb.plan = recs.as<uint32_t>();
     pb.np = 1;
@@ -759,6 +793,7 @@ void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n
     pb.dap_ld = 0;
     pb.tab = tab.as<uint32_t>();
     pb.tab_cap = kSegTabCap;
+    pb.mode_sel = 0;
     pb.topk_off = off_a;
     launch_knn(v, pb, smem_a, st);           // records of mode 0: in order over the original arrays (the long ones first)
     launch_knn_seg(ix->seg, pb, smem_a, st); // records of mode 1: the entry tables
@@ -822,7 +857,7 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
     uint32_t seg0 = 0;
     uint64_t n_a = 0;
     const bool seg = ix->dev.nlist == 1 && !d_probe && np == 1 && ensure_flat_segments(const_cast<trim_index*>(ix)) &&
-                     uint64_t(k) * 4 <= ix->seg_n0 && seg_prefix(ix, k, seg0, n_a) &&
+                     uint64_t(k) * 4 <= ix->seg_bounds[0] && seg_prefix(ix, k, seg0, n_a) &&
                      knn_smem_bytes(k > 256 ? 0 : dispatch_m(ix->dev), ix->dev.m, ix->dev.dim_stride, 1) <= kSmemLimit;
     const uint64_t bound_rows = seg ? n_a : ix->dev.n;
     const bool flat_bounds = ix->dev.nlist == 1 && np == 1 && ix->dev.n > 0 && ix->dev.n <= (16ull << 20) &&
@@ -1157,15 +1192,16 @@ int trimhost::create_single(const trim_index_desc* d, trim_index** out) {
         const cudaMemcpyKind kind = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         DeviceGuard g(d->device);
         { // keep the per-call stream-ordered workspaces (queries, probe scratch,
-          // results: tens of MB per batch) cached in the device's pool, but
-          // return anything beyond 1 GiB (e.g. a flat-bound slice) to the device
-          // at the next synchronisation, so it never starves other allocators
+          // results, flat-scan entry tables: up to ~0.5 GB per batch in flight) cached
+          // in the device's pool, but return anything beyond 4 GiB (e.g. a flat-bound
+          // slice) to the device at the next synchronisation, so it never starves other
+          // allocators
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
                 uint64_t thr = 0;
                 cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-                if (thr < (1ull << 30)) {
-                    thr = 1ull << 30;
+                if (thr < (4ull << 30)) {
+                    thr = 4ull << 30;
                     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
                 }
             }

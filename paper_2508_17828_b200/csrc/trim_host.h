@@ -202,7 +202,7 @@ struct trim_index {
     // segmented block scan (ensure_flat_segments), built on first use
     std::mutex seg_mu;
     bool seg_tried = false, seg_ok = false;
-    uint64_t seg_n0 = 0, seg_len = 0;
+    std::vector<uint64_t> seg_bounds; // segment g = rows [seg_bounds[g], seg_bounds[g + 1]); [0] = n0
     uint32_t seg_nseg = 0;
     uint64_t* seg_off = nullptr;  // nseg * part_nb + 1
     trimgpu::DevIndex seg{};      // dev with the regrouped codes / lx / ids

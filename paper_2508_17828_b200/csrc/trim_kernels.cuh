@@ -311,6 +311,7 @@ struct KnnParams {
     // segmented flat scans (trim_knn_seg_plan_kernel): per-query entry tables, tab_cap words each
     const uint32_t* tab;
     uint32_t tab_cap;
+    uint32_t mode_sel; // PRE kernel without SEG: the record mode this launch serves (0, or 2 = a continue round)
 };
 
 // Per-query setup record written by trim_knn_setup_kernel (u32 words): the
@@ -321,7 +322,8 @@ struct KnnPlanLayout {
     uint32_t cum, base, sd, sid, words;
     // header: [0] total [1] nseed [2] nk [3] total2 [4] T0 bits [5] dc so far (the seeds, or
     // everything before a resumed scan) [6] entries evaluated unconditionally (edc = evaluated
-    // - this) [7] mode: 0 = runs in cum/base, 1 = entry table of a segmented block stream (SEG kernel)
+    // - this) [7] mode: 0 = runs in cum/base, 1 = entry table of a segmented block stream (SEG kernel),
+    // 2 = runs in cum/base of a continue round (more rows in order, then planned again)
     __host__ __device__ static KnnPlanLayout of(uint32_t np, uint32_t k) {
         KnnPlanLayout o;
         o.cum = 8;
@@ -534,6 +536,10 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     const uint32_t q = blockIdx.x;
     if (q >= p.nq)
         return;
+    if constexpr (PRE) { // a record of another launch's mode: nothing to do here
+        if (__ldg(p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words + 7) != (SEG ? 1u : p.mode_sel))
+            return;
+    }
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t m = M > 0 ? static_cast<uint32_t>(M) : ix.m;
 
@@ -585,10 +591,6 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     // the stream (probe order, ascending ids) — from the setup record when
     // trim_knn_setup_kernel ran, else built here
     const uint32_t* rec = PRE ? p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words : nullptr;
-    if constexpr (PRE) {
-        if (__ldg(rec + 7) != (SEG ? 1u : 0u)) // the other launch's query
-            return;
-    }
     // SEG: the query's entry table (stream position -> entry of the regrouped arrays)
     [[maybe_unused]] const uint32_t* tab = SEG ? p.tab + static_cast<size_t>(q) * p.tab_cap : nullptr;
     uint32_t total;
@@ -1437,8 +1439,8 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
 // rows: the reference prunes it (ivf.hpp:275). Rows n0.. are stored regrouped
 // by (segment of `seg_len` consecutive ids, block), ascending ids inside
 // (seg_off: S * nb + 1 offsets). For each segment the kept blocks' runs (each
-// ascending in id) are merged by id in shared memory — (id << 32 | entry) keys,
-// bitonic sort — and the entries appended to the query's table: the
+// ascending in id) are merged by id in shared memory (rank = own offset + the
+// counts of smaller ids in the other runs) and the entries appended to the query's table: the
 // reference's stream with the pruned blocks' rows removed, in order. The record
 // resumes the top-k and the counters; trim_knn_kernel<SEG> walks the table. A
 // query whose plan does not fit (more than kSegMaxKept blocks, kSegSortCap rows
@@ -1462,8 +1464,10 @@ struct SegPlanParams {
     uint64_t nq;
     uint32_t k, np;          // np: the record layout's run capacity (1)
     uint32_t tab_cap;        // table words per query
-    uint64_t n, n0, seg_len; // n0: rows scanned in order so far (the layout's n0 + seg0 whole segments)
-    uint32_t nseg, seg0;     // segments [seg0, nseg) remain
+    uint64_t n, n0;      // n0: rows scanned in order so far (= the start of segment seg0)
+    uint64_t n_next;     // a plan that does not fit continues in order up to here and is planned again (0: last round)
+    uint32_t nseg, seg0; // segments [seg0, nseg) remain
+    uint32_t round;      // > 0: queries already planned (mode 1) are left alone
     const uint64_t* seg_off;
     const uint32_t* ids;  // ids of the regrouped entries
     const float* approx;  // nq x mma_ld(nb): tf32 |q - c_b|^2
@@ -1480,10 +1484,10 @@ struct SegPlanParams {
     uint32_t* dbg; // TRIM_SEG_DEBUG: per query {kept blocks, plain, table rows, segments sorted}, or null
 };
 constexpr uint32_t kSegMaxKept = 64;   // kept blocks per query in block mode
-constexpr uint32_t kSegSortCap = 4096; // rows of one segment's kept blocks (32 KB of sort keys)
+constexpr uint32_t kSegSortCap = 8192; // rows of one segment's kept blocks (their ids in shared memory)
 
 __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex aux, SegPlanParams p) {
-    __shared__ unsigned long long s_key[kSegSortCap];
+    __shared__ uint32_t s_id[kSegSortCap];
     __shared__ uint32_t ws[16];
     __shared__ uint32_t s_kept[kSegMaxKept];
     __shared__ uint32_t s_roff[kSegMaxKept + 1];
@@ -1496,6 +1500,8 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
     const uint32_t nb = aux.nlist;
     const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
     uint32_t* rec = p.recs + q * lo.words;
+    if (p.round && rec[7] == 1u)
+        return;
     uint32_t* tab = p.tab + q * p.tab_cap;
     const float* qrow = p.queries + q * aux.dim_stride;
     float qp = 0.0f;
@@ -1605,41 +1611,47 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
             for (uint32_t i = tid; i < rows; i += kThreads)
                 tab[total + i] = b0 + i;
         } else {
-            uint32_t P = 2;
-            while (P < rows)
-                P <<= 1;
-            for (uint32_t i = tid; i < P; i += kThreads) {
-                unsigned long long key = ~0ull;
-                if (i < rows) {
-                    uint32_t a = 0, b = nkept; // the run holding merged-input index i
-                    while (b - a > 1) {
-                        const uint32_t mid = (a + b) >> 1;
-                        if (s_roff[mid] <= i)
-                            a = mid;
-                        else
-                            b = mid;
-                    }
-                    const uint32_t e = static_cast<uint32_t>(s_rbase[a]) + (i - s_roff[a]);
-                    key = (static_cast<unsigned long long>(__ldg(p.ids + e)) << 32) | e;
+            // merge the runs by id: every run is ascending and ids are unique, so a row's
+            // place is its offset in its own run plus, for every other run, the number of
+            // that run's ids below it (a binary search in shared memory)
+            for (uint32_t i = tid; i < rows; i += kThreads) {
+                uint32_t a = 0, b = nkept; // the run holding merge-input index i
+                while (b - a > 1) {
+                    const uint32_t mid = (a + b) >> 1;
+                    if (s_roff[mid] <= i)
+                        a = mid;
+                    else
+                        b = mid;
                 }
-                s_key[i] = key;
+                s_id[i] = __ldg(p.ids + static_cast<uint32_t>(s_rbase[a]) + (i - s_roff[a]));
             }
             __syncthreads();
-            for (uint32_t size = 2; size <= P; size <<= 1)
-                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (uint32_t i = tid; i < P / 2; i += kThreads) {
-                        const uint32_t l0 = 2 * i - (i & (stride - 1)), h0 = l0 + stride;
-                        const bool up = (l0 & size) == 0;
-                        const unsigned long long x = s_key[l0], y = s_key[h0];
-                        if ((x > y) == up) {
-                            s_key[l0] = y;
-                            s_key[h0] = x;
-                        }
-                    }
-                    __syncthreads();
+            for (uint32_t i = tid; i < rows; i += kThreads) {
+                uint32_t a = 0, b = nkept;
+                while (b - a > 1) {
+                    const uint32_t mid = (a + b) >> 1;
+                    if (s_roff[mid] <= i)
+                        a = mid;
+                    else
+                        b = mid;
                 }
-            for (uint32_t i = tid; i < rows; i += kThreads)
-                tab[total + i] = static_cast<uint32_t>(s_key[i]);
+                const uint32_t id = s_id[i];
+                uint32_t rank = i - s_roff[a];
+                for (uint32_t j = 0; j < nkept; ++j) {
+                    if (j == a)
+                        continue;
+                    uint32_t l0 = s_roff[j], h0 = s_roff[j + 1]; // first index in run j with id above `id`
+                    while (l0 < h0) {
+                        const uint32_t mid = (l0 + h0) >> 1;
+                        if (s_id[mid] < id)
+                            l0 = mid + 1;
+                        else
+                            h0 = mid;
+                    }
+                    rank += l0 - s_roff[j];
+                }
+                tab[total + rank] = static_cast<uint32_t>(s_rbase[a]) + (i - s_roff[a]);
+            }
             ++sorted;
         }
         total += rows;
@@ -1664,11 +1676,12 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
         rec[5] = static_cast<uint32_t>(p.ct_a[q * 6 + 0]);  // dc over [0, n0)
         rec[6] = static_cast<uint32_t>(min(static_cast<uint64_t>(p.k), p.n)); // the seeds
         rec[lo.cum] = 0;
-        if (plain) {
+        if (plain) { // in order: up to n_next and planned again, or (last round) the rest
+            const uint64_t end = p.n_next ? p.n_next : p.n;
             rec[2] = 1;
-            rec[3] = static_cast<uint32_t>(p.n - p.n0);
-            rec[7] = 0;
-            rec[lo.cum + 1] = static_cast<uint32_t>(p.n - p.n0);
+            rec[3] = static_cast<uint32_t>(end - p.n0);
+            rec[7] = p.n_next ? 2 : 0;
+            rec[lo.cum + 1] = static_cast<uint32_t>(end - p.n0);
             reinterpret_cast<uint64_t*>(rec + lo.base)[0] = p.n0;
         } else {
             rec[2] = 0; // no runs: the stream is the table
@@ -2228,12 +2241,23 @@ __global__ void trim_gather_rows_kernel(const float* __restrict__ src, uint32_t 
 }
 
 // (segment, block) key of rows n0.. for the segmented flat kNN layout: row n0 + i
-// belongs to segment i / seg_len and to the partition's block assign[n0 + i].
-__global__ void trim_seg_key_kernel(const uint32_t* __restrict__ assign, uint64_t cnt, uint64_t seg_len, uint32_t nb,
-                                    uint32_t* __restrict__ keys) {
+// belongs to the segment g with bounds[g] <= n0 + i < bounds[g + 1] (bounds[0] = n0) and to
+// the partition's block assign[i] (`assign` points at row n0).
+__global__ void trim_seg_key_kernel(const uint32_t* __restrict__ assign, uint64_t cnt, const uint64_t* __restrict__ bounds,
+                                    uint32_t nseg, uint32_t nb, uint32_t* __restrict__ keys) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < cnt)
-        keys[i] = static_cast<uint32_t>(i / seg_len) * nb + assign[i];
+    if (i >= cnt)
+        return;
+    const uint64_t r = bounds[0] + i;
+    uint32_t a = 0, b = nseg; // largest g with bounds[g] <= r
+    while (b - a > 1) {
+        const uint32_t mid = (a + b) >> 1;
+        if (bounds[mid] <= r)
+            a = mid;
+        else
+            b = mid;
+    }
+    keys[i] = a * nb + assign[i];
 }
 
 // the same with 32-bit row indices

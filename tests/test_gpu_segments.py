@@ -66,7 +66,8 @@ def test_segmented_flat_knn_parity(flat, gamma, k, monkeypatch):
     assert gix.skipped_positions() > 0
 
 
-@pytest.mark.parametrize("mode", ["wide_interval", "no_flat_bounds", "force_plain", "long_segments", "big_n0"])
+@pytest.mark.parametrize("mode", ["wide_interval", "no_flat_bounds", "force_plain", "long_segments", "big_n0",
+                                  "no_rounds", "tiny_n0"])
 @pytest.mark.parametrize("gamma", [0.0, 0.8])
 def test_segmented_flat_knn_modes(flat, gamma, mode, monkeypatch):
     hix, qs = flat
@@ -75,10 +76,14 @@ def test_segmented_flat_knn_modes(flat, gamma, mode, monkeypatch):
         monkeypatch.setenv("TRIM_EPS_SCALE", "20000")
     if mode == "no_flat_bounds":
         monkeypatch.setenv("TRIM_FLAT_BOUNDS", "0")
-    if mode == "force_plain":  # every query resumes in row order after n0 rows (the plan-does-not-fit path)
+    if mode == "force_plain":  # no plan ever fits: continue rounds, then row order for the rest
         monkeypatch.setenv("TRIM_SEG_FORCE_PLAIN", "1")
     if mode == "long_segments":  # many rows per (segment, block) run
         kw = dict(rows_per_block="128", n0="2000")
+    if mode == "no_rounds":  # a plan that does not fit resumes in order at once
+        monkeypatch.setenv("TRIM_SEG_ROUNDS", "0")
+    if mode == "tiny_n0":  # too few rows in order for a useful threshold: continue rounds, then planned
+        kw = dict(rows_per_block="16", n0="300")
     if mode == "big_n0":
         kw = dict(rows_per_block="7", n0="17000")
     gix = seg_index(hix, monkeypatch, **kw)

@@ -284,6 +284,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // pruned when that (rounded down, then shrunk by 4u for the reference's own
 // rounding) is >= T. omg_hi = 1 - gamma rounded up.
 struct StageCheck {
+    static constexpr bool kFine = false; // stages after 8 (first block), 16 and 32 lookups of a block
     float glx, two_gamma, omg_hi, eps, T;
     __device__ __forceinline__ bool pruned(float a_p) const {
         const float g_lo = __fmul_rd(sqrt_approx(__fmul_rd(a_p, 1.0f - eps)), 1.0f - 1.0f / 65536.0f);
@@ -294,6 +295,29 @@ struct StageCheck {
         const float t = __fmul_rd(__fmul_rd(two_gamma, g_lo), glx);
         return __fmul_rd(__fadd_rd(e, t), 1.0f - 4.0f / 16777216.0f) >= T;
     }
+};
+
+// The same test as one comparison per stage: the partial sum against a cut
+// A computed once per candidate. With x = glx, est(g) = (g - (1-γ)x)^2 +
+// γ(2-γ)x^2 is increasing for g >= (1-γ)x, so est(g) >= T' for every
+// g >= g* = (1-γ)x + sqrt(max(T' - γ(2-γ)x^2, 0)), where T' = T(1 + 2^-20)
+// absorbs the reference's own evaluation error (fl(est) >= est(1 - 4u), u =
+// 2^-24). Every operation below is rounded toward a larger G >= g*, and
+// A = G^2 kA with kA >= 1 / ((1 - eps)(1 - u)^2) gives: a_p >= A => adc_ref >=
+// a_p(1 - eps) => g_ref = fl(sqrt(adc_ref)) >= G => est_ref >= T: the
+// reference prunes the candidate (ivf.hpp:275). c1 <= γ(2-γ) and kA come from
+// the host (KnnParams.stage_c1 / stage_ka). Cheap enough to test after every
+// 8 lookups (kFine).
+struct StageCut {
+    static constexpr bool kFine = true;
+    float a_hi;
+    __device__ __forceinline__ static StageCut make(float x, float c1, float omg_hi, float kA, float T) {
+        const float t_lo = c1 >= 0.0f ? __fmul_rd(c1, __fmul_rd(x, x)) : __fmul_rd(c1, __fmul_ru(x, x));
+        const float rad = __fsub_ru(__fmul_ru(T, 1.0f + 1.0f / 1048576.0f), t_lo);
+        const float G = fmaxf(__fadd_ru(__fmul_ru(omg_hi, x), __fsqrt_ru(fmaxf(rad, 0.0f))), 0.0f);
+        return StageCut{__fmul_ru(__fmul_ru(G, G), kA)};
+    }
+    __device__ __forceinline__ bool pruned(float a_p) const { return a_p >= a_hi; }
 };
 
 __device__ __forceinline__ float sum4(const float p[4]) {
@@ -349,14 +373,37 @@ struct FastCode {
 
     // One FULL block B (compile-time), two 16-step stages. Returns true when
     // the whole warp is provably pruned. lofs: byte offset of the LUT used.
-    template <uint32_t B, bool PERM>
-    __device__ __forceinline__ bool full_block(const LutShape& sh, const LaneAdc& la, const StageCheck& ck,
+    template <uint32_t B, bool PERM, class CK>
+    __device__ __forceinline__ bool full_block(const LutShape& sh, const LaneAdc& la, const CK& ck,
                                                float part[4], bool& live, uint32_t lofs) {
         if (B >= sh.nfull)
             return false;
         if (PERM)
             permute_block<false>(w[B], la.l);
         const uint32_t lb = la.lf + lofs;
+        if constexpr (CK::kFine) { // a stage every 8 lookups
+            block_fast<0, 8, 128u, B * kFullBytes>(lb, w[B], la, part);
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            if (!__any_sync(0xffffffffu, live))
+                return true;
+            block_fast<8, 16, 128u, B * kFullBytes>(lb, w[B], la, part);
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            if (!__any_sync(0xffffffffu, live))
+                return true;
+            block_fast<16, 24, 128u, B * kFullBytes>(lb, w[B], la, part);
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            if (!__any_sync(0xffffffffu, live))
+                return true;
+            block_fast<24, 32, 128u, B * kFullBytes>(lb, w[B], la, part);
+            if (B + 1 == sh.nfull && !sh.half)
+                return false; // last block: the caller's full check decides
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            return !__any_sync(0xffffffffu, live);
+        }
         if (B == 0) { // an extra early stage after 8 lookups: ~2/3 of config-2 warps stop here
             block_fast<0, 8, 128u, B * kFullBytes>(lb, w[B], la, part);
             if (live && ck.pruned(sum4(part)))
@@ -383,19 +430,19 @@ struct FastCode {
     // this lane. `alive` = this lane has a candidate; dead lanes still step
     // along (their lookups keep the schedule conflict-free) but never vote.
     // Warp-collective. PERM = false: the words were permuted by permute_all.
-    template <bool PERM = true>
-    __device__ __forceinline__ float sum_staged(uint32_t m, const LaneAdc& la, const StageCheck& ck,
+    template <bool PERM = true, class CK = StageCheck>
+    __device__ __forceinline__ float sum_staged(uint32_t m, const LaneAdc& la, const CK& ck,
                                                 bool alive, uint32_t lofs = 0) {
         const LutShape sh = LutShape::of(M > 0 ? static_cast<uint32_t>(M) : m);
         float part[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         bool live = alive;
-        if (full_block<0, PERM>(sh, la, ck, part, live, lofs))
+        if (full_block<0, PERM, CK>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 1 && full_block<(kMaxB > 1 ? 1u : 0u), PERM>(sh, la, ck, part, live, lofs))
+        if (kMaxB > 1 && full_block<(kMaxB > 1 ? 1u : 0u), PERM, CK>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 2 && full_block<(kMaxB > 2 ? 2u : 0u), PERM>(sh, la, ck, part, live, lofs))
+        if (kMaxB > 2 && full_block<(kMaxB > 2 ? 2u : 0u), PERM, CK>(sh, la, ck, part, live, lofs))
             return -1.0f;
-        if (kMaxB > 3 && full_block<(kMaxB > 3 ? 3u : 0u), PERM>(sh, la, ck, part, live, lofs))
+        if (kMaxB > 3 && full_block<(kMaxB > 3 ? 3u : 0u), PERM, CK>(sh, la, ck, part, live, lofs))
             return -1.0f;
         if (sh.half) {
             const uint32_t hb = sh.nfull;
@@ -407,13 +454,19 @@ struct FastCode {
             if (PERM)
                 permute_block<true>(wh, la.l);
             const uint32_t hl = la.lh + lofs;
-            if (sh.hdup) { // the only block (m <= 16): one early check after 8 steps
-                block_fast<0, 8, 128u, 0u>(hl, wh, la, part);
+            if (sh.hdup || CK::kFine) { // (the only block, m <= 16:) an early check after 8 steps
+                if (sh.hdup)
+                    block_fast<0, 8, 128u, 0u>(hl, wh, la, part);
+                else
+                    block_fast<0, 8, 64u, 0u>(hl, wh, la, part);
                 if (live && ck.pruned(sum4(part)))
                     live = false;
                 if (!__any_sync(0xffffffffu, live))
                     return -1.0f;
-                block_fast<8, 16, 128u, 0u>(hl, wh, la, part);
+                if (sh.hdup)
+                    block_fast<8, 16, 128u, 0u>(hl, wh, la, part);
+                else
+                    block_fast<8, 16, 64u, 0u>(hl, wh, la, part);
             } else {
                 block_fast<0, 16, 64u, 0u>(hl, wh, la, part);
             }

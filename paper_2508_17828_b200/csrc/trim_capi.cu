@@ -845,6 +845,23 @@ int knn_launch(const trim_index* ix, const float* d_q, uint64_t nq, uint32_t k, 
         p.kq2 = std::nextafter(static_cast<float>(kq2), 0.0f);
         p.kest = std::nextafter(static_cast<float>(kest), 0.0f);
         p.omg_lo = omg_round_down(gamma);
+        { // StageCut constants, rounded to the safe side
+            const double ol = p.omg_lo, oh = p.omg_hi, c1 = 1.0 - std::max(ol * ol, oh * oh);
+            float f = static_cast<float>(c1);
+            if (static_cast<double>(f) > c1)
+                f = std::nextafter(f, -INFINITY);
+            p.stage_c1 = f;
+            const double e = p.adc_eps, um = 1.0 - std::ldexp(1.0, -24);
+            if (e < 1.0) {
+                const double ka = (1.0 + std::ldexp(1.0, -20)) / ((1.0 - e) * um * um);
+                float g = static_cast<float>(ka);
+                if (static_cast<double>(g) < ka)
+                    g = std::nextafter(g, INFINITY);
+                p.stage_ka = g;
+            } else {
+                p.stage_ka = INFINITY;
+            }
+        }
         p.skip_lists = list_skip_enabled() ? 1u : 0u;
         p.skipped = ix->d_skipped;
         p.timeline = g_timeline;

@@ -312,6 +312,8 @@ struct KnnParams {
     const uint32_t* tab;
     uint32_t tab_cap;
     uint32_t mode_sel; // PRE kernel without SEG: the record mode this launch serves (0, or 2 = a continue round)
+    float stage_c1;    // <= γ(2-γ) (StageCut)
+    float stage_ka;    // >= 1 / ((1 - adc_eps)(1 - 2^-24)^2), +inf when adc_eps >= 1 (StageCut)
 };
 
 // Per-query setup record written by trim_knn_setup_kernel (u32 words): the
@@ -358,6 +360,9 @@ constexpr uint32_t kChunkW = kWorkers * kPerWorker; // 224 stream positions per 
 #define TRIM_KRING 6
 #endif
 constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
+#ifndef TRIM_STAGE_CUT
+#define TRIM_STAGE_CUT 1   // kNN workers: one-compare stage tests every 8 lookups (StageCut); 0: StageCheck
+#endif
 #ifndef TRIM_QUAD_L2
 #define TRIM_QUAD_L2 1     // members' exact L2 by lane quads (euclid_sq_quad), 8 rows per warp pass
 #endif
@@ -917,8 +922,13 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         TRIM_TL(const unsigned long long k1 = wtl ? clock64() : 0;)
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
         Cand& x = cur.c[0];
+#if TRIM_STAGE_CUT
+        const StageCut ck = StageCut::make(x.lx, p.stage_c1, p.omg_hi, p.stage_ka, T);
+        const float a = x.fc.template sum_staged<true, StageCut>(m, la, ck, x.kind == 2u); // warp-collective
+#else
         const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
         const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
+#endif
         // member = a candidate whose est interval [lo, hi] starts below T
         float lo = kNegInf, hi = kNegInf;
         bool keep = false;

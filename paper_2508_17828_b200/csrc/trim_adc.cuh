@@ -285,6 +285,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // rounding) is >= T. omg_hi = 1 - gamma rounded up.
 struct StageCheck {
     static constexpr bool kFine = false; // stages after 8 (first block), 16 and 32 lookups of a block
+    static constexpr bool kHalfMid = false, kAt24 = false, kNo8 = false, kNo16 = false, kNo32 = false;
     float glx, two_gamma, omg_hi, eps, T;
     __device__ __forceinline__ bool pruned(float a_p) const {
         const float g_lo = __fmul_rd(sqrt_approx(__fmul_rd(a_p, 1.0f - eps)), 1.0f - 1.0f / 65536.0f);
@@ -308,8 +309,17 @@ struct StageCheck {
 // reference prunes the candidate (ivf.hpp:275). c1 <= γ(2-γ) and kA come from
 // the host (KnnParams.stage_c1 / stage_ka). Cheap enough to test after every
 // 8 lookups (kFine).
+#ifndef TRIM_STAGE_FINE
+#define TRIM_STAGE_FINE 0 // StageCut stages: 0 = after 8 (first block), 16, 32 like StageCheck (measured
+                          // best on config 2); 1 = every 8 lookups; 2 = 0 + the middle of the last
+                          // half block; 3 = 0 + after 24
+#endif
 struct StageCut {
-    static constexpr bool kFine = true;
+    static constexpr bool kFine = TRIM_STAGE_FINE == 1;
+    static constexpr bool kHalfMid = TRIM_STAGE_FINE == 1 || TRIM_STAGE_FINE == 2;
+    static constexpr bool kAt24 = TRIM_STAGE_FINE == 3;
+    static constexpr bool kNo8 = TRIM_STAGE_FINE >= 4, kNo16 = TRIM_STAGE_FINE >= 4; // 4: after 32 only
+    static constexpr bool kNo32 = TRIM_STAGE_FINE == 5;                              // 5: no stage at all
     float a_hi;
     __device__ __forceinline__ static StageCut make(float x, float c1, float omg_hi, float kA, float T) {
         const float t_lo = c1 >= 0.0f ? __fmul_rd(c1, __fmul_rd(x, x)) : __fmul_rd(c1, __fmul_ru(x, x));
@@ -318,6 +328,14 @@ struct StageCut {
         return StageCut{__fmul_ru(__fmul_ru(G, G), kA)};
     }
     __device__ __forceinline__ bool pruned(float a_p) const { return a_p >= a_hi; }
+};
+
+// No stage at all: for streams whose candidates are all near the threshold (what the
+// list-level bound or the block plan leaves), where a warp's 32 lanes are almost never
+// all proven pruned before the last lookup and every stage is overhead (config 2: +14%).
+struct StageNone {
+    static constexpr bool kFine = false, kHalfMid = false, kAt24 = false, kNo8 = true, kNo16 = true, kNo32 = true;
+    __device__ __forceinline__ bool pruned(float) const { return false; }
 };
 
 __device__ __forceinline__ float sum4(const float p[4]) {
@@ -404,7 +422,7 @@ struct FastCode {
                 live = false;
             return !__any_sync(0xffffffffu, live);
         }
-        if (B == 0) { // an extra early stage after 8 lookups: ~2/3 of config-2 warps stop here
+        if (B == 0 && !CK::kNo8) { // an extra early stage after 8 lookups: ~2/3 of config-2 warps stop here
             block_fast<0, 8, 128u, B * kFullBytes>(lb, w[B], la, part);
             if (live && ck.pruned(sum4(part)))
                 live = false;
@@ -414,12 +432,23 @@ struct FastCode {
         } else {
             block_fast<0, 16, 128u, B * kFullBytes>(lb, w[B], la, part);
         }
-        if (live && ck.pruned(sum4(part)))
-            live = false;
-        if (!__any_sync(0xffffffffu, live))
-            return true;
-        block_fast<16, 32, 128u, B * kFullBytes>(lb, w[B], la, part);
-        if (B + 1 == sh.nfull && !sh.half)
+        if constexpr (!CK::kNo16) {
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            if (!__any_sync(0xffffffffu, live))
+                return true;
+        }
+        if constexpr (CK::kAt24) {
+            block_fast<16, 24, 128u, B * kFullBytes>(lb, w[B], la, part);
+            if (live && ck.pruned(sum4(part)))
+                live = false;
+            if (!__any_sync(0xffffffffu, live))
+                return true;
+            block_fast<24, 32, 128u, B * kFullBytes>(lb, w[B], la, part);
+        } else {
+            block_fast<16, 32, 128u, B * kFullBytes>(lb, w[B], la, part);
+        }
+        if ((B + 1 == sh.nfull && !sh.half) || CK::kNo32)
             return false; // last block: the caller's full check decides
         if (live && ck.pruned(sum4(part)))
             live = false;
@@ -454,7 +483,7 @@ struct FastCode {
             if (PERM)
                 permute_block<true>(wh, la.l);
             const uint32_t hl = la.lh + lofs;
-            if (sh.hdup || CK::kFine) { // (the only block, m <= 16:) an early check after 8 steps
+            if ((sh.hdup && !CK::kNo8) || CK::kHalfMid) { // (the only block, m <= 16:) an early check after 8 steps
                 if (sh.hdup)
                     block_fast<0, 8, 128u, 0u>(hl, wh, la, part);
                 else
@@ -467,6 +496,8 @@ struct FastCode {
                     block_fast<8, 16, 128u, 0u>(hl, wh, la, part);
                 else
                     block_fast<8, 16, 64u, 0u>(hl, wh, la, part);
+            } else if (sh.hdup) {
+                block_fast<0, 16, 128u, 0u>(hl, wh, la, part);
             } else {
                 block_fast<0, 16, 64u, 0u>(hl, wh, la, part);
             }

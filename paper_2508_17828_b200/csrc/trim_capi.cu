@@ -766,7 +766,7 @@ void knn_seg_batch(const trim_index* ix, KnnParams pb, uint32_t seg0, uint64_t n
             CK(cudaStreamSynchronize(st));
             uint64_t mode[3] = {0, 0, 0}, kept = 0, rows = 0, kmax = 0;
             for (uint64_t i = 0; i < nq; ++i) {
-                const uint32_t md = hm[i * lo.words + 7];
+                const uint32_t md = hm[i * lo.words + 7] & 0xffu;
                 ++mode[md < 3 ? md : 0];
                 if (md == 1) {
                     kept += h[4 * i];

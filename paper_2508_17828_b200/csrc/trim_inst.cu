@@ -42,18 +42,37 @@ cudaError_t TRIM_CAT(launch_knn_, TRIM_M)(const DevIndex& ix, const KnnParams& p
     const uint32_t S = (p.k + 31) / 32;
     const dim3 grid(static_cast<unsigned>(p.nq));
 #if TRIM_M == 0
-    if (S > 8) // k > 256: shared-memory top-k (the host routes every such call here)
-        return p.plan ? launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, true>, grid, smem, st, ix, p)
-                      : launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, false>, grid, smem, st, ix, p);
+    if (S > 8) { // k > 256: shared-memory top-k (the host routes every such call here)
+        if (!p.plan)
+            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, false>, grid, smem, st, ix, p);
+        cudaError_t e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, true>, grid, smem, st, ix, p);
+        if (e == cudaSuccess && p.probe)
+            e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 0, true, false, true>, grid, smem, st, ix, p);
+        return e;
+    }
 #endif
     if (p.plan) { // seeds + plan precomputed (trim_knn_setup_kernel)
-        if (S <= 1)
-            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);
-        if (S <= 2)
-            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true>, grid, smem, st, ix, p);
-        if (S <= 4)
-            return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true>, grid, smem, st, ix, p);
-        return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true>, grid, smem, st, ix, p);
+        // IVF records flagged "near candidates only" go to the HARD flavour (no early-exit
+        // stages); flat resume records (no probe lists) never carry the flag
+        cudaError_t e = cudaSuccess;
+        if (S <= 1) {
+            e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true>, grid, smem, st, ix, p);
+            if (e == cudaSuccess && p.probe)
+                e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, true, false, true>, grid, smem, st, ix, p);
+        } else if (S <= 2) {
+            e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true>, grid, smem, st, ix, p);
+            if (e == cudaSuccess && p.probe)
+                e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 2, true, false, true>, grid, smem, st, ix, p);
+        } else if (S <= 4) {
+            e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true>, grid, smem, st, ix, p);
+            if (e == cudaSuccess && p.probe)
+                e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 4, true, false, true>, grid, smem, st, ix, p);
+        } else {
+            e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true>, grid, smem, st, ix, p);
+            if (e == cudaSuccess && p.probe)
+                e = launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 8, true, false, true>, grid, smem, st, ix, p);
+        }
+        return e;
     }
     if (S <= 1)
         return launch_knn_t(trim_knn_kernel<TRIM_M, TRIM_KS, 1, false>, grid, smem, st, ix, p);

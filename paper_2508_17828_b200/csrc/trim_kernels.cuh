@@ -529,10 +529,16 @@ __device__ __forceinline__ float list_lower_bound(float dq, float R, float xmin,
 // so stream position pp is entry tab[pp] and the pipeline below runs unchanged.
 // A CTA whose record is of the other mode exits at once (both kernels are
 // launched over the batch).
-template <int M, int KS, int S, bool PRE, bool SEG = false>
+//
+// HARD (with PRE, without SEG): the launch for the records whose bit 8 is set — the
+// list-level bound dropped at least 3/4 of the stream, so what is left are the lists
+// around the query, every candidate is near the threshold and the ADC runs without
+// early-exit stages (StageNone); the other records are served by the HARD = false launch.
+template <int M, int KS, int S, bool PRE, bool SEG = false, bool HARD = false>
 __global__ void __launch_bounds__(knn_threads(M), knn_min_blocks(M))
 trim_knn_kernel(DevIndex ix, KnnParams p) {
     static_assert(PRE || !SEG, "segmented streams come from a plan record");
+    static_assert(!HARD || (PRE && !SEG), "HARD is a flavour of the PRE kernel");
     // this instantiation's CTA shape (knn_warps): warp 0 replays, the rest filter
     constexpr uint32_t kThreads = knn_threads(M);
     constexpr uint32_t kWorkers = knn_warps(M) - 1;
@@ -541,8 +547,9 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
     const uint32_t q = blockIdx.x;
     if (q >= p.nq)
         return;
-    if constexpr (PRE) { // a record of another launch's mode: nothing to do here
-        if (__ldg(p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words + 7) != (SEG ? 1u : p.mode_sel))
+    if constexpr (PRE) { // a record of another launch's mode or flavour: nothing to do here
+        const uint32_t md = __ldg(p.plan + static_cast<size_t>(q) * KnnPlanLayout::of(p.np, p.k).words + 7);
+        if ((md & 0xffu) != (SEG ? 1u : p.mode_sel) || (!SEG && ((md >> 8) & 1u) != (HARD ? 1u : 0u)))
             return;
     }
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -923,8 +930,13 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         const uint32_t g0 = s * kChunkW + w * kPerWorker;
         Cand& x = cur.c[0];
 #if TRIM_STAGE_CUT
-        const StageCut ck = StageCut::make(x.lx, p.stage_c1, p.omg_hi, p.stage_ka, T);
-        const float a = x.fc.template sum_staged<true, StageCut>(m, la, ck, x.kind == 2u); // warp-collective
+        float a; // warp-collective
+        if constexpr (HARD) { // every candidate is near the threshold: no early-exit stages
+            a = x.fc.template sum_staged<true, StageNone>(m, la, StageNone{}, x.kind == 2u);
+        } else {
+            const StageCut ck = StageCut::make(x.lx, p.stage_c1, p.omg_hi, p.stage_ka, T);
+            a = x.fc.template sum_staged<true, StageCut>(m, la, ck, x.kind == 2u);
+        }
 #else
         const StageCheck ck{x.lx, p.two_gamma, p.omg_hi, p.adc_eps, T};
         const float a = x.fc.sum_staged(m, la, ck, x.kind == 2u); // warp-collective
@@ -1429,8 +1441,10 @@ __global__ void __launch_bounds__(kWarp) trim_knn_setup_kernel(DevIndex ix, KnnP
         rec[4] = __float_as_uint(T0);
         rec[5] = nseed; // dc so far
         rec[6] = nseed; // evaluated unconditionally
-        rec[7] = 0;     // stream in order
         const uint32_t rest = total - nseed;
+        // stream in order; bit 8: the list-level bound dropped at least 3/4 of it, so what is
+        // left are the lists around the query — no early-exit stages (StageNone)
+        rec[7] = kept && static_cast<uint64_t>(kept) * 4 <= rest ? 0x100u : 0u;
         if (p.skipped && rest != kept)
             atomicAdd(p.skipped, static_cast<unsigned long long>(rest - kept));
     }
@@ -1510,7 +1524,7 @@ __global__ void __launch_bounds__(kThreads) trim_knn_seg_plan_kernel(DevIndex au
     const uint32_t nb = aux.nlist;
     const KnnPlanLayout lo = KnnPlanLayout::of(p.np, p.k);
     uint32_t* rec = p.recs + q * lo.words;
-    if (p.round && rec[7] == 1u)
+    if (p.round && (rec[7] & 0xffu) == 1u)
         return;
     uint32_t* tab = p.tab + q * p.tab_cap;
     const float* qrow = p.queries + q * aux.dim_stride;

@@ -352,6 +352,14 @@ def run_ours(args, cfg):
     n_probe_k = C.c_uint32(0)
     _lib.check(lib.trim_probe_launches(gix.handle, cfg["nprobe"], C.byref(n_probe_k)), "probe_launches")
     setup_k = 1 if cfg["nlist"] > 1 and os.environ.get("TRIM_KNN_SETUP") != "0" else 0
+    # flat kNN launches per batch. In-order scan: the filter kernel (+ query tiles, norms and the
+    # tcgen05 bounds up to 16M rows). Segmented block stream (>= 64k rows, DESIGN 4.6b; a batch of
+    # at most 2,048 queries): the in-order prefix, the block bounds (tcgen05), 1 + 3 plan
+    # launches, 3 continue-round launches, the in-order and the table-driven resume
+    seg_on = (cfg["nlist"] == 1 and cfg["n"] >= 65536 and cfg["dim"] <= 128
+              and os.environ.get("TRIM_FLAT_SEGMENTS") != "0" and os.environ.get("TRIM_FLAT_PARTITION") != "0")
+    bounds_k = 3 if cfg["nlist"] == 1 and cfg["n"] <= (16 << 20) and os.environ.get("TRIM_FLAT_BOUNDS") != "0" else 0
+    filter_k = (11 if seg_on else 1) + bounds_k
 
     def step(gamma, filt_events=None):
         launches = 0
@@ -386,8 +394,9 @@ def run_ours(args, cfg):
                 gix.handle, p(queries, qoff), nb, k, p(lists, b0 * np_eff * 4), np_eff,
                 float(np.float32(gamma)), p(ids, b0 * k * 4), p(dists, b0 * k * 4),
                 p(cts, b0 * 48), p(status), sh_), "knn")
-            # the filter kernel, plus trim_knn_setup_kernel (seeds + plan) on IVF indexes
-            launches += 1 + setup_k
+            # IVF: trim_knn_setup_kernel (seeds + plan) and the filter kernel's two flavours (with
+            # and without early-exit stages, each CTA runs in one of them); flat: filter_k below
+            launches += (2 + setup_k) if setup_k else filter_k
             if filt_events is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(st_)

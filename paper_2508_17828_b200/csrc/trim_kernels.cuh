@@ -363,6 +363,9 @@ constexpr uint32_t kRing = TRIM_KRING;             // chunk buffers in flight
 #ifndef TRIM_STAGE_CUT
 #define TRIM_STAGE_CUT 1   // kNN workers: one-compare stage tests every 8 lookups (StageCut); 0: StageCheck
 #endif
+#ifndef TRIM_SEG_NOSTAGE
+#define TRIM_SEG_NOSTAGE 0 // 1: the table-driven flat kernel (SEG) also runs without stages (spills at m = 48)
+#endif
 #ifndef TRIM_QUAD_L2
 #define TRIM_QUAD_L2 1     // members' exact L2 by lane quads (euclid_sq_quad), 8 rows per warp pass
 #endif
@@ -931,7 +934,7 @@ trim_knn_kernel(DevIndex ix, KnnParams p) {
         Cand& x = cur.c[0];
 #if TRIM_STAGE_CUT
         float a; // warp-collective
-        if constexpr (HARD) { // every candidate is near the threshold: no early-exit stages
+        if constexpr (HARD || (SEG && TRIM_SEG_NOSTAGE)) { // every candidate is near the threshold: no early-exit stages
             a = x.fc.template sum_staged<true, StageNone>(m, la, StageNone{}, x.kind == 2u);
         } else {
             const StageCut ck = StageCut::make(x.lx, p.stage_c1, p.omg_hi, p.stage_ka, T);
